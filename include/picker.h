@@ -1,0 +1,192 @@
+/*
+ * picker.h -- C ABI of the B200-native Picker runtime validator.
+ *
+ * Picker (arXiv 2410.23661) decides, before a GPU kernel instance runs, whether
+ * the instance is idempotent: "an instance is considered non-idempotent if there
+ * exists any overlap in the read and write addresses of all potential memory
+ * accesses, regardless of the access order ... idempotent if Picker can ensure
+ * that each byte of GPU memory is either read-only or write-only"
+ * (§4.1).  The addresses come from per-kernel access
+ * summaries produced offline (symbolic addresses, path conditions and a global
+ * condition, l.690-702) and are evaluated per instance from its launch arguments
+ * and grid/block dimensions (Fig. 3, l.717-730), as ranges [LB, UB] per symbolic
+ * address (l.920-951) with induction-variable compaction (l.1029-1069).
+ *
+ * This library runs that validation for whole batches of launch records on a
+ * B200 (sm_100a).  Python reaches it through ctypes
+ * (paper_2410_23661_b200/_lib.py); nothing here takes a torch type.
+ *
+ * Conventions for every call:
+ *   - Return value: 0 (PICKER_OK) or a negative picker_status; on error a
+ *     message is available from picker_last_error(ctx).
+ *   - "device pointer" = a CUDA global-memory address on the context's device
+ *     (e.g. from torch.empty(..., device="cuda").data_ptr()).  "host pointer" =
+ *     ordinary process memory; pinned memory makes the *_host calls faster.
+ *   - Calls taking a `stream` (a cudaStream_t; NULL = legacy default stream)
+ *     only ENQUEUE work and return: outputs are valid after the stream is
+ *     synchronised.  Inputs must stay valid and unmodified until then.
+ *   - The caller owns every buffer it passes; the context owns its device
+ *     summary tables and scratch until picker_destroy.
+ *   - Thread safety: one context per host thread.  Loaded tables are immutable
+ *     until the next picker_load_summaries on the same context.
+ */
+#ifndef PICKER_H_
+#define PICKER_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+typedef enum {
+  PICKER_OK = 0,
+  PICKER_EINVAL = -1,     /* null / misaligned pointer, n > 2^40, bad option  */
+  PICKER_EFORMAT = -2,    /* summary text is not valid IR      */
+  PICKER_EUNSAFE = -3,    /* summary fails the loader's soundness checks:      */
+                          /* an operand without a precondition bound, possible */
+                          /* int64 wrap, mixed-sign terms on one variable, a   */
+                          /* fresh range not covering its definition (§6)      */
+  PICKER_ENOTLOADED = -4, /* no summaries loaded yet                          */
+  PICKER_ECUDA = -5,      /* a CUDA runtime / NVRTC call failed               */
+  PICKER_ENOMEM = -6      /* device or host allocation failed                 */
+} picker_status;
+
+/* ---- verdict codes (one byte per record) -------------------
+ * Precedence, first match wins (Fig. 3 order, l.721-730):
+ *   0xFF unknown kernel id; 0xFE nargs != param count or args out of range;
+ *   1 kernel-level idempotent (write-only kernel, l.769-770, l.1469-1470);
+ *   2..6 kernel-level non-idempotent SO/ATOMIC/IF/PE/NA (l.771-773, Table 4);
+ *   7 a precondition or a CUDA launch limit fails (l.976-979);
+ *   8 the global condition fails (unbounded loops, l.743-752);
+ *   9 an active non-parameter (opaque) address meets an active access of the
+ *     other kind (l.761-765);
+ *   10 an active read extent and an active write extent share a byte (l.658-666);
+ *   0 idempotent (checked).
+ * picker_exact_check only: 11 = more points than max_points_per_instance.   */
+enum {
+  PICKER_IDEM_CHECKED = 0,
+  PICKER_IDEM_KERNEL = 1,
+  PICKER_NI_KERNEL_SO = 2,
+  PICKER_NI_KERNEL_ATOMIC = 3,
+  PICKER_NI_KERNEL_IF = 4,
+  PICKER_NI_KERNEL_PE = 5,
+  PICKER_NI_KERNEL_NA = 6,
+  PICKER_NI_PRECOND = 7,
+  PICKER_NI_GLOBAL = 8,
+  PICKER_NI_OPAQUE = 9,
+  PICKER_NI_OVERLAP = 10,
+  PICKER_EXACT_SKIPPED = 11,
+  PICKER_ERR_ARITY = 0xFE,
+  PICKER_ERR_KERNEL = 0xFF
+};
+/* counts_out[c] for c in 0..11; every 0xFE / 0xFF record is counted in [15]. */
+#define PICKER_NUM_COUNTS 16
+
+/* ---- launch records: 32 bytes, little-endian --------------
+ * An instance = kernel identity + launch arguments + grid/block dims
+ * (PAPER.md l.88).  Argument i of record r is args[rec[r].arg_off + i]; i32
+ * parameters use the low 32 bits of their slot, sign-extended.              */
+typedef struct {
+  uint32_t kernel_id;
+  uint32_t nargs;
+  uint32_t grid_x;
+  uint16_t grid_y, grid_z;
+  uint16_t block_x, block_y, block_z, reserved;
+  uint64_t arg_off;
+} picker_rec_t;
+
+/* A batch.  `rec` (16-byte aligned) and `args` (8-byte aligned) point to
+ * n records and args_len int64 slots.  In picker_validate_batch /
+ * picker_exact_check they are DEVICE pointers; in the *_host calls HOST
+ * pointers.  args_packed = 1 promises arg_off[i+1] = arg_off[i] + nargs[i]
+ * (lets the kernels stream args contiguously); 0 makes no promise.          */
+typedef struct {
+  const picker_rec_t* rec;
+  const int64_t* args;
+  uint64_t args_len;
+  uint32_t args_packed;
+  uint32_t reserved;
+} picker_batch_t;
+
+typedef struct picker_ctx picker_ctx_t;
+
+/* Create a context on CUDA device `device` (>= 0).  *ctx receives the handle. */
+int picker_create(picker_ctx_t** ctx, int device);
+
+/* Destroy a context and free its device tables (after its streams are idle). */
+void picker_destroy(picker_ctx_t* ctx);
+
+/* Last error message of this context ("" if none).  Valid until the next call
+ * on the context.  ctx may be NULL (returns the last create error).          */
+const char* picker_last_error(const picker_ctx_t* ctx);
+
+/* Load the per-kernel access summaries: `text` is `len` bytes of UTF-8 JSON in
+ * the summary IR (kernels, params, class, pre, glob, desc with
+ * guard / vars / terms) -- the analyzer output the validator loads at runtime
+ * (PAPER.md l.628-629, l.690-702).  The text is copied; the caller may free it.
+ * The loader verifies the summaries and flattens them into
+ * device tables (synchronously; not on the per-record clock).  Replaces any
+ * previously loaded set.  Returns the number of kernels (>= 0) or an error.  */
+int picker_load_summaries(picker_ctx_t* ctx, const char* text, size_t len);
+
+/* Parse and verify summaries without a device (no context needed): the same
+ * checks as picker_load_summaries.  Returns the kernel count or an error; the
+ * message (NUL-terminated, truncated to msg_len) goes to msg when non-NULL. */
+int picker_verify_summaries(const char* text, size_t len, char* msg, size_t msg_len);
+
+/* Validate n launch records (device pointers) on `stream` (Fig. 3 with the
+ * range model of §5.1-5.3).  Outputs (device pointers, caller-owned):
+ *   flags_out[n]            one verdict code per record (required);
+ *   idem_bits_out[ceil(n/32)] bit (r % 32) of word r/32 = 1 iff record r is
+ *                            idempotent (code 0 or 1); NULL to skip;
+ *   counts_out[16]          per-code histogram (overwritten, not
+ *                            accumulated); NULL to skip.
+ * Bad records are not call errors: they get codes 0xFE / 0xFF.               */
+int picker_validate_batch(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
+                          uint8_t* flags_out, uint32_t* idem_bits_out,
+                          uint64_t* counts_out, void* stream);
+
+/* Same as picker_validate_batch, but batch->rec / batch->args and the outputs
+ * are HOST pointers.  The call copies the inputs to the device, validates, and
+ * copies the outputs back, pipelined in chunks on `stream` and one internal
+ * stream; it returns after the outputs are in host memory (synchronous).     */
+int picker_validate_batch_host(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
+                               uint8_t* flags_out, uint32_t* idem_bits_out,
+                               uint64_t* counts_out, void* stream);
+
+/* Exact verifier (the paper's strawman, Fig. 3 / l.717-730): identical to
+ * picker_validate_batch except that the read/write test enumerates every
+ * point (thread, induction and fresh variable) of every active symbolic
+ * address and intersects the touched BYTES, so it has no range
+ * overestimation (l.1170-1185).  Records with more than
+ * max_points_per_instance points get code 11.  exact_out[n] and counts_out[16]
+ * are device pointers (counts_out nullable).  Intended for small grids.     */
+int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
+                       uint8_t* exact_out, uint64_t* counts_out,
+                       uint64_t max_points_per_instance, void* stream);
+
+/* Number of kernels loaded and the path each kernel was compiled to
+ * (per-kernel introspection for tests): path_out[i] for kernel id ids_out[i];
+ * path 0 = shortcut, 1 = generic table path, 2 = specialised (JIT) path,
+ * 3 = wide (sort + sweep) path.  Either array may be NULL; cap bounds both.  */
+int picker_kernel_info(picker_ctx_t* ctx, uint32_t* ids_out, uint8_t* path_out, uint32_t cap);
+
+/* Tuning options (semantics never depend on them).  Keys:
+ *   "jit"          0 = table-driven kernels only, 1 = NVRTC-specialised (default 1)
+ *   "wide_pairs"   R*W pair count above which a kernel uses the wide path
+ *   "force_path"   0 = automatic, 1 = generic, 2 = jit, 3 = wide
+ *   "tile"         records per CTA super-tile in the specialised kernel
+ * Takes effect at the next picker_load_summaries.                            */
+int picker_set_option(picker_ctx_t* ctx, const char* key, int64_t value);
+
+/* Per-kernel-launch statistics of the last validate call: number of device
+ * kernels this library launched (for the bench's gpu_launches).             */
+int picker_last_launch_count(const picker_ctx_t* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PICKER_H_ */

@@ -54,8 +54,8 @@ DIM_MAX = {"gdim.x": 2**31 - 1, "gdim.y": 65535, "gdim.z": 65535,
            "bdim.x": 1024, "bdim.y": 1024, "bdim.z": 64}
 BLOCK_MAX_THREADS = 1024
 
-BRUTE_BOX_POINTS = 1 << 12   # whole-box enumeration below this many points
-BRUTE_VAR_POINTS = 1 << 12   # per-variable enumeration below this range size
+BRUTE_BOX_POINTS = 1 << 8    # whole-box enumeration below this many points
+BRUTE_VAR_POINTS = 1 << 8    # per-variable enumeration below this range size
 
 
 class OracleUnsupported(Exception):
@@ -372,3 +372,24 @@ def oracle_batch(summary, rec_array, args, fn=oracle_interval, **kw):
     """Apply fn to every record of a packed batch; returns a list of codes."""
     kernels = index_summary(summary)
     return [fn(kernels, decode_record(r, args), **kw) for r in rec_array]
+
+
+def _mp_chunk(job):
+    summary, rec, args, fn_name, kw = job
+    return oracle_batch(summary, rec, args, globals()[fn_name], **kw)
+
+
+def oracle_batch_mp(summary, rec_array, args, fn=oracle_interval, processes=None, **kw):
+    """oracle_batch over a multiprocessing pool (same results, more cores)."""
+    import multiprocessing as mp
+    import os
+
+    processes = processes or os.cpu_count() or 1
+    n = len(rec_array)
+    if processes <= 1 or n < 256:
+        return oracle_batch(summary, rec_array, args, fn, **kw)
+    step = (n + processes * 4 - 1) // (processes * 4)
+    jobs = [(summary, rec_array[i:i + step], args, fn.__name__, kw) for i in range(0, n, step)]
+    with mp.get_context("forkserver").Pool(processes) as pool:
+        parts = pool.map(_mp_chunk, jobs)
+    return [c for p in parts for c in p]

@@ -1,0 +1,110 @@
+// Device helpers shared by the validation kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/picker.h"
+#include "tables.hpp"
+
+namespace picker {
+
+// Wrapping 64-bit arithmetic (the loader proves no wrap happens on records
+// that pass their checks; unsigned ops keep the other cases defined).
+__device__ __forceinline__ int64_t mul64(int64_t a, int64_t b) {
+  return (int64_t)((uint64_t)a * (uint64_t)b);
+}
+__device__ __forceinline__ int64_t add64(int64_t a, int64_t b) {
+  return (int64_t)((uint64_t)a + (uint64_t)b);
+}
+__device__ __forceinline__ int64_t min64(int64_t a, int64_t b) { return a < b ? a : b; }
+__device__ __forceinline__ int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
+__device__ __forceinline__ int64_t floordiv64(int64_t x, uint32_t d) {
+  if (d == 1) return x;
+  int64_t q = x / (int64_t)d;
+  if ((q * (int64_t)d != x) && x < 0) --q;
+  return q;
+}
+__device__ __forceinline__ bool cmp64(int64_t a, uint8_t op, int64_t b) {
+  switch (op) {
+    case CMP_LT: return a < b;
+    case CMP_LE: return a <= b;
+    case CMP_GT: return a > b;
+    case CMP_GE: return a >= b;
+    case CMP_EQ: return a == b;
+    default: return a != b;
+  }
+}
+
+__device__ __forceinline__ picker_rec_t load_rec(const picker_rec_t* p) {
+  const uint4* q = reinterpret_cast<const uint4*>(p);
+  uint4 a = __ldg(q), b = __ldg(q + 1);
+  picker_rec_t r;
+  r.kernel_id = a.x;
+  r.nargs = a.y;
+  r.grid_x = a.z;
+  r.grid_y = (uint16_t)(a.w & 0xFFFF);
+  r.grid_z = (uint16_t)(a.w >> 16);
+  r.block_x = (uint16_t)(b.x & 0xFFFF);
+  r.block_y = (uint16_t)(b.x >> 16);
+  r.block_z = (uint16_t)(b.y & 0xFFFF);
+  r.reserved = (uint16_t)(b.y >> 16);
+  r.arg_off = ((uint64_t)b.w << 32) | b.z;
+  return r;
+}
+
+// Record's args lie inside the pool and match the kernel's arity.
+__device__ __forceinline__ bool args_in_range(const picker_rec_t& r, uint32_t nparams,
+                                              uint64_t lo, uint64_t hi) {
+  return r.nargs == nparams && r.arg_off >= lo && r.arg_off <= hi &&
+         (uint64_t)r.nargs <= hi - r.arg_off;
+}
+
+struct RecVals {
+  int64_t d[6];
+  const int64_t* __restrict__ a;
+  const uint32_t* m;
+  __device__ __forceinline__ RecVals(const picker_rec_t& r, const int64_t* __restrict__ args,
+                                     const uint32_t* i32mask)
+      : a(args + r.arg_off), m(i32mask) {
+    d[0] = r.grid_x, d[1] = r.grid_y, d[2] = r.grid_z;
+    d[3] = r.block_x, d[4] = r.block_y, d[5] = r.block_z;
+  }
+  __device__ __forceinline__ int64_t get(uint8_t op) const {
+    if (op < 6) return d[op];
+    if (op == OPD_ONE) return 1;
+    if (op == OPD_NONE) return 0;
+    const int i = op - OPD_ARG0;
+    int64_t v = __ldg(a + i);
+    if ((m[i >> 5] >> (i & 31)) & 1u) v = (int64_t)(int32_t)(uint32_t)v;
+    return v;
+  }
+};
+
+// CUDA launch limits as implicit preconditions (Q21).
+__device__ __forceinline__ bool launch_limits_ok(const RecVals& X) {
+  // grid.x <= 2^31-1, grid.y,z <= 65535, block.x,y <= 1024, block.z <= 64
+  // (kDimMax); the header fields are unsigned, so only the lower bound and the
+  // fields wider than their limit need a test.
+  if (X.d[0] < 1 || X.d[0] > 2147483647LL || X.d[1] < 1 || X.d[2] < 1) return false;
+  if (X.d[3] < 1 || X.d[3] > 1024 || X.d[4] < 1 || X.d[4] > 1024 || X.d[5] < 1 || X.d[5] > 64)
+    return false;
+  return X.d[3] * X.d[4] * X.d[5] <= kBlockMaxThreads;
+}
+
+__device__ __forceinline__ int count_bin(uint8_t code) { return code <= 11 ? code : 15; }
+
+// Epilogue: u8 code, ballot-packed idempotent bit, histogram.
+// Lane 0 of each warp must hold a record index that is a multiple of 32.
+__device__ __forceinline__ void emit(uint64_t i, bool valid, uint8_t code, uint8_t* flags,
+                                     uint32_t* bits, unsigned int* hist) {
+  const unsigned bal = __ballot_sync(0xffffffffu, valid && code <= V_IDEM_KERNEL);
+  if (valid) {
+    flags[i] = code;
+    atomicAdd(hist + count_bin(code), 1u);
+  }
+  if (bits && (threadIdx.x & 31) == 0 && valid) bits[i >> 5] = bal;
+}
+
+}  // namespace picker

@@ -1,0 +1,382 @@
+// C ABI (include/picker.h): context, summary loading, batch validation.
+#include "../../include/picker.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "launch.hpp"
+#include "loader.hpp"
+
+using namespace picker;
+
+struct picker_ctx {
+  int device = 0;
+  int num_sms = 148;
+  std::string err;
+  bool loaded = false;
+  std::vector<IrKernel> ir;
+  HostTables ht;
+  void* dev_tables = nullptr;
+  size_t dev_tables_bytes = 0;
+  Tables T{};
+  Options opt;
+  JitModule* jit = nullptr;
+  // host-path staging (two pipelines)
+  void* stage[2] = {nullptr, nullptr};
+  size_t stage_bytes[2] = {0, 0};
+  unsigned long long* dev_counts = nullptr;
+  cudaStream_t aux = nullptr;
+  int last_launches = 0;
+};
+
+static std::string g_create_err;
+
+namespace {
+
+struct DevGuard {
+  int prev = -1;
+  bool ok = true;
+  explicit DevGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+  }
+  ~DevGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+int fail(picker_ctx* c, int status, const std::string& m) {
+  if (c) c->err = m;
+  return status;
+}
+
+int cuda_fail(picker_ctx* c, cudaError_t e, const char* where) {
+  return fail(c, PICKER_ECUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+template <class T>
+size_t append_bytes(std::vector<uint8_t>& blob, const std::vector<T>& v) {
+  size_t off = (blob.size() + 255) & ~(size_t)255;
+  blob.resize(off + v.size() * sizeof(T));
+  if (!v.empty()) memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+int check_batch(picker_ctx* c, const picker_batch_t* b, uint64_t n, const void* out) {
+  if (!c) return PICKER_EINVAL;
+  if (!b || (!out && n)) return fail(c, PICKER_EINVAL, "null batch or output pointer");
+  if (n > (1ULL << 40)) return fail(c, PICKER_EINVAL, "n > 2^40");
+  if (n && (!b->rec || ((uintptr_t)b->rec & 15)))
+    return fail(c, PICKER_EINVAL, "records must be non-null and 16-byte aligned");
+  if (b->args_len && (!b->args || ((uintptr_t)b->args & 7)))
+    return fail(c, PICKER_EINVAL, "args must be non-null and 8-byte aligned");
+  if (!c->loaded) return fail(c, PICKER_ENOTLOADED, "no summaries loaded");
+  return PICKER_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int picker_create(picker_ctx_t** out, int device) {
+  if (!out) return PICKER_EINVAL;
+  *out = nullptr;
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || device < 0 || device >= count) {
+    g_create_err = e != cudaSuccess ? std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e)
+                                    : "device index out of range";
+    return e != cudaSuccess ? PICKER_ECUDA : PICKER_EINVAL;
+  }
+  picker_ctx* c = new (std::nothrow) picker_ctx();
+  if (!c) return PICKER_ENOMEM;
+  c->device = device;
+  DevGuard g(device);
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  *out = c;
+  return PICKER_OK;
+}
+
+void picker_destroy(picker_ctx_t* c) {
+  if (!c) return;
+  {
+    DevGuard g(c->device);
+    if (c->dev_tables) cudaFree(c->dev_tables);
+    for (int i = 0; i < 2; ++i)
+      if (c->stage[i]) cudaFree(c->stage[i]);
+    if (c->dev_counts) cudaFree(c->dev_counts);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    jit_destroy(c->jit);
+  }
+  delete c;
+}
+
+const char* picker_last_error(const picker_ctx_t* c) {
+  return c ? c->err.c_str() : g_create_err.c_str();
+}
+
+int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
+  if (!c || !key) return PICKER_EINVAL;
+  std::string k(key);
+  if (k == "jit") c->opt.jit = v != 0;
+  else if (k == "wide_pairs") c->opt.wide_pairs = v;
+  else if (k == "force_path") c->opt.force_path = (int)v;
+  else if (k == "tile") c->opt.tile = (int)v;
+  else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
+  return PICKER_OK;
+}
+
+int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
+  if (!c) return PICKER_EINVAL;
+  if (!text && len) return fail(c, PICKER_EINVAL, "null summary text");
+  DevGuard g(c->device);
+  if (!g.ok) return fail(c, PICKER_ECUDA, "cudaSetDevice failed");
+  std::vector<IrKernel> ks;
+  HostTables ht;
+  try {
+    ks = parse_summaries(text, len);
+    for (auto& k : ks) verify_kernel(k);
+    select_paths(ks, c->opt);
+    flatten(ks, ht);
+  } catch (const LoadError& e) {
+    return fail(c, e.status, e.msg);
+  } catch (const std::exception& e) {
+    return fail(c, PICKER_EFORMAT, e.what());
+  }
+  // one device allocation for all tables
+  std::vector<uint8_t> blob;
+  size_t o_k = append_bytes(blob, ht.kernels), o_c = append_bytes(blob, ht.checks),
+         o_p = append_bytes(blob, ht.prods), o_b = append_bytes(blob, ht.bexprs),
+         o_v = append_bytes(blob, ht.vars), o_t = append_bytes(blob, ht.terms),
+         o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
+         o_l = append_bytes(blob, ht.varlist);
+  blob.resize(blob.size() + 256);
+  void* dev = nullptr;
+  cudaError_t e = cudaMalloc(&dev, blob.size());
+  if (e != cudaSuccess) return fail(c, PICKER_ENOMEM, "cudaMalloc(tables) failed");
+  e = cudaMemcpy(dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(dev);
+    return cuda_fail(c, e, "cudaMemcpy(tables)");
+  }
+  JitModule* jm = nullptr;
+  std::string jerr;
+  if (c->opt.jit && any_jit(ks)) {
+    jm = jit_build(ks, c->opt, jerr);
+    if (!jm) {
+      cudaFree(dev);
+      return fail(c, PICKER_ECUDA, "JIT: " + jerr);
+    }
+  }
+  if (c->dev_tables) cudaFree(c->dev_tables);
+  jit_destroy(c->jit);
+  c->jit = jm;
+  c->dev_tables = dev;
+  c->dev_tables_bytes = blob.size();
+  uint8_t* b = (uint8_t*)dev;
+  c->T.kernels = (const DKernel*)(b + o_k);
+  c->T.nkernel_slots = (uint32_t)ht.kernels.size();
+  c->T.checks = (const DCheck*)(b + o_c);
+  c->T.prods = (const DProd*)(b + o_p);
+  c->T.bexprs = (const DBexpr*)(b + o_b);
+  c->T.vars = (const DVar*)(b + o_v);
+  c->T.terms = (const DTerm*)(b + o_t);
+  c->T.guards = (const DGuard*)(b + o_g);
+  c->T.descs = (const DDesc*)(b + o_d);
+  c->T.varlist = (const uint16_t*)(b + o_l);
+  c->ir = std::move(ks);
+  c->ht = std::move(ht);
+  c->loaded = true;
+  c->err.clear();
+  return (int)c->ir.size();
+}
+
+int picker_verify_summaries(const char* text, size_t len, char* msg, size_t msg_len) {
+  auto put = [&](const std::string& m) {
+    if (msg && msg_len) {
+      size_t k = std::min(m.size(), msg_len - 1);
+      memcpy(msg, m.data(), k);
+      msg[k] = 0;
+    }
+  };
+  if (!text && len) {
+    put("null summary text");
+    return PICKER_EINVAL;
+  }
+  try {
+    std::vector<IrKernel> ks = parse_summaries(text, len);
+    for (auto& k : ks) verify_kernel(k);
+    put("");
+    return (int)ks.size();
+  } catch (const LoadError& e) {
+    put(e.msg);
+    return e.status;
+  } catch (const std::exception& e) {
+    put(e.what());
+    return PICKER_EFORMAT;
+  }
+}
+
+int picker_kernel_info(picker_ctx_t* c, uint32_t* ids, uint8_t* paths, uint32_t cap) {
+  if (!c) return PICKER_EINVAL;
+  if (!c->loaded) return fail(c, PICKER_ENOTLOADED, "no summaries loaded");
+  uint32_t n = 0;
+  for (auto& k : c->ir) {
+    if (n < cap) {
+      if (ids) ids[n] = k.id;
+      if (paths) paths[n] = k.path;
+    }
+    ++n;
+  }
+  return (int)n;
+}
+
+int picker_last_launch_count(const picker_ctx_t* c) { return c ? c->last_launches : 0; }
+
+int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* flags,
+                          uint32_t* bits, uint64_t* counts, void* stream) {
+  int st = check_batch(c, b, n, flags);
+  if (st) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  c->last_launches = 0;
+  if (counts) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
+  }
+  DevBatch db{b->rec, b->args, 0, b->args_len};
+  cudaError_t e = launch_validate(c->T, c->jit, c->opt, db, n, flags, bits,
+                                  (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
+  if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
+  return PICKER_OK;
+}
+
+int picker_validate_batch_host(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
+                               uint8_t* flags, uint32_t* bits, uint64_t* counts, void* stream) {
+  int st = check_batch(c, b, n, flags);
+  if (st) return st;
+  DevGuard g(c->device);
+  cudaError_t e;
+  cudaStream_t s[2] = {(cudaStream_t)stream, nullptr};
+  if (!c->aux) {
+    e = cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamCreate");
+  }
+  s[1] = c->aux;
+  if (!c->dev_counts) {
+    e = cudaMalloc(&c->dev_counts, PICKER_NUM_COUNTS * sizeof(uint64_t));
+    if (e != cudaSuccess) return fail(c, PICKER_ENOMEM, "cudaMalloc(counts)");
+  }
+  c->last_launches = 0;
+  // Both pipelines start after anything already queued on the caller's stream.
+  cudaEvent_t ev0;
+  cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming);
+  e = cudaMemsetAsync(c->dev_counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s[0]);
+  cudaEventRecord(ev0, s[0]);
+  cudaStreamWaitEvent(s[1], ev0, 0);
+  cudaEventDestroy(ev0);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync");
+
+  const bool packed = b->args_packed != 0;
+  const uint64_t CH = 1ULL << 22;  // records per chunk (multiple of 32)
+  const int64_t* whole_args = nullptr;
+  if (!packed && b->args_len) {
+    // no contiguity promise: copy the whole pool once into pipeline 1's buffer
+    size_t need = b->args_len * 8;
+    if (c->stage_bytes[1] < need) {
+      if (c->stage[1]) cudaFree(c->stage[1]);
+      c->stage[1] = nullptr;
+      c->stage_bytes[1] = 0;
+      if (cudaMalloc(&c->stage[1], need) != cudaSuccess) return fail(c, PICKER_ENOMEM, "staging");
+      c->stage_bytes[1] = need;
+    }
+    e = cudaMemcpyAsync(c->stage[1], b->args, need, cudaMemcpyHostToDevice, s[0]);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D args");
+    whole_args = (const int64_t*)c->stage[1];
+    s[1] = s[0];  // single pipeline
+  }
+  for (uint64_t c0 = 0, k = 0; c0 < n; c0 += CH, ++k) {
+    const uint64_t m = std::min(CH, n - c0);
+    const int p = packed ? (int)(k & 1) : 0;
+    cudaStream_t ss = s[p];
+    uint64_t lo = 0, hi = b->args_len;
+    if (packed && b->args_len) {
+      lo = std::min<uint64_t>(b->rec[c0].arg_off, b->args_len);
+      const picker_rec_t& last = b->rec[c0 + m - 1];
+      hi = std::min<uint64_t>(b->args_len, last.arg_off + last.nargs);
+      if (hi < lo) hi = lo;
+    }
+    const size_t rec_b = m * sizeof(picker_rec_t);
+    const size_t arg_b = packed ? (hi - lo) * 8 : 0;
+    const size_t flag_b = (m + 255) & ~(size_t)255, bits_b = ((m + 31) / 32) * 4;
+    const size_t need = rec_b + ((arg_b + 255) & ~(size_t)255) + flag_b + bits_b + 256;
+    if (c->stage_bytes[p] < need || (!packed && p == 0 && c->stage[0] == nullptr)) {
+      cudaStreamSynchronize(ss);
+      if (c->stage[p]) cudaFree(c->stage[p]);
+      c->stage[p] = nullptr;
+      c->stage_bytes[p] = 0;
+      size_t want = std::max(need, (size_t)(CH * 100));
+      if (cudaMalloc(&c->stage[p], want) != cudaSuccess) return fail(c, PICKER_ENOMEM, "staging");
+      c->stage_bytes[p] = want;
+    }
+    uint8_t* base = (uint8_t*)c->stage[p];
+    picker_rec_t* d_rec = (picker_rec_t*)base;
+    int64_t* d_args = (int64_t*)(base + rec_b);
+    uint8_t* d_flags = base + rec_b + ((arg_b + 255) & ~(size_t)255);
+    uint32_t* d_bits = (uint32_t*)(d_flags + flag_b);
+    e = cudaMemcpyAsync(d_rec, b->rec + c0, rec_b, cudaMemcpyHostToDevice, ss);
+    if (e == cudaSuccess && arg_b)
+      e = cudaMemcpyAsync(d_args, b->args + lo, arg_b, cudaMemcpyHostToDevice, ss);
+    if (e != cudaSuccess) return cuda_fail(c, e, "H2D");
+    DevBatch db = packed ? DevBatch{d_rec, d_args - lo, lo, hi}
+                         : DevBatch{d_rec, whole_args, 0, b->args_len};
+    int launches = 0;
+    e = launch_validate(c->T, c->jit, c->opt, db, m, d_flags, bits ? d_bits : nullptr,
+                        c->dev_counts, c->num_sms, ss, &launches);
+    if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
+    c->last_launches += launches;
+    e = cudaMemcpyAsync(flags + c0, d_flags, m, cudaMemcpyDeviceToHost, ss);
+    if (e == cudaSuccess && bits)
+      e = cudaMemcpyAsync(bits + c0 / 32, d_bits, ((m + 31) / 32) * 4, cudaMemcpyDeviceToHost, ss);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H");
+  }
+  if (s[1] != s[0]) {
+    cudaEvent_t ev;
+    cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    cudaEventRecord(ev, s[1]);
+    cudaStreamWaitEvent(s[0], ev, 0);
+    cudaEventDestroy(ev);
+  }
+  if (counts) {
+    e = cudaMemcpyAsync(counts, c->dev_counts, PICKER_NUM_COUNTS * 8, cudaMemcpyDeviceToHost, s[0]);
+    if (e != cudaSuccess) return cuda_fail(c, e, "D2H counts");
+  }
+  e = cudaStreamSynchronize(s[0]);
+  if (e != cudaSuccess) return cuda_fail(c, e, "stream sync");
+  return PICKER_OK;
+}
+
+int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* out,
+                       uint64_t* counts, uint64_t max_points, void* stream) {
+  int st = check_batch(c, b, n, out);
+  if (st) return st;
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (counts) {
+    cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
+  }
+  DevBatch db{b->rec, b->args, 0, b->args_len};
+  std::string err;
+  cudaError_t e = launch_exact(c->T, db, n, out, (unsigned long long*)counts, max_points,
+                               c->num_sms, s, &c->last_launches, err);
+  if (e != cudaSuccess) return cuda_fail(c, e, ("exact check: " + err).c_str());
+  return PICKER_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,122 @@
+// Flattened device tables for the summary IR.
+//
+// The loader (loader.cpp) verifies each kernel summary and flattens it into
+// these structure-of-records arrays, uploaded once per picker_load_summaries.
+// This is the B200 analog of the paper's compiled execution (PAPER.md
+// l.1077-1090): no expression trees on the device, common products shared
+// across terms and bounds (the "common expression extraction" of l.1088-1090),
+// one variable-bound slot per distinct (variable, bound lists) pair.
+#pragma once
+
+#include <cstdint>
+
+namespace picker {
+
+// Operand codes (u8).  X[op] is the value of an operand for one record.
+enum : uint8_t {
+  OPD_GX = 0, OPD_GY = 1, OPD_GZ = 2,  // grid dims
+  OPD_BX = 3, OPD_BY = 4, OPD_BZ = 5,  // block dims
+  OPD_ONE = 6,                         // the constant 1
+  OPD_NONE = 7,
+  OPD_ARG0 = 8                         // argument i -> OPD_ARG0 + i
+};
+constexpr int kMaxParams = 247;
+
+// Structural variable kinds (implicit thread-space bounds).
+enum : uint8_t { SK_NONE = 0, SK_TID = 1, SK_BID = 2, SK_GIDX = 3 };
+enum : uint8_t { CMP_LT = 0, CMP_LE, CMP_GT, CMP_GE, CMP_EQ, CMP_NE };
+enum : uint8_t { KIND_R = 0, KIND_W = 1 };
+
+constexpr uint16_t kNone16 = 0xFFFF;
+
+// Verdict codes (mirror include/picker.h).
+enum : uint8_t {
+  V_IDEM_CHECKED = 0, V_IDEM_KERNEL = 1, V_NI_SO = 2, V_NI_ATOMIC = 3, V_NI_IF = 4,
+  V_NI_PE = 5, V_NI_NA = 6, V_NI_PRECOND = 7, V_NI_GLOBAL = 8, V_NI_OPAQUE = 9,
+  V_NI_OVERLAP = 10, V_EXACT_SKIPPED = 11, V_ERR_ARITY = 0xFE, V_ERR_KERNEL = 0xFF
+};
+
+// Execution paths per kernel.
+enum : uint8_t { PATH_SHORTCUT = 0, PATH_GENERIC = 1, PATH_JIT = 2, PATH_WIDE = 3 };
+
+struct DCheck {   // lo <= X[op] <= hi   (24 B)
+  int64_t lo, hi;
+  uint32_t op, pad;
+};
+
+struct DProd {    // value = k * X[a] * X[b]   (16 B)
+  int64_t k;
+  uint8_t a, b, pad[6];
+};
+
+struct DBexpr {   // value = k0 + P[p0] + P[p1]  (p = kNone16: absent)   (16 B)
+  int64_t k0;
+  uint16_t p0, p1;
+  uint32_t pad;
+};
+
+struct DVar {     // one variable-bound slot   (8 B)
+  uint8_t skind, axis;  // structural bounds (SK_*)
+  uint8_t nlo, nhi;     // declared bexprs: lo list at bex, hi list at bex + nlo
+  uint32_t bex;
+};
+
+struct DTerm {    // contribution C * floor(x / div), C = P[prod]; var = kNone16: constant C   (8 B)
+  uint16_t prod, var;
+  uint32_t div;
+};
+
+struct DGuard {   // X[a] cmp (b == OPD_NONE ? bconst : X[b])   (16 B)
+  int64_t bconst;
+  uint8_t a, cmp, b, pad[5];
+};
+
+struct DDesc {    // one symbolic address (range descriptor)   (24 B)
+  uint8_t kind, opaque, base, nguard;  // base = OPD_NONE: address 0
+  uint8_t nvar, pad0;
+  uint16_t nterm;
+  uint32_t guard;  // index into guards[]
+  uint32_t var;    // index into varlist[] (u16 var-slot ids of this descriptor)
+  uint32_t term;   // index into terms[]
+  uint32_t width;
+};
+
+struct DKernel {  // 64 B
+  uint8_t shortcut;  // 0: evaluate; otherwise the verdict code (1..6, or 0xFF unknown id)
+  uint8_t nparams;
+  uint8_t path;
+  uint8_t pad0;
+  uint16_t npre, nglob;   // checks[check .. check+npre) then glob
+  uint32_t check;
+  uint16_t nprod, nvar;
+  uint32_t prod, var;     // prods[prod..], vars[var..]
+  uint16_t ndesc, nr, nw, pad1;
+  uint32_t desc;
+  uint32_t jit_slot;      // index of the specialised function (PATH_JIT)
+  uint32_t i32mask[6];    // bit i: param i is i32 (sign-extend the low 32 bits); params < 192
+};
+static_assert(sizeof(DKernel) == 64, "DKernel layout");
+
+// Device-side view of all tables (passed by value to kernels).
+struct Tables {
+  const DKernel* kernels;
+  uint32_t nkernel_slots;  // kernel ids are dense indices < nkernel_slots
+  const DCheck* checks;
+  const DProd* prods;
+  const DBexpr* bexprs;
+  const DVar* vars;
+  const DTerm* terms;
+  const DGuard* guards;
+  const DDesc* descs;
+  const uint16_t* varlist;
+};
+
+// Generic-path limits (a kernel beyond them uses the wide path).
+constexpr int kGenMaxDesc = 64;  // per kind
+constexpr int kGenMaxVar = 64;
+
+// Launch-limit preconditions (Q21).
+constexpr int64_t kDimMax[6] = {2147483647LL, 65535, 65535, 1024, 1024, 64};
+constexpr int64_t kBlockMaxThreads = 1024;
+
+}  // namespace picker

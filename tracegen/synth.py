@@ -117,7 +117,9 @@ def random_kernel(rng, kid, *, max_desc=8, max_dim=3, small=True):
     cls, reason = "COND", None
     r = rng.random()
     if r < 0.05:
-        cls = "IDEM"
+        cls = "IDEM"  # write-only kernel
+        for d in descs:
+            d["kind"] = "W"
     elif r < 0.12:
         cls, reason = "NONIDEM", str(rng.choice(REASONS))
     return kernel(kid, f"rk{kid}", params, descs, pre=pre, glob=glob, cls=cls, reason=reason)
