@@ -1,0 +1,366 @@
+"""Benchmark: batched instance-level idempotency validation on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+Workload: the C2 trace shaped like the paper's evaluation
+(547 kernels / 18,217 instances / 6 apps, Table 3) tiled to
+12,495,862 records per GPU (686 replicas, each relocating every pointer by
+r * 2^37; verdicts are translation invariant).  At 8 GPUs that is
+the 100M-instance stream of BASELINE.json's C5.  One step = one
+picker_validate_batch over the rank's whole shard (plus, for N > 1, the NCCL
+all-gather of the bit-packed flags and all-reduce of the counts).  Inputs
+(~0.83 GB per GPU) are 6.6x the 126 MB L2, so no L2 flush is needed between
+steps.
+
+Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle
+(oracle/, test infrastructure) on the host cores on bounded samples of the same
+workload instead.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "validated kernel instances/sec"
+UNIT = "instances/s"
+REPLICAS = 686  # per GPU: 686 x 18,217 = 12,496,862 records (~0.83 GB)
+DELTA = 1 << 37
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--replicas", type=int, default=REPLICAS)
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--oracle-seconds", type=float, default=12.0)
+    ap.add_argument("--path", default="auto", choices=["auto", "generic", "jit"])
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_config(args, world):
+    return {
+        "workload": "C2 paper-shaped trace (547 kernels / 18,217 instances / 6 apps) tiled "
+                    f"x{args.replicas} per GPU with pointer relocation" + (" (C5 stream)" if world > 1 else ""),
+        "records_per_gpu": 18217 * args.replicas,
+        "records_total": 18217 * args.replicas * world,
+        "kernels": 547,
+        "seed": 23661,
+        "l2": "inputs 6.6x L2 per GPU, no flush needed",
+        "parallelism": f"dp{world} (instance shards, all-gather of flag bits)" if world > 1 else "single GPU",
+    }
+
+
+def algorithmic_bytes(rec, args):
+    """Per SURVEY §8 row d: 32-B header + 8*nargs + 1 (code) + 1/8 (bit) per record."""
+    n = len(rec)
+    return 32 * n + 8 * int(rec["nargs"].astype(np.int64).sum()) + n + n / 8.0
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(
+                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                    self.rows.append([x.strip() for x in out.strip().split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.1)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        sm = [float(r[0]) for r in self.rows if len(r) >= 6 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 6 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 6 for i in range(4)
+                          if r[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def build_inputs(args, rank):
+    from tracegen.workloads import make_c2, replicate
+
+    s, rec, a, meta = make_c2()
+    # this rank's replicas: r in [rank*R, (rank+1)*R)
+    R = args.replicas
+    rr, aa = replicate(rec, a, meta["ptr_mask"], R, DELTA)
+    if rank:
+        aa = aa + np.tile(meta["ptr_mask"].astype(np.int64), R) * (rank * R * DELTA)
+    return s, rec, a, meta, rr, aa
+
+
+def cpu_baseline(s, rec, a, seconds):
+    """The oracle as it stands, on this host's cores, over whole C2 copies until
+    `seconds` of wall time are spent."""
+    import oracle.picker_oracle as O
+
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    done = 0
+    copies = 0
+    while time.perf_counter() - t0 < seconds:
+        O.oracle_batch_mp(s, rec, a, processes=cores)
+        done += len(rec)
+        copies += 1
+    dt = time.perf_counter() - t0
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{copies} full copies of the C2 base trace ({len(rec)} records each), "
+                      f"oracle_interval over a {cores}-process pool, {dt:.1f} s"}
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle.picker_oracle as O
+    from tracegen.workloads import make_c2
+
+    s, rec, a, meta = make_c2()
+    cores = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        O.oracle_batch_mp(s, rec[:2048], a, processes=cores)
+    times = []
+    for _ in range(args.steps):
+        t = time.perf_counter()
+        O.oracle_batch_mp(s, rec, a, processes=cores)
+        times.append(time.perf_counter() - t)
+    ms = 1e3 * float(np.median(times))
+    v = len(rec) / (ms / 1e3)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int (exact Python integers)",
+        "data": "synthetic", "config": workload_config(args, world),
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": f"each step: the full C2 base trace ({len(rec)} records), "
+                                   f"{cores}-process pool"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "p50_us_per_instance": 1e3 * ms / len(rec),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2410_23661_b200 as pk
+    from paper_2410_23661_b200 import dist as pdist
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+
+    s, base_rec, base_args, meta, rec, a = build_inputs(args, rank)
+    n = len(rec)
+    opts = {}
+    if args.path == "generic":
+        opts["jit"] = 0
+    p = pk.Picker(local, **opts)
+    p.load(s)
+    paths = p.kernel_paths()
+    rec_d = torch.from_numpy(rec.view(np.uint8).reshape(-1, 32)).to(dev)
+    args_d = torch.from_numpy(a).to(dev)
+    flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    counts = torch.empty(16, dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream()
+    n_total = n * world
+
+    def step():
+        p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
+        if world > 1:
+            pdist.gather_bits(bits, n_total)
+            pdist.reduce_counts(counts)
+
+    # parity of the timed configuration: the base trace's oracle codes, tiled (G9)
+    step()
+    torch.cuda.synchronize()
+    import oracle.picker_oracle as O
+
+    base_codes = np.array(O.oracle_batch_mp(s, base_rec, base_args), np.uint8)
+    got = flags.cpu().numpy()
+    mism = int((got != np.tile(base_codes, args.replicas)).sum())
+    # plus a directly-checked random sample of the relocated records
+    idx = np.random.default_rng(rank).choice(n, size=2000, replace=False)
+    direct = np.array(O.oracle_batch(s, rec[idx], a), np.uint8)
+    mism += int((direct != got[idx]).sum())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = ClockSampler(local)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    kev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    launches = 0
+    torch.cuda.synchronize()
+    t_all0 = torch.cuda.Event(enable_timing=True)
+    t_all1 = torch.cuda.Event(enable_timing=True)
+    t_all0.record(stream)
+    for i in range(args.steps):
+        ev[i][0].record(stream)
+        kev[i][0].record(stream)
+        p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
+        kev[i][1].record(stream)
+        launches += p.last_launch_count()
+        if world > 1:
+            pdist.gather_bits(bits, n_total)
+            pdist.reduce_counts(counts)
+        ev[i][1].record(stream)
+    t_all1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clocks = clk.stop()
+    total_ms = t_all0.elapsed_time(t_all1)
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    kern_ms = [e0.elapsed_time(e1) for e0, e1 in kev]
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        mm = torch.tensor([mism], dtype=torch.int64, device=dev)
+        dist.all_reduce(mm)
+        mism = int(mm.item())
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+
+    # end to end through the public API with host buffers (pinned)
+    e2e = None
+    if args.e2e_steps > 0:
+        rh = torch.from_numpy(rec.view(np.uint8).reshape(-1, 32)).pin_memory()
+        ah = torch.from_numpy(a).pin_memory()
+        fh = torch.empty(n, dtype=torch.uint8).pin_memory()
+        bh = torch.empty((n + 31) // 32, dtype=torch.int32).pin_memory()
+        ch = torch.empty(16, dtype=torch.int64).pin_memory()
+        p.validate_host(rh, ah, out=(fh, bh, ch))
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.e2e_steps):
+            p.validate_host(rh, ah, out=(fh, bh, ch), stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = torch.tensor([e0.elapsed_time(e1) / args.e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / (float(te.item()) / 1e3), "unit": UNIT,
+               "h2d_bytes_per_step": int(rec.nbytes + a.nbytes),
+               "d2h_bytes_per_step": int(n + 4 * ((n + 31) // 32) + 128),
+               "ms_per_step": float(te.item())}
+        e2e_ok = bool((fh.numpy() == got).all())
+        mism += 0 if e2e_ok else 1
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        pass
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    abytes = algorithmic_bytes(rec, a)
+    kmean = float(np.mean(kern_ms))
+    achieved = abytes / (kmean / 1e3) / 1e9
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        cpu = cpu_baseline(s, base_rec, base_args, args.oracle_seconds)
+    codes_hist = counts.cpu().numpy().tolist()
+    line = {
+        "metric": METRIC,
+        "value": n_total / (ms_per_step / 1e3),
+        "unit": UNIT,
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "int64",
+        "data": "synthetic",
+        "config": workload_config(args, world),
+        "p50_us_per_instance": 1e3 * float(np.median(step_ms)) / n,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "kernel_ms": kmean, "algorithmic_bytes_per_launch": abytes,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured)" if peaks else "fallback 6650"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "parity": {"mismatches": mism, "checked": f"all {n} records vs tiled oracle codes of the "
+                                                    f"base trace + 2000 direct oracle samples per rank"},
+        "paths": {k: sum(1 for v in paths.values() if v == k) for k in set(paths.values())},
+        "verdict_counts": codes_hist,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -382,6 +382,7 @@ def _mp_chunk(job):
 def oracle_batch_mp(summary, rec_array, args, fn=oracle_interval, processes=None, **kw):
     """oracle_batch over a multiprocessing pool (same results, more cores)."""
     import multiprocessing as mp
+    import warnings
     import os
 
     processes = processes or os.cpu_count() or 1
@@ -390,6 +391,9 @@ def oracle_batch_mp(summary, rec_array, args, fn=oracle_interval, processes=None
         return oracle_batch(summary, rec_array, args, fn, **kw)
     step = (n + processes * 4 - 1) // (processes * 4)
     jobs = [(summary, rec_array[i:i + step], args, fn.__name__, kw) for i in range(0, n, step)]
-    with mp.get_context("forkserver").Pool(processes) as pool:
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore", DeprecationWarning)
+        pool = mp.get_context("fork").Pool(processes)
+    with pool:
         parts = pool.map(_mp_chunk, jobs)
     return [c for p in parts for c in p]
