@@ -33,8 +33,10 @@
 #ifndef PICKER_H_
 #define PICKER_H_
 
+#ifndef PICKER_NO_LIBC_HEADERS /* defined by the library's NVRTC prelude */
 #include <stddef.h>
 #include <stdint.h>
+#endif
 
 #ifdef __cplusplus
 extern "C" {
@@ -136,6 +138,14 @@ int picker_load_summaries(picker_ctx_t* ctx, const char* text, size_t len);
  * checks as picker_load_summaries.  Returns the kernel count or an error; the
  * message (NUL-terminated, truncated to msg_len) goes to msg when non-NULL. */
 int picker_verify_summaries(const char* text, size_t len, char* msg, size_t msg_len);
+
+/* Generate and compile (NVRTC, sm_100a) the specialised validation module of
+ * these summaries without a device -- the load-time compile of
+ * picker_load_summaries, exposed for build checks.  Returns the number of
+ * distinct specialised functions or an error; msg gets a status line and
+ * src_out (both nullable, NUL-terminated, truncated) the generated CUDA source. */
+int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg_len,
+                             char* src_out, size_t src_len);
 
 /* Validate n launch records (device pointers) on `stream` (Fig. 3 with the
  * range model of §5.1-5.3).  Outputs (device pointers, caller-owned):

@@ -43,6 +43,8 @@ SIGNATURES = {
     "picker_load_summaries": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.c_size_t]),
     "picker_verify_summaries": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p,
                                                ctypes.c_size_t]),
+    "picker_compile_summaries": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_size_t, ctypes.c_char_p,
+                                                ctypes.c_size_t, ctypes.c_char_p, ctypes.c_size_t]),
     "picker_validate_batch": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P, P]),
     "picker_validate_batch_host": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P,
                                                   P]),

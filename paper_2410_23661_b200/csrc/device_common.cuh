@@ -1,9 +1,11 @@
 // Device helpers shared by the validation kernels.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#endif
 
 #include "../../include/picker.h"
 #include "tables.hpp"
@@ -61,13 +63,15 @@ __device__ __forceinline__ bool args_in_range(const picker_rec_t& r, uint32_t np
          (uint64_t)r.nargs <= hi - r.arg_off;
 }
 
+// Operand values of one record.  `a` points at the record's own argument
+// slots: global memory, or the CTA's shared-memory copy (generic pointer).
 struct RecVals {
   int64_t d[6];
-  const int64_t* __restrict__ a;
+  const int64_t* a;
   const uint32_t* m;
-  __device__ __forceinline__ RecVals(const picker_rec_t& r, const int64_t* __restrict__ args,
+  __device__ __forceinline__ RecVals(const picker_rec_t& r, const int64_t* rec_args,
                                      const uint32_t* i32mask)
-      : a(args + r.arg_off), m(i32mask) {
+      : a(rec_args), m(i32mask) {
     d[0] = r.grid_x, d[1] = r.grid_y, d[2] = r.grid_z;
     d[3] = r.block_x, d[4] = r.block_y, d[5] = r.block_z;
   }
@@ -76,7 +80,7 @@ struct RecVals {
     if (op == OPD_ONE) return 1;
     if (op == OPD_NONE) return 0;
     const int i = op - OPD_ARG0;
-    int64_t v = __ldg(a + i);
+    int64_t v = a[i];
     if ((m[i >> 5] >> (i & 31)) & 1u) v = (int64_t)(int32_t)(uint32_t)v;
     return v;
   }
@@ -91,6 +95,13 @@ __device__ __forceinline__ bool launch_limits_ok(const RecVals& X) {
   if (X.d[3] < 1 || X.d[3] > 1024 || X.d[4] < 1 || X.d[4] > 1024 || X.d[5] < 1 || X.d[5] > 64)
     return false;
   return X.d[3] * X.d[4] * X.d[5] <= kBlockMaxThreads;
+}
+
+__device__ __forceinline__ bool launch_limits_ok6(int64_t gx, int64_t gy, int64_t gz, int64_t bx,
+                                                  int64_t by, int64_t bz) {
+  if (gx < 1 || gx > 2147483647LL || gy < 1 || gz < 1) return false;
+  if (bx < 1 || bx > 1024 || by < 1 || by > 1024 || bz < 1 || bz > 64) return false;
+  return bx * by * bz <= kBlockMaxThreads;
 }
 
 __device__ __forceinline__ int count_bin(uint8_t code) { return code <= 11 ? code : 15; }

@@ -9,9 +9,15 @@ namespace picker {
 cudaError_t launch_generic(const Tables& T, const DevBatch& B, uint64_t n, uint8_t* flags,
                            uint32_t* bits, unsigned long long* counts, int num_sms,
                            cudaStream_t s);
-cudaError_t launch_jit(JitModule* m, const Tables& T, const DevBatch& B, uint64_t n,
+cudaError_t launch_bucket_generic(const BucketParams& P, const DevBatch& B, uint64_t n,
+                                  uint8_t* flags, uint32_t* bits, unsigned long long* counts,
+                                  int num_sms, cudaStream_t s);
+cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n,
                        uint8_t* flags, uint32_t* bits, unsigned long long* counts, int num_sms,
-                       cudaStream_t s, int* launches);
+                       cudaStream_t s);
+
+// Largest read x write pair count the specialised path emits as straight-line code.
+constexpr int64_t kJitMaxPairs = 4096;
 
 void select_paths(std::vector<IrKernel>& ks, const Options& opt) {
   for (auto& k : ks) {
@@ -19,18 +25,24 @@ void select_paths(std::vector<IrKernel>& ks, const Options& opt) {
       k.path = PATH_SHORTCUT;
       continue;
     }
-    size_t nr = 0, nw = 0;
-    for (auto& d : k.desc) (d.kind == KIND_R ? nr : nw)++;
-    size_t nvars = 0;
-    for (auto& d : k.desc) nvars += d.vars.size();
+    size_t nr = 0, nw = 0, nvars = 0;
+    for (auto& d : k.desc) {
+      (d.kind == KIND_R ? nr : nw)++;
+      nvars += d.vars.size();
+    }
     const bool fits_generic =
         nr <= (size_t)kGenMaxDesc && nw <= (size_t)kGenMaxDesc && nvars <= (size_t)kGenMaxVar;
-    if (!fits_generic)
-      throw LoadError{PICKER_EFORMAT, "kernel " + std::to_string(k.id) +
-                                          ": more than 64 read/write descriptors or variables "
-                                          "(wide path not built in this version)"};
-    (void)opt;
-    k.path = PATH_GENERIC;
+    const bool fits_jit = (int64_t)(nr * nw) <= kJitMaxPairs;
+    if (opt.jit && fits_jit && opt.force_path != 1) {
+      k.path = PATH_JIT;
+    } else if (fits_generic) {
+      k.path = PATH_GENERIC;
+    } else {
+      throw LoadError{PICKER_EFORMAT,
+                      "kernel " + std::to_string(k.id) +
+                          ": too many descriptors for the table-driven path and the "
+                          "specialised path is disabled or the pair count is too large"};
+    }
   }
 }
 
@@ -40,15 +52,16 @@ bool any_jit(const std::vector<IrKernel>& ks) {
   return false;
 }
 
-cudaError_t launch_validate(const Tables& T, JitModule* jit, const Options& opt, const DevBatch& b,
-                            uint64_t n, uint8_t* flags, uint32_t* bits,
+cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options& opt,
+                            const DevBatch& b, uint64_t n, uint8_t* flags, uint32_t* bits,
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches) {
-  (void)opt;
   if (n == 0) return cudaSuccess;
-  if (jit) return launch_jit(jit, T, b, n, flags, bits, counts, num_sms, s, launches);
   *launches += 1;
-  return launch_generic(T, b, n, flags, bits, counts, num_sms, s);
+  if (jit) return launch_jit(jit, P, b, n, flags, bits, counts, num_sms, s);
+  if (opt.bucket && bucket_smem_bytes(P.nbins + 1) <= kMaxSmem)
+    return launch_bucket_generic(P, b, n, flags, bits, counts, num_sms, s);
+  return launch_generic(P.T, b, n, flags, bits, counts, num_sms, s);
 }
 
 }  // namespace picker

@@ -1,29 +1,522 @@
-// NVRTC-specialised validation kernels (placeholder until the JIT lands).
+// Specialised validation functions, compiled at load time with NVRTC.
+//
+// The paper turns each kernel's symbolic addresses into C, compiles them into
+// a shared library and calls the function of the launched kernel (compiled
+// execution: "the loop over the symbolic addresses is
+// unrolled, and the functions that calculate the ranges are all inlined ...
+// common expression extraction").  The B200 analog generates straight-line
+// CUDA per kernel *shape*: the structure of a summary (which operands, how
+// many checks, descriptors, terms and variables, which sign each term has,
+// which read/write pairs exist) becomes code with extents in registers and one
+// endpoint per bound; the kernel's integer constants (coefficients, bounds,
+// widths) are read from a per-kernel constant table with warp-uniform loads.
+// Many kernels share a shape (every TVM dense kernel, every elementwise
+// kernel of one arity), so the module stays small enough for the instruction
+// caches: specialising per kernel instead made the bucketed kernel
+// instruction-fetch bound (ncu: no_instruction stalls, profiles/).
+//
+// Dispatch (inside k_bucket.cuh, warp-uniform per 32-record group):
+//   shape 0: unknown kernel id      shape 1: table-driven evaluator
+//   shape 2: kernel-level shortcut  shape 3+s: generated function ks<s>
+// Bins are ordered by shape so neighbouring groups run the same code.
+// The compiled cubin is cached on disk by source hash ($PICKER_JIT_CACHE,
+// default ~/.cache/picker_jit); the cache only saves compile time.
 #include <cuda_runtime.h>
+#include <nvrtc.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <fstream>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
 
 #include "launch.hpp"
 #include "loader.hpp"
 
 namespace picker {
 
-struct JitModule {};
+#include "jit_embed.inc"  // kEmbedNames[], kEmbedSrc[], kEmbedCount (build.py)
 
-JitModule* jit_build(const std::vector<IrKernel>&, const Options&, std::string& err) {
-  err = "specialised path not built in this version";
-  return nullptr;
+struct JitModule {
+  cudaLibrary_t lib = nullptr;
+  cudaKernel_t kernel = nullptr;
+  size_t smem = 0;
+  JitMeta* d_meta = nullptr;
+  int64_t* d_consts = nullptr;
+  uint32_t* d_kb = nullptr;
+  uint32_t kb_unknown = 0;
+  uint32_t nkeys = 0;
+  int nshapes = 0;
+  int tile = 0, threads = 0, ctas = 0;
+};
+
+namespace {
+
+constexpr uint32_t SHAPE_UNKNOWN = 0, SHAPE_GENERIC = 1, SHAPE_SHORTCUT = 2, SHAPE_FIRST = 3;
+
+std::string lit(int64_t v) {
+  if (v == (int64_t)(-9223372036854775807LL - 1)) return "(-9223372036854775807LL - 1)";
+  return std::to_string(v) + "LL";
 }
 
-void jit_destroy(JitModule* m) { delete m; }
-
-cudaError_t launch_jit(JitModule*, const Tables&, const DevBatch&, uint64_t, uint8_t*, uint32_t*,
-                       unsigned long long*, int, cudaStream_t, int*) {
-  return cudaErrorNotSupported;
+std::string opnd(uint8_t o) {
+  if (o < 6) return "d" + std::to_string(o);
+  if (o == OPD_ONE) return "1LL";
+  if (o == OPD_NONE) return "0LL";
+  return "x" + std::to_string(o - OPD_ARG0);
 }
 
-cudaError_t launch_exact(const Tables&, const DevBatch&, uint64_t, uint8_t*, unsigned long long*,
-                         uint64_t, int, cudaStream_t, int*, std::string& err) {
-  err = "exact verifier not built in this version";
-  return cudaErrorNotSupported;
+const char* kCmp[6] = {"<", "<=", ">", ">=", "==", "!="};
+
+void uses(uint8_t o, std::vector<bool>& used) {
+  if (o >= OPD_ARG0) used[o - OPD_ARG0] = true;
+}
+
+// Emits the body of one kernel's function; integer constants go to `K` and
+// appear in the text as __ldg(K + i), so kernels of one shape share the text.
+struct Gen {
+  std::vector<int64_t>& K;
+  std::ostringstream s;
+  explicit Gen(std::vector<int64_t>& k) : K(k) {}
+  std::string k(int64_t v) {
+    K.push_back(v);
+    return "__ldg(K + " + std::to_string(K.size() - 1) + ")";
+  }
+  std::string prod(const IrProd& p) {
+    std::string e;
+    auto mul = [&](const std::string& x) { e = e.empty() ? x : "mul64(" + e + ", " + x + ")"; };
+    if (p.k != 1) mul(k(p.k));
+    if (p.a != OPD_ONE) mul(opnd(p.a));
+    if (p.b != OPD_ONE) mul(opnd(p.b));
+    return e.empty() ? "1LL" : e;
+  }
+  std::string bexpr(const IrBexpr& b) {
+    std::string e = b.k0 ? k(b.k0) : "";
+    for (auto& p : b.p) e = e.empty() ? prod(p) : "add64(" + e + ", " + prod(p) + ")";
+    return e.empty() ? "0LL" : e;
+  }
+};
+
+std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
+  Gen g(K);
+  std::ostringstream& s = g.s;
+  const int np = (int)k.param_names.size();
+  s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K) {\n";
+  s << "  const int64_t d0 = r.grid_x, d1 = r.grid_y, d2 = r.grid_z, d3 = r.block_x, d4 = r.block_y,"
+       " d5 = r.block_z;\n";
+  s << "  if (!launch_limits_ok6(d0, d1, d2, d3, d4, d5)) return V_NI_PRECOND;\n";
+  std::vector<bool> used(np, false);
+  for (auto* lst : {&k.pre, &k.glob})
+    for (auto& c : *lst) uses(c.op, used);
+  for (auto& d : k.desc) {
+    uses(d.base, used);
+    for (auto& gd : d.guard) uses(gd.a, used), uses(gd.b, used);
+    for (auto& v : d.vars)
+      for (auto* side : {&v.lo, &v.hi})
+        for (auto& e : *side)
+          for (auto& p : e.p) uses(p.a, used), uses(p.b, used);
+    for (auto& t : d.terms) uses(t.c.a, used), uses(t.c.b, used);
+  }
+
+  for (int i = 0; i < np; ++i)
+    if (used[i]) {
+      if (k.param_i32[i])
+        s << "  const int64_t x" << i << " = (int64_t)(int32_t)(uint32_t)a[" << i << "];\n";
+      else
+        s << "  const int64_t x" << i << " = a[" << i << "];\n";
+    }
+  for (auto& c : k.pre)
+    s << "  if (" << opnd(c.op) << " < " << g.k(c.lo) << " || " << opnd(c.op) << " > " << g.k(c.hi)
+      << ") return V_NI_PRECOND;\n";
+  for (auto& c : k.glob)
+    s << "  if (" << opnd(c.op) << " < " << g.k(c.lo) << " || " << opnd(c.op) << " > " << g.k(c.hi)
+      << ") return V_NI_GLOBAL;\n";
+  // variable slots, deduplicated by content (as in flatten())
+  struct SlotKey {
+    uint8_t skind, axis;
+    std::vector<std::pair<int64_t, std::vector<std::tuple<int64_t, int, int>>>> lo, hi;
+    bool operator==(const SlotKey& o) const {
+      return skind == o.skind && axis == o.axis && lo == o.lo && hi == o.hi;
+    }
+  };
+  auto key_of = [](const IrVar& v) {
+    SlotKey kk{v.skind, v.axis, {}, {}};
+    for (auto* side : {&v.lo, &v.hi})
+      for (auto& e : *side) {
+        std::vector<std::tuple<int64_t, int, int>> ps;
+        for (auto& p : e.p) ps.emplace_back(p.k, p.a, p.b);
+        (side == &v.lo ? kk.lo : kk.hi).emplace_back(e.k0, ps);
+      }
+    return kk;
+  };
+  std::vector<SlotKey> keys;
+  std::vector<bool> lo0;
+  auto slot_of = [&](const IrVar& v) -> int {
+    SlotKey kk = key_of(v);
+    for (size_t i = 0; i < keys.size(); ++i)
+      if (keys[i] == kk) return (int)i;
+    std::string lo, hi;
+    auto add_lo = [&](const std::string& e) { lo = lo.empty() ? e : "max64(" + lo + ", " + e + ")"; };
+    auto add_hi = [&](const std::string& e) { hi = hi.empty() ? e : "min64(" + hi + ", " + e + ")"; };
+    if (v.skind != SK_NONE) {
+      add_lo("0LL");
+      std::string gg = "d" + std::to_string(v.axis), b = "d" + std::to_string(3 + v.axis);
+      add_hi(v.skind == SK_TID ? b + " - 1" : v.skind == SK_BID ? gg + " - 1" : gg + " * " + b + " - 1");
+    }
+    for (auto& e : v.lo) add_lo(g.bexpr(e));
+    for (auto& e : v.hi) add_hi(g.bexpr(e));
+    keys.push_back(kk);
+    lo0.push_back(v.skind != SK_NONE && v.lo.empty());
+    const size_t i = keys.size() - 1;
+    s << "  const int64_t vl" << i << " = " << lo << ", vh" << i << " = " << hi << ";\n";
+    return (int)i;
+  };
+  std::vector<int> rd, wr, rd_opq, wr_opq;
+  for (size_t di = 0; di < k.desc.size(); ++di) {
+    const IrDesc& d = k.desc[di];
+    std::vector<int> sid;
+    for (auto& v : d.vars) sid.push_back(slot_of(v));
+    std::string on = "true";
+    for (auto& gd : d.guard)
+      on += " && (" + opnd(gd.a) + " " + kCmp[gd.cmp] + " " + (gd.b == OPD_NONE ? g.k(gd.bconst) : opnd(gd.b)) + ")";
+    for (int x : sid) on += " && (vl" + std::to_string(x) + " <= vh" + std::to_string(x) + ")";
+    s << "  const bool on" << di << " = " << on << ";\n";
+    if (d.opaque) {
+      (d.kind == KIND_R ? rd_opq : wr_opq).push_back((int)di);
+      continue;
+    }
+    std::string lb = d.base == OPD_NONE ? "0LL" : opnd(d.base), ub = lb;
+    for (auto& t : d.terms) {
+      std::string c = g.prod(t.c);
+      if (t.var < 0) {
+        lb = "add64(" + lb + ", " + c + ")";
+        ub = "add64(" + ub + ", " + c + ")";
+        continue;
+      }
+      const int x = sid[t.var];
+      auto phi = [&](const std::string& v) {
+        return t.div == 1 ? v : "floordiv64(" + v + ", " + std::to_string(t.div) + "u)";
+      };
+      const std::string L = "vl" + std::to_string(x), H = "vh" + std::to_string(x);
+      const int sign = k.var_sign[di][t.var];
+      if (sign > 0) {  // non-decreasing: min at lo, max at hi
+        if (!lo0[x]) lb = "add64(" + lb + ", mul64(" + c + ", " + phi(L) + "))";
+        ub = "add64(" + ub + ", mul64(" + c + ", " + phi(H) + "))";
+      } else if (sign < 0) {
+        lb = "add64(" + lb + ", mul64(" + c + ", " + phi(H) + "))";
+        if (!lo0[x]) ub = "add64(" + ub + ", mul64(" + c + ", " + phi(L) + "))";
+      } else {
+        s << "  const int64_t c" << di << "_" << &t - &d.terms[0] << " = " << c << ";\n";
+        const std::string cv = "c" + std::to_string(di) + "_" + std::to_string(&t - &d.terms[0]);
+        std::string A = "mul64(" + cv + ", " + phi(L) + ")", Bv = "mul64(" + cv + ", " + phi(H) + ")";
+        lb = "add64(" + lb + ", min64(" + A + ", " + Bv + "))";
+        ub = "add64(" + ub + ", max64(" + A + ", " + Bv + "))";
+      }
+    }
+    if (d.width > 1) ub = "add64(" + ub + ", " + g.k((int64_t)d.width - 1) + ")";
+    s << "  const int64_t lb" << di << " = " << lb << ", ub" << di << " = " << ub << ";\n";
+    (d.kind == KIND_R ? rd : wr).push_back((int)di);
+  }
+  auto any = [&](const std::vector<int>& a, const std::vector<int>& b) {
+    std::string e = "false";
+    for (int i : a) e += " || on" + std::to_string(i);
+    for (int i : b) e += " || on" + std::to_string(i);
+    return e;
+  };
+  if (!rd_opq.empty() || !wr_opq.empty()) {
+    s << "  {\n    const bool act_r = " << any(rd, rd_opq) << ", act_w = " << any(wr, wr_opq) << ";\n";
+    s << "    const bool opq_r = " << any(rd_opq, {}) << ", opq_w = " << any(wr_opq, {}) << ";\n";
+    s << "    if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;\n  }\n";
+  }
+  s << "  bool ov = false;\n";
+  for (int i : rd)
+    for (int j : wr)
+      s << "  ov |= on" << i << " & on" << j << " & (lb" << i << " <= ub" << j << ") & (lb" << j
+        << " <= ub" << i << ");\n";
+  s << "  return ov ? V_NI_OVERLAP : V_IDEM_CHECKED;\n}\n";
+  return s.str();
+}
+
+uint64_t fnv1a(const std::string& s) {
+  uint64_t h = 1469598103934665603ULL;
+  for (unsigned char c : s) h = (h ^ c) * 1099511628211ULL;
+  return h;
+}
+
+std::string cache_dir() {
+  const char* e = getenv("PICKER_JIT_CACHE");
+  if (e && *e) return e;
+  const char* home = getenv("HOME");
+  return std::string(home && *home ? home : "/tmp") + "/.cache/picker_jit";
+}
+
+bool read_file(const std::string& p, std::string& out) {
+  std::ifstream f(p, std::ios::binary);
+  if (!f) return false;
+  std::stringstream ss;
+  ss << f.rdbuf();
+  out = ss.str();
+  return !out.empty();
+}
+
+void write_file_atomic(const std::string& dir, const std::string& name, const std::string& data) {
+  for (size_t i = 1; i <= dir.size(); ++i)
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+  std::string tmp = dir + "/" + name + ".tmp" + std::to_string(getpid());
+  {
+    std::ofstream f(tmp, std::ios::binary);
+    if (!f) return;
+    f.write(data.data(), (std::streamsize)data.size());
+  }
+  rename(tmp.c_str(), (dir + "/" + name).c_str());
+}
+
+bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defines, std::string& cubin,
+                   std::string& lowered, std::string& err) {
+  nvrtcProgram prog;
+  nvrtcResult r = nvrtcCreateProgram(&prog, src.c_str(), "picker_jit.cu", kEmbedCount, kEmbedSrc, kEmbedNames);
+  if (r != NVRTC_SUCCESS) {
+    err = nvrtcGetErrorString(r);
+    return false;
+  }
+  const char* name_expr = "picker::k_validate_bucket<picker::JitDispatch>";
+  nvrtcAddNameExpression(prog, name_expr);
+  std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
+                                   "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
+  for (auto& d : defines) opts.push_back(d.c_str());
+  r = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
+  if (r != NVRTC_SUCCESS) {
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    std::string log(n, '\0');
+    nvrtcGetProgramLog(prog, &log[0]);
+    err = std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 4000);
+    nvrtcDestroyProgram(&prog);
+    return false;
+  }
+  const char* low = nullptr;
+  nvrtcGetLoweredName(prog, name_expr, &low);
+  lowered = low ? low : "";
+  size_t n = 0;
+  nvrtcGetCUBINSize(prog, &n);
+  cubin.assign(n, '\0');
+  nvrtcGetCUBIN(prog, &cubin[0]);
+  nvrtcDestroyProgram(&prog);
+  return true;
+}
+
+}  // namespace
+
+JitPlan jit_plan(const std::vector<IrKernel>& ks) {
+  JitPlan P;
+  std::ostringstream src;
+  src << "// generated by picker jit.cpp\n"
+         "typedef signed char int8_t; typedef short int16_t; typedef int int32_t; typedef long long int64_t;\n"
+         "typedef unsigned char uint8_t; typedef unsigned short uint16_t; typedef unsigned int uint32_t;\n"
+         "typedef unsigned long long uint64_t; typedef unsigned long size_t; typedef unsigned long uintptr_t;\n"
+         "#include \"eval_generic.cuh\"\n#include \"k_bucket.cuh\"\nnamespace picker {\n";
+  // pass 1: body text with every constant as a load, grouped into shapes
+  std::map<std::string, uint32_t> shape_id;
+  std::vector<std::string> shapes;
+  std::vector<std::vector<size_t>> members;
+  std::vector<std::vector<int64_t>> kconst(ks.size());
+  std::vector<int> shape_of(ks.size(), -1);
+  for (size_t i = 0; i < ks.size(); ++i) {
+    if (ks[i].path != PATH_JIT) continue;
+    std::string body = gen_body(ks[i], kconst[i]);
+    auto it = shape_id.find(body);
+    if (it == shape_id.end()) {
+      it = shape_id.emplace(body, (uint32_t)shapes.size()).first;
+      shapes.push_back(body);
+      members.emplace_back();
+    }
+    shape_of[i] = (int)it->second;
+    members[it->second].push_back(i);
+  }
+  // pass 2: a constant position with one value across all kernels of the shape
+  // becomes an immediate again; only the varying positions stay in the table
+  std::vector<std::vector<int>> slot(shapes.size());  // position -> compacted index, -1: immediate
+  for (size_t s = 0; s < shapes.size(); ++s) {
+    const std::vector<int64_t>& k0 = kconst[members[s][0]];
+    slot[s].assign(k0.size(), -1);
+    int q = 0;
+    for (size_t p = 0; p < k0.size(); ++p) {
+      bool uniform = true;
+      for (size_t i : members[s]) uniform &= kconst[i][p] == k0[p];
+      if (!uniform) slot[s][p] = q++;
+    }
+    std::string& b = shapes[s];
+    for (size_t p = k0.size(); p-- > 0;) {
+      const std::string tok = "__ldg(K + " + std::to_string(p) + ")";
+      // kept loads are renamed through a marker so later passes cannot match them
+      const std::string rep = slot[s][p] < 0 ? "(" + lit(k0[p]) + ")"
+                                             : "__ldg(K@ + " + std::to_string(slot[s][p]) + ")";
+      for (size_t at = b.find(tok); at != std::string::npos; at = b.find(tok, at + rep.size()))
+        b.replace(at, tok.size(), rep);
+    }
+    for (size_t at = b.find("K@"); at != std::string::npos; at = b.find("K@", at)) b.erase(at + 1, 1);
+  }
+  P.meta.resize(ks.size() + 1);
+  for (size_t i = 0; i < ks.size(); ++i) {
+    const IrKernel& k = ks[i];
+    JitMeta m{SHAPE_GENERIC, (uint32_t)P.consts.size(), (uint32_t)k.param_names.size(), 0};
+    if (k.path == PATH_SHORTCUT) {
+      m.shape = SHAPE_SHORTCUT;
+      P.consts.push_back(k.shortcut);
+    } else if (k.path == PATH_JIT) {
+      const int s = shape_of[i];
+      m.shape = SHAPE_FIRST + (uint32_t)s;
+      for (size_t p = 0; p < kconst[i].size(); ++p)
+        if (slot[s][p] >= 0) P.consts.push_back(kconst[i][p]);
+    }
+    P.meta[i] = m;
+  }
+  P.meta[ks.size()] = JitMeta{SHAPE_UNKNOWN, 0, 0, 0};
+  if (P.consts.empty()) P.consts.push_back(0);
+  for (auto& m : P.meta) P.key_of.push_back((uint16_t)m.shape);
+  for (size_t s = 0; s < shapes.size(); ++s)
+    src << "__device__ __forceinline__ uint8_t ks" << s << shapes[s];
+  // key = shape (warp-uniform); bin = the lane's kernel (its constants)
+  src << "struct JitDispatch {\n  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, "
+         "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
+         "    if (key == 0) return V_ERR_KERNEL;\n"
+         "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n"
+         "    const JitMeta m = P.jit_meta[bin];\n"
+         "    if (!args_in_range(r, m.nparams, B.args_lo, B.args_hi)) return V_ERR_ARITY;\n"
+         "    const int64_t* __restrict__ K = P.jit_consts + m.koff;\n"
+         "    switch (key) {\n"
+         "      case 2: return (uint8_t)__ldg(K);\n";
+  for (size_t s = 0; s < shapes.size(); ++s)
+    src << "      case " << SHAPE_FIRST + s << ": return ks" << s << "(r, a, K);\n";
+  src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
+         "template __global__ void k_validate_bucket<JitDispatch>(const __grid_constant__ BucketParams, "
+         "const __grid_constant__ DevBatch, uint64_t, "
+         "uint8_t*, uint32_t*, unsigned long long*);\n}  // namespace picker\n";
+  P.src = src.str();
+  P.nshapes = (int)shapes.size();
+  return P;
+}
+
+void order_by_shape(std::vector<IrKernel>& ks) {
+  JitPlan P = jit_plan(ks);
+  std::vector<size_t> idx(ks.size());
+  for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
+  std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return P.meta[a].shape < P.meta[b].shape; });
+  std::vector<IrKernel> out;
+  out.reserve(ks.size());
+  for (size_t i : idx) out.push_back(std::move(ks[i]));
+  ks.swap(out);
+}
+
+std::vector<std::string> geometry_defines(const Options& opt) {
+  return {"-DPICKER_TILE=" + std::to_string(opt.tile), "-DPICKER_THREADS=" + std::to_string(opt.threads),
+          "-DPICKER_CTAS=" + std::to_string(opt.ctas),
+          "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec)};
+}
+
+bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
+                 bool use_cache, std::string& err) {
+  const std::vector<std::string> defs = geometry_defines(opt);
+  std::string key = plan.src + "|sm_100a|v3";
+  for (auto& d : defs) key += "|" + d;
+  const uint64_t h = fnv1a(key);
+  char name[64];
+  snprintf(name, sizeof(name), "%016llx.cubin", (unsigned long long)h);
+  const std::string dir = cache_dir();
+  const std::string meta_name = std::string(name) + ".name";
+  if (use_cache && read_file(dir + "/" + name, cubin) && read_file(dir + "/" + meta_name, lowered))
+    return true;
+  if (!nvrtc_compile(plan.src, defs, cubin, lowered, err)) return false;
+  if (use_cache) {
+    write_file_atomic(dir, name, cubin);
+    write_file_atomic(dir, meta_name, lowered);
+  }
+  return true;
+}
+
+JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt, std::string& err) {
+  if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
+      opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1) {
+    err = "invalid tile / threads / ctas / args_per_rec options";
+    return nullptr;
+  }
+  JitPlan plan = jit_plan(ks);
+  std::string cubin, lowered;
+  if (!jit_compile(plan, opt, cubin, lowered, true, err)) return nullptr;
+  JitModule* m = new JitModule();
+  m->nshapes = plan.nshapes;
+  m->tile = opt.tile;
+  m->threads = opt.threads;
+  m->ctas = opt.ctas;
+  cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, lowered.c_str());
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_meta, plan.meta.size() * sizeof(JitMeta));
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_consts, plan.consts.size() * sizeof(int64_t));
+  // kernel id -> (bin | shape << 16); bins are positions in `ks`
+  uint32_t maxid = 0;
+  for (auto& k : ks) maxid = std::max(maxid, k.id);
+  const uint32_t nbins = (uint32_t)ks.size();
+  m->kb_unknown = nbins | ((uint32_t)SHAPE_UNKNOWN << 16);
+  std::vector<uint32_t> kb(ks.empty() ? 1 : (size_t)maxid + 1, m->kb_unknown);
+  for (uint32_t i = 0; i < nbins; ++i) kb[ks[i].id] = i | ((uint32_t)plan.key_of[i] << 16);
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_kb, kb.size() * sizeof(uint32_t));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->d_kb, kb.data(), kb.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->d_meta, plan.meta.data(), plan.meta.size() * sizeof(JitMeta), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess)
+    e = cudaMemcpy(m->d_consts, plan.consts.data(), plan.consts.size() * sizeof(int64_t),
+                   cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    err = std::string("loading the JIT module: ") + cudaGetErrorString(e);
+    jit_destroy(m);
+    return nullptr;
+  }
+  m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes;
+  m->smem = bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
+  if (m->smem > kMaxSmem) {
+    err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";
+    jit_destroy(m);
+    return nullptr;
+  }
+  e = cudaFuncSetAttribute((const void*)m->kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m->smem);
+  if (e != cudaSuccess) {
+    err = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString(e);
+    jit_destroy(m);
+    return nullptr;
+  }
+  return m;
+}
+
+void jit_destroy(JitModule* m) {
+  if (!m) return;
+  if (m->lib) cudaLibraryUnload(m->lib);
+  if (m->d_meta) cudaFree(m->d_meta);
+  if (m->d_consts) cudaFree(m->d_consts);
+  if (m->d_kb) cudaFree(m->d_kb);
+  delete m;
+}
+
+cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, uint64_t n,
+                       uint8_t* flags, uint32_t* bits, unsigned long long* counts, int num_sms,
+                       cudaStream_t s) {
+  BucketParams P = P0;
+  P.jit_meta = m->d_meta;
+  P.jit_consts = m->d_consts;
+  P.kb_of = m->d_kb;
+  P.kb_unknown = m->kb_unknown;
+  P.nkeys = m->nkeys;
+  const uint64_t ntiles = (n + m->tile - 1) / m->tile;
+  const uint64_t cap = (uint64_t)num_sms * m->ctas;
+  const uint64_t grid = ntiles < cap ? ntiles : cap;
+  void* argv[] = {(void*)&P, (void*)&B, (void*)&n, (void*)&flags, (void*)&bits, (void*)&counts};
+  return cudaLaunchKernel((const void*)m->kernel, dim3((unsigned)grid), dim3(m->threads), argv, m->smem, s);
 }
 
 }  // namespace picker

@@ -1,0 +1,300 @@
+// K1 staged + bucketed validation kernel.
+//
+// One persistent CTA per SM walks tiles of kTile launch records.  Each tile's
+// 32-byte headers and its contiguous argument span are copied global->shared
+// by the TMA engine (cp.async.bulk, completion on an mbarrier), double-
+// buffered so the copy of the next tile overlaps the evaluation of this one:
+// every input byte crosses HBM once, in bulk, and all per-record gathers hit
+// shared memory.
+//
+// Inside a tile the records are grouped by `key` before evaluation, so that a
+// warp evaluates up to 32 instances that run the SAME code:
+//   - specialised module (jit.cpp): key = the kernel's shape, so kernels that
+//     share generated code (e.g. every TVM dense kernel) share warps; each lane
+//     reads its own kernel's constants;
+//   - table-driven path: key = the kernel, so table reads are warp-uniform.
+// A launch stream interleaves many kernels (C2: 547), so without grouping 32
+// consecutive records would run 32 different control paths.
+//
+// Per tile:
+//   1. key:     key and bin of each record -> smem; per-key counts (smem atomics)
+//   2. scan:    exclusive scans of counts and of 32-record group counts; a table
+//               of (key, group) work items
+//   3. scatter: record index of every slot of the key-sorted order
+//   4. eval:    warps take work items round-robin; lane l evaluates the l-th record
+//               of the group through Dispatch::eval
+//   5. emit:    codes in record order -> flags (u8), ballot-packed idempotent bits,
+//               per-code histogram (match_any-aggregated shared atomics)
+#pragma once
+
+#include "device_common.cuh"
+#include "eval_generic.cuh"
+
+namespace picker {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// TMA 1-D bulk copy global -> shared (16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+struct StageInfo {
+  uint64_t lo, hi;  // staged argument slots [lo, hi)
+  uint32_t shift;   // byte offset of slot lo inside the staged buffer
+  uint32_t staged;  // 1: args of this tile are in shared memory
+};
+
+// Thread 0: start the copies of tile `tile` into buffer `buf`.  `lo`, `last_off`
+// and `last_n` were loaded earlier (the tile's first arg_off and its last
+// record's arg_off / nargs) so their latency is off the critical path.
+__device__ __forceinline__ void stage_tile(const DevBatch& B, uint64_t n, uint64_t tile, unsigned char* hdr,
+                                           unsigned char* arg, uint64_t* bar, StageInfo* info, uint64_t lo,
+                                           uint64_t last_off, uint64_t last_n) {
+  const uint64_t base = tile * kTile;
+  if (base >= n) return;
+  const uint64_t m = min((uint64_t)kTile, n - base);
+  const uint32_t hbytes = (uint32_t)(m * sizeof(picker_rec_t));
+  const uint64_t hi = last_off + last_n;
+  StageInfo si{lo, hi, 0, 0};
+  uint32_t abytes = 0;
+  const char* src = nullptr;
+  if (hi > lo && hi - lo <= (uint64_t)kArgCap && lo >= B.args_lo && hi <= B.args_hi) {
+    const uintptr_t a0 = (uintptr_t)(B.args + lo), a1 = (uintptr_t)(B.args + hi);
+    const uintptr_t s0 = a0 & ~(uintptr_t)15, s1 = (a1 + 15) & ~(uintptr_t)15;
+    const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
+    if (s0 >= p0 && s1 <= p1) {  // the rounded span stays inside the pool
+      si.staged = 1;
+      si.shift = (uint32_t)(a0 - s0);
+      abytes = (uint32_t)(s1 - s0);
+      src = (const char*)s0;
+    }
+  }
+  *info = si;
+  mbar_arrive_expect_tx(bar, hbytes + abytes);
+  tma_load_1d(hdr, B.rec + base, hbytes, bar);
+  if (abytes) tma_load_1d(arg, src, abytes, bar);
+}
+
+__device__ __forceinline__ picker_rec_t rec_from_smem(const unsigned char* p) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p), b = *reinterpret_cast<const uint4*>(p + 16);
+  picker_rec_t r;
+  r.kernel_id = a.x;
+  r.nargs = a.y;
+  r.grid_x = a.z;
+  r.grid_y = (uint16_t)(a.w & 0xFFFF);
+  r.grid_z = (uint16_t)(a.w >> 16);
+  r.block_x = (uint16_t)(b.x & 0xFFFF);
+  r.block_y = (uint16_t)(b.x >> 16);
+  r.block_z = (uint16_t)(b.y & 0xFFFF);
+  r.reserved = (uint16_t)(b.y >> 16);
+  r.arg_off = ((uint64_t)b.w << 32) | b.z;
+  return r;
+}
+
+// Lane 0 claims the next work item; the index is broadcast to the warp.
+__device__ __forceinline__ uint32_t warp_claim(uint32_t* counter) {
+  uint32_t g = 0;
+  if ((threadIdx.x & 31) == 0) g = atomicAdd(counter, 1u);
+  return __shfl_sync(0xffffffffu, g, 0);
+}
+
+template <class Dispatch>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    k_validate_bucket(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B,
+                      uint64_t n, uint8_t* __restrict__ flags,
+                      uint32_t* __restrict__ bits, unsigned long long* __restrict__ counts) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t nk = P.nkeys;
+  // staging buffers: headers at smem + buf*kHdrBytes, args at smem + kArgOff + buf*kArgBufBytes
+  constexpr uint32_t kHdrBytes = kTile * 32;
+  constexpr uint32_t kArgOff = 2 * kHdrBytes;
+  uint16_t* s_key = reinterpret_cast<uint16_t*>(smem + kArgOff + 2 * kArgBufBytes);
+  uint16_t* s_bin = s_key + kTile;
+  uint16_t* s_perm = s_bin + kTile;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_perm + kTile);
+  uint32_t* s_off = s_cnt + nk;
+  uint32_t* s_cur = s_off + nk;
+  uint32_t* s_grp = s_cur + nk;
+  __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
+  __shared__ uint32_t s_bits[kTile / 32];
+  __shared__ uint32_t s_wsum[2][kWarps];
+  __shared__ uint32_t s_ngrp, s_next;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ StageInfo s_info[2];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t G = gridDim.x;
+  if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
+  if (tid < kTile / 32) s_bits[tid] = 0;
+  // arg_off bounds of a tile, loaded ahead of its staging
+  auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& lo_last, uint64_t& n_last) {
+    const uint64_t base = tile * kTile;
+    lo = lo_last = n_last = 0;
+    if (base < n) {
+      const uint64_t m = min((uint64_t)kTile, n - base);
+      lo = __ldg(&B.rec[base].arg_off);
+      lo_last = __ldg(&B.rec[base + m - 1].arg_off);
+      n_last = __ldg(&B.rec[base + m - 1].nargs);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int b = 0; b < 2; ++b) {
+      uint64_t lo, ll, nl;
+      bounds(blockIdx.x + b * G, lo, ll, nl);
+      stage_tile(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, smem + kArgOff + b * kArgBufBytes,
+                 &s_bar[b], &s_info[b], lo, ll, nl);
+    }
+  }
+  __syncthreads();
+
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
+    const uint32_t buf = it & 1, parity = (it >> 1) & 1;
+    const uint64_t base = tile * kTile;
+    const int m = (int)min((uint64_t)kTile, n - base);
+    uint64_t nlo = 0, nll = 0, nnl = 0;
+    if (tid == 0) bounds(tile + 2 * G, nlo, nll, nnl);  // consumed after this tile
+    for (uint32_t b = tid; b < nk; b += kThreads) s_cnt[b] = 0;
+    mbar_wait(&s_bar[buf], parity);
+    const unsigned char* hdr = smem + buf * kHdrBytes;
+    const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
+    const StageInfo si = s_info[buf];
+    __syncthreads();
+
+    // 1. keys
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
+      const uint32_t kb = kid < P.T.nkernel_slots ? __ldg(P.kb_of + kid) : P.kb_unknown;
+      const uint32_t key = kb >> 16;
+      s_bin[i] = (uint16_t)(kb & 0xFFFFu);
+      s_key[i] = (uint16_t)key;
+      atomicAdd(s_cnt + key, 1u);
+    }
+    __syncthreads();
+
+    // 2. scans: record offsets and 32-record groups per key
+    {
+      const uint32_t per = (nk + kThreads - 1) / kThreads;
+      const uint32_t b0 = min(nk, tid * per), b1 = min(nk, b0 + per);
+      uint32_t rs = 0, gs = 0;
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t c = s_cnt[b];
+        rs += c;
+        gs += (c + 31) >> 5;
+      }
+      uint32_t ri = rs, gi = gs;  // inclusive warp scans
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t r2 = __shfl_up_sync(0xffffffffu, ri, d), g2 = __shfl_up_sync(0xffffffffu, gi, d);
+        if (lane >= d) ri += r2, gi += g2;
+      }
+      if (lane == 31) s_wsum[0][warp] = ri, s_wsum[1][warp] = gi;
+      __syncthreads();
+      uint32_t ro = ri - rs, go = gi - gs;
+      for (int w = 0; w < warp; ++w) ro += s_wsum[0][w], go += s_wsum[1][w];
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t c = s_cnt[b];
+        s_off[b] = ro;
+        s_cur[b] = ro;
+        const uint32_t ng = (c + 31) >> 5;
+        for (uint32_t j = 0; j < ng; ++j) s_grp[go + j] = (b << 8) | j;
+        ro += c;
+        go += ng;
+      }
+      if (tid == kThreads - 1) s_ngrp = go, s_next = 0;
+    }
+    __syncthreads();
+
+    // 3. scatter record indices into key order
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t pos = atomicAdd(s_cur + s_key[i], 1u);
+      s_perm[pos] = (uint16_t)i;
+    }
+    __syncthreads();
+
+    // 4. evaluate one 32-record group of one key per warp (warps claim groups
+    //    dynamically: groups of different shapes cost different amounts) and
+    //    emit: the u8 code, the idempotent bit (shared atomics into the tile's
+    //    bit words) and the histogram (match_any-aggregated shared atomics)
+    const uint32_t ngrp = s_ngrp;
+    for (uint32_t g = warp_claim(&s_next); g < ngrp; g = warp_claim(&s_next)) {
+      const uint32_t e = s_grp[g];
+      const uint32_t key = e >> 8, j = e & 255u;
+      const uint32_t cnt = s_cnt[key] - 32u * j;
+      const bool on = (uint32_t)lane < cnt;
+      uint8_t code = 0;
+      uint32_t li = 0;
+      if (on) {
+        li = s_perm[s_off[key] + 32u * j + lane];
+        const picker_rec_t r = rec_from_smem(hdr + 32 * li);
+        const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                           (uint64_t)r.nargs <= si.hi - r.arg_off;
+        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                 : B.args + r.arg_off;
+        code = Dispatch::eval(key, s_bin[li], P, r, a, B);
+        flags[base + li] = code;
+        if (code <= V_IDEM_KERNEL) atomicOr(s_bits + (li >> 5), 1u << (li & 31));
+      }
+      const int hb = on ? count_bin(code) : 16;
+      const unsigned same = __match_any_sync(0xffffffffu, hb);
+      if (on && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
+    }
+    __syncthreads();
+    // this tile's buffers are free: start the copy of the tile after next
+    if (tid == 0)
+      stage_tile(B, n, tile + 2 * G, smem + buf * kHdrBytes, smem + kArgOff + buf * kArgBufBytes,
+                 &s_bar[buf], &s_info[buf], nlo, nll, nnl);
+    if (tid < (m + 31) / 32) {
+      if (bits) bits[(base >> 5) + tid] = s_bits[tid];
+      s_bits[tid] = 0;
+    }
+  }
+  __syncthreads();
+  if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid])
+    atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+}
+
+// Dispatch used by the static library: every bin through the table-driven
+// evaluator (grouping by kernel makes its table reads warp-uniform).
+struct GenericDispatch {
+  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, const BucketParams& P,
+                                                 const picker_rec_t& r, const int64_t* a,
+                                                 const DevBatch& B) {
+    (void)key;
+    if (bin >= P.nbins) return V_ERR_KERNEL;
+    return eval_generic(P.T, r, a, B.args_lo, B.args_hi);
+  }
+};
+
+}  // namespace picker

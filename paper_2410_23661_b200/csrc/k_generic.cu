@@ -14,100 +14,11 @@
 #include <cstdint>
 
 #include "../../include/picker.h"
-#include "device_common.cuh"
+#include "eval_generic.cuh"
+#include "k_bucket.cuh"
 #include "launch.hpp"
-#include "tables.hpp"
 
 namespace picker {
-
-__device__ __noinline__ uint8_t eval_generic(const Tables& T, const picker_rec_t& r,
-                                             const int64_t* __restrict__ args, uint64_t args_lo,
-                                             uint64_t args_hi) {
-  const uint32_t kid = r.kernel_id;
-  if (kid >= T.nkernel_slots) return V_ERR_KERNEL;
-  const DKernel K = T.kernels[kid];
-  if (K.shortcut == V_ERR_KERNEL) return V_ERR_KERNEL;
-  if (!args_in_range(r, K.nparams, args_lo, args_hi)) return V_ERR_ARITY;
-  if (K.shortcut) return K.shortcut;
-
-  RecVals X(r, args, K.i32mask);
-  if (!launch_limits_ok(X)) return V_NI_PRECOND;
-  for (int c = 0; c < K.npre + K.nglob; ++c) {
-    const DCheck ch = T.checks[K.check + c];
-    const int64_t v = X.get(ch.op);
-    if (v < ch.lo || v > ch.hi) return c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
-  }
-
-  auto P = [&](uint16_t j) -> int64_t {
-    const DProd p = T.prods[K.prod + j];
-    return mul64(mul64(p.k, X.get(p.a)), X.get(p.b));
-  };
-  auto B = [&](const DBexpr& b) -> int64_t {
-    int64_t v = b.k0;
-    if (b.p0 != kNone16) v = add64(v, P(b.p0));
-    if (b.p1 != kNone16) v = add64(v, P(b.p1));
-    return v;
-  };
-
-  int64_t vlo[kGenMaxVar], vhi[kGenMaxVar];
-  for (int s = 0; s < K.nvar; ++s) {
-    const DVar v = T.vars[K.var + s];
-    int64_t lo = INT64_MIN, hi = INT64_MAX;
-    if (v.skind != SK_NONE) {
-      const int64_t g = X.get(OPD_GX + v.axis), b = X.get(OPD_BX + v.axis);
-      lo = 0;
-      hi = (v.skind == SK_TID ? b : v.skind == SK_BID ? g : g * b) - 1;
-    }
-    for (int j = 0; j < v.nlo; ++j) lo = max64(lo, B(T.bexprs[v.bex + j]));
-    for (int j = 0; j < v.nhi; ++j) hi = min64(hi, B(T.bexprs[v.bex + v.nlo + j]));
-    vlo[s] = lo;
-    vhi[s] = hi;
-  }
-
-  int64_t rlb[kGenMaxDesc], rub[kGenMaxDesc], wlb[kGenMaxDesc], wub[kGenMaxDesc];
-  int nr = 0, nw = 0;
-  bool opq_r = false, opq_w = false, act_r = false, act_w = false;
-  for (int di = 0; di < K.ndesc; ++di) {
-    const DDesc D = T.descs[K.desc + di];
-    bool on = true;
-    for (int g = 0; g < D.nguard && on; ++g) {
-      const DGuard G = T.guards[D.guard + g];
-      on = cmp64(X.get(G.a), G.cmp, G.b == OPD_NONE ? G.bconst : X.get(G.b));
-    }
-    for (int v = 0; v < D.nvar && on; ++v) {
-      const uint16_t s = T.varlist[D.var + v];
-      on = vlo[s] <= vhi[s];  // empty range: the site never executes
-    }
-    if (!on) continue;
-    if (D.kind == KIND_R) act_r = true; else act_w = true;
-    if (D.opaque) {
-      if (D.kind == KIND_R) opq_r = true; else opq_w = true;
-      continue;
-    }
-    int64_t lb = D.base == OPD_NONE ? 0 : X.get(D.base), ub = lb;
-    for (int t = 0; t < D.nterm; ++t) {
-      const DTerm tm = T.terms[D.term + t];
-      const int64_t c = P(tm.prod);
-      if (tm.var == kNone16) {
-        lb = add64(lb, c);
-        ub = add64(ub, c);
-      } else {
-        const int64_t a = mul64(c, floordiv64(vlo[tm.var], tm.div));
-        const int64_t b = mul64(c, floordiv64(vhi[tm.var], tm.div));
-        lb = add64(lb, min64(a, b));
-        ub = add64(ub, max64(a, b));
-      }
-    }
-    ub = add64(ub, (int64_t)D.width - 1);
-    if (D.kind == KIND_R) { rlb[nr] = lb; rub[nr] = ub; ++nr; }
-    else { wlb[nw] = lb; wub[nw] = ub; ++nw; }
-  }
-  if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
-  for (int i = 0; i < nr; ++i)
-    for (int j = 0; j < nw; ++j)
-      if (rlb[i] <= wub[j] && wlb[j] <= rub[i]) return V_NI_OVERLAP;
-  return V_IDEM_CHECKED;
-}
 
 __global__ void __launch_bounds__(256) k_validate_generic(Tables T, DevBatch B, uint64_t n,
                                                           uint8_t* __restrict__ flags,
@@ -121,12 +32,44 @@ __global__ void __launch_bounds__(256) k_validate_generic(Tables T, DevBatch B, 
     const uint64_t i = i0 + threadIdx.x;
     const bool valid = i < n;
     uint8_t code = 0;
-    if (valid) code = eval_generic(T, load_rec(B.rec + i), B.args, B.args_lo, B.args_hi);
+    if (valid) {
+      const picker_rec_t r = load_rec(B.rec + i);
+      code = eval_generic(T, r, B.args + r.arg_off, B.args_lo, B.args_hi);
+    }
     emit(i, valid, code, flags, bits, hist);
   }
   __syncthreads();
   if (counts && threadIdx.x < PICKER_NUM_COUNTS && hist[threadIdx.x])
     atomicAdd(counts + threadIdx.x, (unsigned long long)hist[threadIdx.x]);
+}
+
+template __global__ void k_validate_bucket<GenericDispatch>(const __grid_constant__ BucketParams,
+                                                            const __grid_constant__ DevBatch, uint64_t,
+                                                            uint8_t*, uint32_t*, unsigned long long*);
+
+// Table-driven evaluation through the staged + bucketed kernel (key = kernel).
+// Returns cudaErrorInvalidValue when the per-key arrays do not fit in shared
+// memory (the caller then uses the unbucketed kernel).
+cudaError_t launch_bucket_generic(const BucketParams& P0, const DevBatch& B, uint64_t n,
+                                  uint8_t* flags, uint32_t* bits, unsigned long long* counts,
+                                  int num_sms, cudaStream_t s) {
+  if (n == 0) return cudaSuccess;
+  BucketParams P = P0;  // kb_of / kb_unknown: key = bin (set at load time)
+  P.nkeys = P.nbins + 1;
+  const size_t smem = bucket_smem_bytes(P.nkeys);
+  if (smem > kMaxSmem) return cudaErrorInvalidValue;
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(k_validate_bucket<GenericDispatch>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t cap = (uint64_t)num_sms * kCtasPerSm;
+  const uint64_t grid = ntiles < cap ? ntiles : cap;
+  k_validate_bucket<GenericDispatch><<<(unsigned)grid, kThreads, smem, s>>>(P, B, n, flags, bits, counts);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_generic(const Tables& T, const DevBatch& B, uint64_t n, uint8_t* flags,

@@ -15,29 +15,36 @@ namespace picker {
 struct IrKernel;
 
 struct Options {
-  bool jit = false;
-  int64_t wide_pairs = 1024;  // |R|*|W| above which the wide path is used
-  int force_path = 0;         // 0 auto, 1 generic, 2 jit, 3 wide
-  int tile = 4096;            // records per CTA super-tile (specialised path)
-};
-
-// Records [0, n) at rec; argument slots valid at indices [args_lo, args_hi) of args.
-struct DevBatch {
-  const picker_rec_t* rec;
-  const int64_t* args;
-  uint64_t args_lo, args_hi;
+  bool jit = true;     // NVRTC-specialised functions for every COND kernel
+  bool bucket = true;  // group each tile's records by kernel before evaluating
+  int force_path = 0;  // 0 auto, 1 generic (table-driven) for every COND kernel
+  // geometry of the specialised kernel (tuning; k_bucket.cuh)
+  int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;
 };
 
 struct JitModule;
 
-// Assign a path to every kernel (shortcut / generic / jit / wide).
+// Assign a path to every kernel (shortcut / generic / jit).
 void select_paths(std::vector<IrKernel>& ks, const Options& opt);
 bool any_jit(const std::vector<IrKernel>& ks);
 JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt, std::string& err);
 void jit_destroy(JitModule* m);
+// The generated module of a summary set: source, per-bin (shape, constants).
+struct JitPlan {
+  std::string src;
+  std::vector<JitMeta> meta;   // [kernels + 1], bin order = ks order
+  std::vector<int64_t> consts;
+  std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
+  int nshapes = 0;
+};
+JitPlan jit_plan(const std::vector<IrKernel>& ks);
+// Stable-sort kernels by generated shape so neighbouring bins share code.
+void order_by_shape(std::vector<IrKernel>& ks);
+bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
+                 bool use_cache, std::string& err);
 
-cudaError_t launch_validate(const Tables& T, JitModule* jit, const Options& opt, const DevBatch& b,
-                            uint64_t n, uint8_t* flags, uint32_t* bits,
+cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options& opt,
+                            const DevBatch& b, uint64_t n, uint8_t* flags, uint32_t* bits,
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches);
 

@@ -466,6 +466,12 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
   unknown.shortcut = V_ERR_KERNEL;
   unknown.path = PATH_SHORTCUT;
   t.kernels.assign(ks.empty() ? 1 : maxid + 1, unknown);
+  t.bin_of.assign(t.kernels.size(), kNone16);
+  for (size_t i = 0; i < ks.size() && i < kNone16; ++i) t.bin_of[ks[i].id] = (uint16_t)i;
+  const uint32_t nb = (uint32_t)ks.size();
+  t.kb_unknown = nb | (nb << 16);
+  t.kb.assign(t.kernels.size(), t.kb_unknown);
+  for (uint32_t i = 0; i < nb; ++i) t.kb[ks[i].id] = i | (i << 16);
   for (auto& k : ks) {
     DKernel dk{};
     dk.shortcut = k.shortcut;

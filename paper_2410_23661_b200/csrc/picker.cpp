@@ -22,7 +22,7 @@ struct picker_ctx {
   HostTables ht;
   void* dev_tables = nullptr;
   size_t dev_tables_bytes = 0;
-  Tables T{};
+  BucketParams P{};
   Options opt;
   JitModule* jit = nullptr;
   // host-path staging (two pipelines)
@@ -124,9 +124,13 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   if (!c || !key) return PICKER_EINVAL;
   std::string k(key);
   if (k == "jit") c->opt.jit = v != 0;
-  else if (k == "wide_pairs") c->opt.wide_pairs = v;
+  else if (k == "bucket") c->opt.bucket = v != 0;
   else if (k == "force_path") c->opt.force_path = (int)v;
   else if (k == "tile") c->opt.tile = (int)v;
+  else if (k == "threads") c->opt.threads = (int)v;
+  else if (k == "ctas") c->opt.ctas = (int)v;
+  else if (k == "args_per_rec") c->opt.args_per_rec = (int)v;
+
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
@@ -142,6 +146,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
     ks = parse_summaries(text, len);
     for (auto& k : ks) verify_kernel(k);
     select_paths(ks, c->opt);
+    if (c->opt.jit && any_jit(ks)) order_by_shape(ks);
     flatten(ks, ht);
   } catch (const LoadError& e) {
     return fail(c, e.status, e.msg);
@@ -154,7 +159,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
          o_p = append_bytes(blob, ht.prods), o_b = append_bytes(blob, ht.bexprs),
          o_v = append_bytes(blob, ht.vars), o_t = append_bytes(blob, ht.terms),
          o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
-         o_l = append_bytes(blob, ht.varlist);
+         o_l = append_bytes(blob, ht.varlist), o_m = append_bytes(blob, ht.bin_of),
+         o_kb = append_bytes(blob, ht.kb);
   blob.resize(blob.size() + 256);
   void* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, blob.size());
@@ -179,16 +185,20 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->dev_tables = dev;
   c->dev_tables_bytes = blob.size();
   uint8_t* b = (uint8_t*)dev;
-  c->T.kernels = (const DKernel*)(b + o_k);
-  c->T.nkernel_slots = (uint32_t)ht.kernels.size();
-  c->T.checks = (const DCheck*)(b + o_c);
-  c->T.prods = (const DProd*)(b + o_p);
-  c->T.bexprs = (const DBexpr*)(b + o_b);
-  c->T.vars = (const DVar*)(b + o_v);
-  c->T.terms = (const DTerm*)(b + o_t);
-  c->T.guards = (const DGuard*)(b + o_g);
-  c->T.descs = (const DDesc*)(b + o_d);
-  c->T.varlist = (const uint16_t*)(b + o_l);
+  c->P.T.kernels = (const DKernel*)(b + o_k);
+  c->P.T.nkernel_slots = (uint32_t)ht.kernels.size();
+  c->P.T.checks = (const DCheck*)(b + o_c);
+  c->P.T.prods = (const DProd*)(b + o_p);
+  c->P.T.bexprs = (const DBexpr*)(b + o_b);
+  c->P.T.vars = (const DVar*)(b + o_v);
+  c->P.T.terms = (const DTerm*)(b + o_t);
+  c->P.T.guards = (const DGuard*)(b + o_g);
+  c->P.T.descs = (const DDesc*)(b + o_d);
+  c->P.T.varlist = (const uint16_t*)(b + o_l);
+  c->P.bin_of = (const uint16_t*)(b + o_m);
+  c->P.kb_of = (const uint32_t*)(b + o_kb);
+  c->P.kb_unknown = ht.kb_unknown;
+  c->P.nbins = (uint32_t)ks.size();
   c->ir = std::move(ks);
   c->ht = std::move(ht);
   c->loaded = true;
@@ -222,6 +232,41 @@ int picker_verify_summaries(const char* text, size_t len, char* msg, size_t msg_
   }
 }
 
+int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg_len,
+                             char* src_out, size_t src_len) {
+  auto put = [&](char* dst, size_t cap, const std::string& m) {
+    if (dst && cap) {
+      size_t k = std::min(m.size(), cap - 1);
+      memcpy(dst, m.data(), k);
+      dst[k] = 0;
+    }
+  };
+  try {
+    std::vector<IrKernel> ks = parse_summaries(text, len);
+    for (auto& k : ks) verify_kernel(k);
+    Options opt;
+    select_paths(ks, opt);
+    order_by_shape(ks);
+    JitPlan plan = jit_plan(ks);
+    std::string cubin, lowered, err;
+    if (!jit_compile(plan, opt, cubin, lowered, false, err)) {
+      put(msg, msg_len, err);
+      put(src_out, src_len, plan.src);
+      return PICKER_ECUDA;
+    }
+    put(msg, msg_len, "cubin " + std::to_string(cubin.size()) + " bytes, " +
+                          std::to_string(plan.consts.size()) + " constants, kernel " + lowered);
+    put(src_out, src_len, plan.src);
+    return plan.nshapes;
+  } catch (const LoadError& e) {
+    put(msg, msg_len, e.msg);
+    return e.status;
+  } catch (const std::exception& e) {
+    put(msg, msg_len, e.what());
+    return PICKER_EFORMAT;
+  }
+}
+
 int picker_kernel_info(picker_ctx_t* c, uint32_t* ids, uint8_t* paths, uint32_t cap) {
   if (!c) return PICKER_EINVAL;
   if (!c->loaded) return fail(c, PICKER_ENOTLOADED, "no summaries loaded");
@@ -250,7 +295,7 @@ int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, 
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
-  cudaError_t e = launch_validate(c->T, c->jit, c->opt, db, n, flags, bits,
+  cudaError_t e = launch_validate(c->P, c->jit, c->opt, db, n, flags, bits,
                                   (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
   if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
   return PICKER_OK;
@@ -336,7 +381,7 @@ int picker_validate_batch_host(picker_ctx_t* c, const picker_batch_t* b, uint64_
     DevBatch db = packed ? DevBatch{d_rec, d_args - lo, lo, hi}
                          : DevBatch{d_rec, whole_args, 0, b->args_len};
     int launches = 0;
-    e = launch_validate(c->T, c->jit, c->opt, db, m, d_flags, bits ? d_bits : nullptr,
+    e = launch_validate(c->P, c->jit, c->opt, db, m, d_flags, bits ? d_bits : nullptr,
                         c->dev_counts, c->num_sms, ss, &launches);
     if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
     c->last_launches += launches;
@@ -373,7 +418,7 @@ int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uin
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
   std::string err;
-  cudaError_t e = launch_exact(c->T, db, n, out, (unsigned long long*)counts, max_points,
+  cudaError_t e = launch_exact(c->P.T, db, n, out, (unsigned long long*)counts, max_points,
                                c->num_sms, s, &c->last_launches, err);
   if (e != cudaSuccess) return cuda_fail(c, e, ("exact check: " + err).c_str());
   return PICKER_OK;

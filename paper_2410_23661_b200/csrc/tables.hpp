@@ -8,7 +8,10 @@
 // one variable-bound slot per distinct (variable, bound lists) pair.
 #pragma once
 
+#ifndef __CUDACC_RTC__
 #include <cstdint>
+#endif
+#include "../../include/picker.h"
 
 namespace picker {
 
@@ -110,6 +113,64 @@ struct Tables {
   const DDesc* descs;
   const uint16_t* varlist;
 };
+
+// Records [0, n) at rec; argument slots valid at indices [args_lo, args_hi) of args.
+struct DevBatch {
+  const picker_rec_t* rec;
+  const int64_t* args;
+  uint64_t args_lo, args_hi;
+};
+
+// Per-bin entry of the specialised module (jit.cpp): which generated function
+// evaluates the bin and where its constants start.
+struct JitMeta {
+  uint32_t shape, koff, nparams, pad;
+};
+
+// Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
+struct BucketParams {
+  Tables T;
+  const uint16_t* bin_of;  // [T.nkernel_slots]: dense bin of each loaded kernel id, kNone16 if none
+  uint32_t nbins;          // bins 0..nbins-1 are kernels; bin nbins collects unknown ids
+  uint32_t nkeys;          // grouping keys 0..nkeys-1
+  const uint32_t* kb_of;   // [T.nkernel_slots]: bin | key << 16 of each kernel id
+  uint32_t kb_unknown;     // bin | key << 16 of an id that is not loaded
+  const JitMeta* jit_meta;     // [nbins + 1] (specialised module only)
+  const int64_t* jit_consts;   // per-kernel constants (specialised module only)
+};
+
+// Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads
+// per CTA (one CTA per SM), staged argument slots per tile buffer.
+// The specialised module is compiled with -DPICKER_TILE/THREADS/CTAS from the
+// load options (tuning only); the static library uses the defaults.
+#ifndef PICKER_TILE
+#define PICKER_TILE 512
+#endif
+#ifndef PICKER_THREADS
+#define PICKER_THREADS 256
+#endif
+#ifndef PICKER_CTAS
+#define PICKER_CTAS 2
+#endif
+#ifndef PICKER_ARGS_PER_REC
+#define PICKER_ARGS_PER_REC 8
+#endif
+constexpr int kTile = PICKER_TILE;
+constexpr int kThreads = PICKER_THREADS;
+constexpr int kWarps = kThreads / 32;
+constexpr int kCtasPerSm = PICKER_CTAS;
+constexpr int kArgCap = PICKER_TILE * PICKER_ARGS_PER_REC;  // staged argument slots per tile
+constexpr int kArgBufBytes = kArgCap * 8 + 16;              // + alignment slack
+constexpr size_t kMaxSmem = 227 * 1024;
+constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec) {
+  // 2 x (headers + args) staging buffers; s_key, s_bin, s_perm (u16) per record;
+  // s_cnt, s_off, s_cur (u32) per key; group table
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 6 +
+         (size_t)nkeys * 12 + ((size_t)tile / 32 + nkeys) * 4 + 128;
+}
+constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
+  return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC);
+}
 
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind

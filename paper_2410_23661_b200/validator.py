@@ -38,6 +38,16 @@ def verify_summaries(summary):
     return r, buf.value.decode()
 
 
+def compile_summaries(summary, want_source=False):
+    """Generate + NVRTC-compile the specialised module without a device.
+    Returns (n_functions_or_status, message, source)."""
+    t = summary_text(summary)
+    msg = ctypes.create_string_buffer(8192)
+    src = ctypes.create_string_buffer(1 << 24) if want_source else None
+    r = lib.picker_compile_summaries(t, len(t), msg, len(msg), src, len(src) if src is not None else 0)
+    return r, msg.value.decode(), (src.value.decode() if src is not None else None)
+
+
 def records_tensor(rec, device=None):
     """numpy structured records (tracegen.records.REC_DTYPE) or a uint8 tensor -> u8[n, 32]."""
     if isinstance(rec, np.ndarray):

@@ -1,0 +1,57 @@
+"""Sweep the specialised kernel's geometry (tile, threads, CTAs/SM) on the bench
+workload; prints instances/s per setting (tuning aid, not a bench line)."""
+import itertools
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2410_23661_b200 as pk  # noqa: E402
+from tracegen.workloads import make_c2, replicate  # noqa: E402
+
+
+def main():
+    reps = int(os.environ.get("REPLICAS", "686"))
+    s, rec, a, meta = make_c2()
+    R, A = replicate(rec, a, meta["ptr_mask"], reps, 1 << 37)
+    dev = torch.device("cuda", 0)
+    rd = torch.from_numpy(R.view(np.uint8).reshape(-1, 32)).to(dev)
+    ad = torch.from_numpy(A).to(dev)
+    n = len(R)
+    flags = torch.empty(n, dtype=torch.uint8, device=dev)
+    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    cnt = torch.empty(16, dtype=torch.int64, device=dev)
+    ref = None
+    grid = [(t, th, c, apr) for t, th, c, apr in itertools.product(
+        [256, 512, 1024], [128, 256, 512], [1, 2, 3, 4], [8])]
+    for t, th, c, apr in grid:
+        if th * c > 1024 or t < th:
+            continue
+        try:
+            p = pk.Picker(0, tile=t, threads=th, ctas=c, args_per_rec=apr)
+            p.load(s)
+        except Exception as e:  # noqa: BLE001
+            print(f"tile={t} threads={th} ctas={c}: {str(e)[:80]}")
+            continue
+        for _ in range(3):
+            p.validate(rd, ad, out=(flags, bits, cnt))
+        torch.cuda.synchronize()
+        if ref is None:
+            ref = flags.clone()
+        ok = bool(torch.equal(flags, ref))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(10):
+            p.validate(rd, ad, out=(flags, bits, cnt))
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        print(f"tile={t:5d} threads={th:4d} ctas={c} apr={apr}: {ms:7.3f} ms  {n / ms / 1e6:7.2f} G inst/s  "
+              f"same={ok}", flush=True)
+        p.close()
+
+
+if __name__ == "__main__":
+    main()

@@ -50,7 +50,7 @@ def _check_outputs(flags, bits, counts, want):
         assert np.array_equal(counts.cpu().numpy(), exp_c)
 
 
-PATH_OPTS = [dict(jit=0)]
+PATH_OPTS = [dict(jit=0, bucket=0), dict(jit=0, bucket=1), dict(jit=1)]
 
 
 @pytest.mark.parametrize("opt", PATH_OPTS, ids=str)
