@@ -172,8 +172,11 @@ int picker_validate_batch_host(picker_ctx_t* ctx, const picker_batch_t* batch, u
  * point (thread, induction and fresh variable) of every active symbolic
  * address and intersects the touched BYTES, so it has no range
  * overestimation (l.1170-1185).  Records with more than
- * max_points_per_instance points get code 11.  exact_out[n] and counts_out[16]
- * are device pointers (counts_out nullable).  Intended for small grids.     */
+ * max_points_per_instance points, or whose possibly-shared bytes (the hull of
+ * the pairwise read/write extent intersections) span more than 2^31 bytes, get
+ * code 11.  exact_out[n] and counts_out[16] are device pointers (counts_out
+ * nullable).  Intended for small grids.  Unlike the other calls this one is
+ * SYNCHRONOUS: it returns after the outputs are written.                     */
 int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                        uint8_t* exact_out, uint64_t* counts_out,
                        uint64_t max_points_per_instance, void* stream);

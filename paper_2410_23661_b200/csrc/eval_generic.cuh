@@ -16,7 +16,7 @@ namespace picker {
 
 // `rec_args` = the record's argument slots (args + r.arg_off, or its staged
 // shared-memory copy); [args_lo, args_hi) is the valid slot range of the pool.
-__device__ __noinline__ uint8_t eval_generic(const Tables& T, const picker_rec_t r,
+static __device__ __noinline__ uint8_t eval_generic(const Tables& T, const picker_rec_t r,
                                              const int64_t* rec_args, uint64_t args_lo,
                                              uint64_t args_hi) {
   const uint32_t kid = r.kernel_id;

@@ -541,12 +541,19 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
       for (auto& v : d.vars) {
         sid.push_back(slot_id(v));
         t.varlist.push_back(sid.back());
+        DVarDef vd{};
+        vd.op = v.def_op;
+        vd.src = (uint8_t)(v.def_src < 0 ? 0 : v.def_src);
+        vd.arg = v.def_arg;
+        t.vardef.push_back(vd);
       }
       dd.term = (uint32_t)t.terms.size();
       dd.nterm = (uint16_t)(d.opaque ? 0 : d.terms.size());
       if (!d.opaque)
-        for (auto& tm : d.terms)
+        for (auto& tm : d.terms) {
           t.terms.push_back(DTerm{prod_id(tm.c), tm.var < 0 ? kNone16 : sid[tm.var], (uint32_t)tm.div});
+          t.term_lvar.push_back((uint8_t)(tm.var < 0 ? 0xFF : tm.var));
+        }
       (d.kind == KIND_R ? dk.nr : dk.nw)++;
       t.descs.push_back(dd);
     }

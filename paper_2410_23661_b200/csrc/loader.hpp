@@ -95,6 +95,8 @@ struct HostTables {
   std::vector<DGuard> guards;
   std::vector<DDesc> descs;
   std::vector<uint16_t> varlist;
+  std::vector<DVarDef> vardef;
+  std::vector<uint8_t> term_lvar;
   std::vector<uint16_t> bin_of;  // kernel id -> index in the summary (kNone16: not loaded)
   std::vector<uint32_t> kb;      // kernel id -> bin | bin << 16 (table-driven grouping key)
   uint32_t kb_unknown = 0;

@@ -160,7 +160,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
          o_v = append_bytes(blob, ht.vars), o_t = append_bytes(blob, ht.terms),
          o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
          o_l = append_bytes(blob, ht.varlist), o_m = append_bytes(blob, ht.bin_of),
-         o_kb = append_bytes(blob, ht.kb);
+         o_kb = append_bytes(blob, ht.kb), o_vd = append_bytes(blob, ht.vardef),
+         o_tl = append_bytes(blob, ht.term_lvar);
   blob.resize(blob.size() + 256);
   void* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, blob.size());
@@ -197,6 +198,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.T.varlist = (const uint16_t*)(b + o_l);
   c->P.bin_of = (const uint16_t*)(b + o_m);
   c->P.kb_of = (const uint32_t*)(b + o_kb);
+  c->P.T.vardef = (const DVarDef*)(b + o_vd);
+  c->P.T.term_lvar = (const uint8_t*)(b + o_tl);
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
   c->ir = std::move(ks);

@@ -100,6 +100,16 @@ struct DKernel {  // 64 B
 };
 static_assert(sizeof(DKernel) == 64, "DKernel layout");
 
+enum : uint8_t { DEF_OP_NONE = 0, DEF_OP_MOD = 1, DEF_OP_AND = 2 };
+
+// Exact-verifier extras, parallel to varlist[] / terms[] (picker_exact_check).
+struct DVarDef {  // a fresh variable defined from another variable of the descriptor   (16 B)
+  uint8_t op;     // 0: free variable (enumerated); 1: src mod arg; 2: src and arg
+  uint8_t src;    // index of the source variable within the descriptor
+  uint8_t pad[6];
+  int64_t arg;
+};
+
 // Device-side view of all tables (passed by value to kernels).
 struct Tables {
   const DKernel* kernels;
@@ -112,6 +122,8 @@ struct Tables {
   const DGuard* guards;
   const DDesc* descs;
   const uint16_t* varlist;
+  const DVarDef* vardef;     // [varlist size]
+  const uint8_t* term_lvar;  // [terms size]: term's variable as an index into its descriptor's vars
 };
 
 // Records [0, n) at rec; argument slots valid at indices [args_lo, args_hi) of args.

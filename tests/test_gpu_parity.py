@@ -135,3 +135,43 @@ def test_unpacked_args(pk):
     p = _make(pk, s)
     flags, bits, counts = p.validate(rec2, args, packed=False)
     _check_outputs(flags, bits, counts, want)
+
+
+# ---- K3 exact verifier (picker_exact_check) vs oracle_exact ---------------------
+
+def test_exact_paper_examples(pk):
+    s = golden.golden_summary()
+    cases = json.load(open(os.path.join(HERE, "golden", "paper_examples.json")))["cases"]
+    b = RecordBuilder()
+    for c in cases:
+        b.add(c["kernel_id"], c["args"], c["grid"], c["block"])
+    rec, args = b.build()
+    p = _make(pk, s)
+    out, counts = p.exact_check(rec, args)
+    want = np.array([c["exact"] for c in cases], np.uint8)
+    assert np.array_equal(out.cpu().numpy(), want), (out.cpu().numpy(), want)
+    exp_c = np.zeros(16, np.int64)
+    for c in want:
+        exp_c[c if c <= 11 else 15] += 1
+    assert np.array_equal(counts.cpu().numpy(), exp_c)
+
+
+@pytest.mark.parametrize("seed", [201, 202, 203])
+def test_exact_random(pk, seed):
+    """Byte-set intersection on the GPU == the oracle's Python sets, including
+    the point cap (code 11) and range-overestimation records (interval 10,
+    exact 0)."""
+    cap = 1 << 12
+    s = random_summary(seed, n_kernels=30)
+    rec, args = random_records(seed + 5, s, 1500, max_threads=32, max_grid=4)
+    want = _oracle_codes(s, rec, args, O.oracle_exact, cap=cap)
+    inter = _oracle_codes(s, rec, args)
+    p = _make(pk, s)
+    out, _ = p.exact_check(rec, args, max_points=cap)
+    got = out.cpu().numpy()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+    # range overestimation exists in these traces and is measured exactly
+    assert ((inter == 10) & (got == 0)).sum() > 0
+    # no false positives: interval idempotent => exact idempotent
+    assert not ((inter == 0) & (got == 10)).any()
