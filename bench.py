@@ -219,7 +219,7 @@ def main():
     def step():
         p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
         if world > 1:
-            pdist.gather_bits(bits, n_total)
+            pdist.gather_bits_equal(bits)
             pdist.reduce_counts(counts)
 
     # parity of the timed configuration: the base trace's oracle codes, tiled (G9)
@@ -256,7 +256,7 @@ def main():
         kev[i][1].record(stream)
         launches += p.last_launch_count()
         if world > 1:
-            pdist.gather_bits(bits, n_total)
+            pdist.gather_bits_equal(bits)
             pdist.reduce_counts(counts)
         ev[i][1].record(stream)
     t_all1.record(stream)

@@ -49,6 +49,15 @@ def gather_bits(local_bits: torch.Tensor, n: int, group=None) -> torch.Tensor:
     return torch.cat(parts)
 
 
+def gather_bits_equal(local_bits: torch.Tensor, group=None) -> torch.Tensor:
+    """All-gather when every rank holds a shard of the same size (rank-major
+    result; each rank's mask ends on a word boundary, its pad bits are 0)."""
+    world = dist.get_world_size(group)
+    out = torch.empty(local_bits.numel() * world, dtype=local_bits.dtype, device=local_bits.device)
+    dist.all_gather_into_tensor(out, local_bits, group=group)
+    return out
+
+
 def reduce_counts(counts: torch.Tensor, group=None) -> torch.Tensor:
     dist.all_reduce(counts, op=dist.ReduceOp.SUM, group=group)
     return counts
