@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--path", default="auto", choices=["auto", "generic", "jit"])
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value (tuning)")
     return ap.parse_args()
 
 
@@ -205,6 +206,9 @@ def main():
     opts = {}
     if args.path == "generic":
         opts["jit"] = 0
+    for kv in args.opt:
+        k, v = kv.split("=")
+        opts[k] = int(v)
     p = pk.Picker(local, **opts)
     p.load(s)
     paths = p.kernel_paths()

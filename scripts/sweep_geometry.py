@@ -24,16 +24,15 @@ def main():
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     cnt = torch.empty(16, dtype=torch.int64, device=dev)
     ref = None
-    grid = [(t, th, c, apr) for t, th, c, apr in itertools.product(
-        [256, 512, 1024], [128, 256, 512], [1, 2, 3, 4], [8])]
-    for t, th, c, apr in grid:
-        if th * c > 1024 or t < th:
-            continue
+    cfgs = os.environ.get("CONFIGS", "512/512/1/4/4")
+    for cfg in cfgs.split(","):
+        t, th, c, st, bw = (int(x) for x in cfg.split("/"))
+        apr = 8
         try:
-            p = pk.Picker(0, tile=t, threads=th, ctas=c, args_per_rec=apr)
+            p = pk.Picker(0, tile=t, threads=th, ctas=c, args_per_rec=apr, stages=st, bwarps=bw)
             p.load(s)
         except Exception as e:  # noqa: BLE001
-            print(f"tile={t} threads={th} ctas={c}: {str(e)[:80]}")
+            print(f"{cfg}: {str(e)[:100]}")
             continue
         for _ in range(3):
             p.validate(rd, ad, out=(flags, bits, cnt))
@@ -48,7 +47,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        print(f"tile={t:5d} threads={th:4d} ctas={c} apr={apr}: {ms:7.3f} ms  {n / ms / 1e6:7.2f} G inst/s  "
+        print(f"tile={t:5d} threads={th:4d} ctas={c} stages={st} bwarps={bw}: {ms:7.3f} ms  {n / ms / 1e6:7.2f} G inst/s  "
               f"same={ok}", flush=True)
         p.close()
 
