@@ -417,8 +417,7 @@ void order_by_shape(std::vector<IrKernel>& ks) {
 std::vector<std::string> geometry_defines(const Options& opt) {
   return {"-DPICKER_TILE=" + std::to_string(opt.tile), "-DPICKER_THREADS=" + std::to_string(opt.threads),
           "-DPICKER_CTAS=" + std::to_string(opt.ctas),
-          "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
-          "-DPICKER_STAGES=" + std::to_string(opt.stages), "-DPICKER_BWARPS=" + std::to_string(opt.bwarps)};
+          "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec)};
 }
 
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
@@ -442,10 +441,9 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 }
 
 JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt, std::string& err) {
-  if (opt.tile < 32 || opt.tile % 32 || opt.tile > 2048 || opt.threads < 128 || opt.threads % 32 ||
-      opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1 || opt.stages < 2 ||
-      opt.stages > 8 || opt.threads < 32 * (opt.bwarps + 2) || opt.bwarps < 1) {
-    err = "invalid tile / threads / ctas / args_per_rec / stages options";
+  if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
+      opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1) {
+    err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
   JitPlan plan = jit_plan(ks);
@@ -481,8 +479,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt, std::s
     return nullptr;
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes;
-  m->smem = bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
-                                  (uint32_t)opt.stages);
+  m->smem = bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {
     err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";
     jit_destroy(m);

@@ -45,9 +45,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)
+      : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return ok != 0;
 }
@@ -117,277 +117,167 @@ __device__ __forceinline__ picker_rec_t rec_from_smem(const unsigned char* p) {
   return r;
 }
 
-// ---------------------------------------------------------------------------
-// The pipelined kernel.  Warp roles (no CTA-wide barrier in the steady state):
-//   warp 0       producer: lane 0 waits until a stage is empty, then issues the
-//                TMA bulk copies of the next tile into it (full[s] mbarrier);
-//   warps 1, 2   bucketers (tiles alternate): wait full[s], group the tile's
-//                records by key (counting sort in shared memory), write the
-//                stage's group table, publish ready_tile[s];
-//   warps 3..    consumers: claim groups of the oldest ready tile (tile-tagged
-//                64-bit counter), evaluate one group of <= 32 records of one key,
-//                emit codes / bits / histogram; the consumer that finishes the
-//                tile's last group writes its bit words and arrives on empty[s].
-// Consumers never wait for stragglers: a warp that finds no group left in a
-// tile moves on to the next one.
-// ---------------------------------------------------------------------------
-constexpr int kMaxStages = 8;
-
-struct StageCtl {
-  uint64_t full, empty;        // mbarriers
-  uint32_t claim, pad2;        // next group of the tile in `ngrp`
-  unsigned long long ngrp;     // (tile << 32) | group count
-  unsigned long long ready;    // tile + 1 once bucketed
-  uint32_t remaining;          // groups not yet finished
-  uint32_t pad;
-  StageInfo info;
-};
-
-__device__ __forceinline__ void fence_acq_rel_cta() { asm volatile("fence.acq_rel.cta;" ::: "memory"); }
-__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.release.cta.shared::cta.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
-}
-__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.acquire.cta.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(smem_u32(p)) : "memory");
-  return v;
-}
-__device__ __forceinline__ uint32_t atom_add_acq_rel_u32(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v)
-               : "memory");
-  return old;
-}
-__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long* p) {
-  return *reinterpret_cast<const volatile unsigned long long*>(p);
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// named barrier of the bucketer warps only (id 1; consumers never take part)
-__device__ __forceinline__ void bucket_sync() {
-  asm volatile("bar.sync 1, %0;" ::"r"(kBucketThreads) : "memory");
+// Lane 0 claims the next work item; the index is broadcast to the warp.
+__device__ __forceinline__ uint32_t warp_claim(uint32_t* counter) {
+  uint32_t g = 0;
+  if ((threadIdx.x & 31) == 0) g = atomicAdd(counter, 1u);
+  return __shfl_sync(0xffffffffu, g, 0);
 }
 
 template <class Dispatch>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k_validate_bucket(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B,
-                      uint64_t n, uint8_t* __restrict__ flags, uint32_t* __restrict__ bits,
-                      unsigned long long* __restrict__ counts) {
+                      uint64_t n, uint8_t* __restrict__ flags,
+                      uint32_t* __restrict__ bits, unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(128) unsigned char smem[];
-  __shared__ StageCtl ctl[kMaxStages];
-  __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   const uint32_t nk = P.nkeys;
+  // staging buffers: headers at smem + buf*kHdrBytes, args at smem + kArgOff + buf*kArgBufBytes
+  constexpr uint32_t kHdrBytes = kTile * 32;
+  constexpr uint32_t kArgOff = 2 * kHdrBytes;
+  uint16_t* s_key = reinterpret_cast<uint16_t*>(smem + kArgOff + 2 * kArgBufBytes);
+  uint16_t* s_bin = s_key + kTile;
+  uint16_t* s_perm = s_bin + kTile;
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_perm + kTile);
+  uint32_t* s_off = s_cnt + nk;
+  uint32_t* s_cur = s_off + nk;
+  uint32_t* s_grp = s_cur + nk;
+  __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
+  __shared__ uint32_t s_bits[kTile / 32];
+  __shared__ uint32_t s_wsum[2][kWarps];
+  __shared__ uint32_t s_ngrp, s_next;
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ StageInfo s_info[2];
+
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t G = gridDim.x;
-  // stage s: [headers | args | perm (u32 per record) | groups | bits]
-  const size_t sbytes = stage_bytes(nk);  // group table: kTile/32 + nk entries
-  auto stage_hdr = [&](int s) { return smem + (size_t)s * sbytes; };
-  auto stage_arg = [&](int s) { return smem + (size_t)s * sbytes + kTile * 32; };
-  auto stage_perm = [&](int s) {
-    return reinterpret_cast<uint32_t*>(smem + (size_t)s * sbytes + kTile * 32 + kArgBufBytes);
-  };
-  auto stage_bits = [&](int s) { return stage_perm(s) + kTile; };
-  auto stage_grp = [&](int s) { return stage_bits(s) + kTile / 32; };
-
   if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
-  if (tid < kStages) {
-    StageCtl& c = ctl[tid];
-    mbar_init(&c.full, 1);
-    mbar_init(&c.empty, 1);
-    c.claim = 0;
-    c.ngrp = 0;
-    c.ready = 0;
-    c.remaining = 0;
-  }
-  for (int s = 0; s < kStages; ++s)
-    for (int w = tid; w < kTile / 32; w += kThreads) stage_bits(s)[w] = 0;
+  if (tid < kTile / 32) s_bits[tid] = 0;
+  // arg_off bounds of a tile, loaded ahead of its staging
+  auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& lo_last, uint64_t& n_last) {
+    const uint64_t base = tile * kTile;
+    lo = lo_last = n_last = 0;
+    if (base < n) {
+      const uint64_t m = min((uint64_t)kTile, n - base);
+      lo = __ldg(&B.rec[base].arg_off);
+      lo_last = __ldg(&B.rec[base + m - 1].arg_off);
+      n_last = __ldg(&B.rec[base + m - 1].nargs);
+    }
+  };
   if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int b = 0; b < 2; ++b) {
+      uint64_t lo, ll, nl;
+      bounds(blockIdx.x + b * G, lo, ll, nl);
+      stage_tile(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, smem + kArgOff + b * kArgBufBytes,
+                 &s_bar[b], &s_info[b], lo, ll, nl);
+    }
   }
   __syncthreads();
 
-  if (warp == 0) {
-    // ---------------- producer ----------------
-    if (lane == 0) {
-      // argument-span bounds of a tile (two header fields of its first and last
-      // record), loaded one tile ahead so their latency overlaps the empty wait
-      auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& ll, uint64_t& nl) {
-        lo = ll = nl = 0;
-        if (tile < ntiles) {
-          const uint64_t base = tile * kTile, m = min((uint64_t)kTile, n - base);
-          lo = __ldg(&B.rec[base].arg_off);
-          ll = __ldg(&B.rec[base + m - 1].arg_off);
-          nl = __ldg(&B.rec[base + m - 1].nargs);
-        }
-      };
-      uint64_t lo, ll, nl;
-      bounds(blockIdx.x, lo, ll, nl);
-      for (uint64_t k = 0;; ++k) {
-        const uint64_t tile = blockIdx.x + k * G;
-        if (tile >= ntiles) break;
-        const int s = (int)(k % kStages);
-        const uint64_t clo = lo, cll = ll, cnl = nl;
-        bounds(tile + G, lo, ll, nl);
-        if (k >= (uint64_t)kStages) {
-          mbar_wait(&ctl[s].empty, (uint32_t)((k / kStages - 1) & 1));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        stage_tile(B, n, tile, stage_hdr(s), stage_arg(s), &ctl[s].full, &ctl[s].info, clo, cll, cnl);
-      }
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
+    const uint32_t buf = it & 1, parity = (it >> 1) & 1;
+    const uint64_t base = tile * kTile;
+    const int m = (int)min((uint64_t)kTile, n - base);
+    uint64_t nlo = 0, nll = 0, nnl = 0;
+    if (tid == 0) bounds(tile + 2 * G, nlo, nll, nnl);  // consumed after this tile
+    for (uint32_t b = tid; b < nk; b += kThreads) s_cnt[b] = 0;
+    mbar_wait(&s_bar[buf], parity);
+    const unsigned char* hdr = smem + buf * kHdrBytes;
+    const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
+    const StageInfo si = s_info[buf];
+    __syncthreads();
+
+    // 1. keys
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
+      const uint32_t kb = kid < P.T.nkernel_slots ? __ldg(P.kb_of + kid) : P.kb_unknown;
+      const uint32_t key = kb >> 16;
+      s_bin[i] = (uint16_t)(kb & 0xFFFFu);
+      s_key[i] = (uint16_t)key;
+      atomicAdd(s_cnt + key, 1u);
     }
-  } else if (warp <= kBucketWarps) {
-    // ---------------- bucketers (warps 1..kBucketWarps, one tile at a time) ----------------
-    const int bt = tid - 32;  // 0 .. kBucketThreads-1
-    uint32_t* sc_kb = reinterpret_cast<uint32_t*>(smem + (size_t)kStages * sbytes);
-    uint32_t* cnt = sc_kb + kTile;
-    uint32_t* off = cnt + nk;
-    __shared__ uint32_t s_ngroups;
-    for (uint64_t k = 0;; ++k) {
-      const uint64_t tile = blockIdx.x + k * G;
-      if (tile >= ntiles) break;
-      const int s = (int)(k % kStages);
-      const int m = (int)min((uint64_t)kTile, n - tile * kTile);
-      for (uint32_t i = bt; i < nk; i += kBucketThreads) cnt[i] = 0;
-      mbar_wait(&ctl[s].full, (uint32_t)((k / kStages) & 1));
-      bucket_sync();
-      const unsigned char* hdr = stage_hdr(s);
-      // keys and per-key counts
-      for (int i0 = (bt & ~31); i0 < m; i0 += kBucketThreads) {
-        const int i = i0 + lane;
-        const bool valid = i < m;
-        const unsigned mask = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-          const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
-          const uint32_t kb = kid < P.T.nkernel_slots ? __ldg(P.kb_of + kid) : P.kb_unknown;
-          sc_kb[i] = kb;
-          const uint32_t key = kb >> 16;
-          const unsigned same = __match_any_sync(mask, key);
-          if ((__ffs(same) - 1) == lane) atomicAdd(cnt + key, (uint32_t)__popc(same));
-        }
+    __syncthreads();
+
+    // 2. scans: record offsets and 32-record groups per key
+    {
+      const uint32_t per = (nk + kThreads - 1) / kThreads;
+      const uint32_t b0 = min(nk, tid * per), b1 = min(nk, b0 + per);
+      uint32_t rs = 0, gs = 0;
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t c = s_cnt[b];
+        rs += c;
+        gs += (c + 31) >> 5;
       }
-      bucket_sync();
-      // one warp: exclusive scans of counts and 32-record groups; group table
-      uint32_t* grp = stage_grp(s);
-      if (warp == 1) {
-        const uint32_t per = (nk + 31) / 32;
-        const uint32_t b0 = min(nk, lane * per), b1 = min(nk, b0 + per);
-        uint32_t rs = 0, gs = 0;
-        for (uint32_t q = b0; q < b1; ++q) {
-          rs += cnt[q];
-          gs += (cnt[q] + 31) >> 5;
-        }
-        uint32_t ri = rs, gi = gs;
+      uint32_t ri = rs, gi = gs;  // inclusive warp scans
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t r2 = __shfl_up_sync(0xffffffffu, ri, d), g2 = __shfl_up_sync(0xffffffffu, gi, d);
-          if (lane >= d) ri += r2, gi += g2;
-        }
-        if (lane == 31) s_ngroups = gi;
-        uint32_t ro = ri - rs, go = gi - gs;
-        for (uint32_t q = b0; q < b1; ++q) {
-          const uint32_t c = cnt[q];
-          off[q] = ro;
-          for (uint32_t j = 0; 32 * j < c; ++j)
-            grp[go++] = (ro + 32 * j) | ((min(32u, c - 32 * j) - 1) << 11) | (q << 16);
-          ro += c;
-        }
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t r2 = __shfl_up_sync(0xffffffffu, ri, d), g2 = __shfl_up_sync(0xffffffffu, gi, d);
+        if (lane >= d) ri += r2, gi += g2;
       }
-      bucket_sync();
-      // scatter record indices (and bins) into key order
-      uint32_t* perm = stage_perm(s);
-      for (int i0 = (bt & ~31); i0 < m; i0 += kBucketThreads) {
-        const int i = i0 + lane;
-        const bool valid = i < m;
-        const unsigned mask = __ballot_sync(0xffffffffu, valid);
-        if (valid) {
-          const uint32_t kb = sc_kb[i];
-          const uint32_t key = kb >> 16;
-          const unsigned same = __match_any_sync(mask, key);
-          const int leader = __ffs(same) - 1;
-          uint32_t pos0 = 0;
-          if (leader == lane) pos0 = atomicAdd(off + key, (uint32_t)__popc(same));
-          pos0 = __shfl_sync(same, pos0, leader);
-          const uint32_t rank = __popc(same & ((1u << lane) - 1));
-          perm[pos0 + rank] = (uint32_t)i | ((kb & 0xFFFFu) << 16);
-        }
+      if (lane == 31) s_wsum[0][warp] = ri, s_wsum[1][warp] = gi;
+      __syncthreads();
+      uint32_t ro = ri - rs, go = gi - gs;
+      for (int w = 0; w < warp; ++w) ro += s_wsum[0][w], go += s_wsum[1][w];
+      for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t c = s_cnt[b];
+        s_off[b] = ro;
+        s_cur[b] = ro;
+        const uint32_t ng = (c + 31) >> 5;
+        for (uint32_t j = 0; j < ng; ++j) s_grp[go + j] = (b << 8) | j;
+        ro += c;
+        go += ng;
       }
-      bucket_sync();
-      if (bt == 0) {
-        const uint32_t ngroups = s_ngroups;
-        // tag first, then the claim counter: a consumer whose claim hits the reset
-        // counter is guaranteed to read the new tag (and skip a tile it does not own)
-        ctl[s].remaining = ngroups;
-        ctl[s].ngrp = ((unsigned long long)tile << 32) | ngroups;
-        fence_acq_rel_cta();
-        ctl[s].claim = 0;
-        st_release_u64(&ctl[s].ready, tile + 1);
-      }
+      if (tid == kThreads - 1) s_ngrp = go, s_next = 0;
     }
-  } else {
-    // ---------------- consumers ----------------
-    for (uint64_t k = 0;; ++k) {
-      const uint64_t tile = blockIdx.x + k * G;
-      if (tile >= ntiles) break;
-      const int s = (int)(k % kStages);
-      if (lane == 0)
-        while (ld_acquire_u64(&ctl[s].ready) < tile + 1) __nanosleep(64);
-      __syncwarp();
-      const uint64_t base = tile * kTile;
-      const unsigned char* hdr = stage_hdr(s);
-      const unsigned char* sarg = stage_arg(s);
-      const uint32_t* perm = stage_perm(s);
-      const uint32_t* grp = stage_grp(s);
-      uint32_t* sbits = stage_bits(s);
-      const StageInfo si = ctl[s].info;
-      for (;;) {
-        uint32_t g = 0;
-        unsigned long long ng = 0;
-        if (lane == 0) {
-          g = atom_add_acq_rel_u32(&ctl[s].claim, 1u);
-          ng = ld_volatile_u64(&ctl[s].ngrp);
-        }
-        g = __shfl_sync(0xffffffffu, g, 0);
-        ng = __shfl_sync(0xffffffffu, ng, 0);
-        if ((ng >> 32) != tile || g >= (uint32_t)ng) break;  // no group left / stage reused
-        const uint32_t e = grp[g];
-        const uint32_t start = e & 0x7FFu, cnt = ((e >> 11) & 31u) + 1, key = e >> 16;
-        const bool on = (uint32_t)lane < cnt;
-        uint8_t code = 0;
-        if (on) {
-          const uint32_t pe = perm[start + lane];
-          const uint32_t li = pe & 0xFFFFu, bin = pe >> 16;
-          const picker_rec_t r = rec_from_smem(hdr + 32 * li);
-          const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
-                             (uint64_t)r.nargs <= si.hi - r.arg_off;
-          const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
-                                   : B.args + r.arg_off;
-          code = Dispatch::eval(key, bin, P, r, a, B);
-          flags[base + li] = code;
-          if (code <= V_IDEM_KERNEL) atomicOr(sbits + (li >> 5), 1u << (li & 31));
-        }
-        const int hb = on ? count_bin(code) : 16;
-        const unsigned same = __match_any_sync(0xffffffffu, hb);
-        if (on && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
-        __syncwarp();
-        uint32_t left = 0;
-        if (lane == 0) left = atom_add_acq_rel_u32(&ctl[s].remaining, 0xFFFFFFFFu);  // -1
-        left = __shfl_sync(0xffffffffu, left, 0);
-        if (left == 1) {  // this warp finished the tile's last group
-          const int m = (int)min((uint64_t)kTile, n - base);
-          for (int w = lane; w < (m + 31) / 32; w += 32) {
-            const uint32_t v = *reinterpret_cast<volatile uint32_t*>(sbits + w);
-            if (bits) bits[(base >> 5) + w] = v;
-            sbits[w] = 0;
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&ctl[s].empty);
-        }
+    __syncthreads();
+
+    // 3. scatter record indices into key order
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t pos = atomicAdd(s_cur + s_key[i], 1u);
+      s_perm[pos] = (uint16_t)i;
+    }
+    __syncthreads();
+
+    // 4. evaluate one 32-record group of one key per warp (warps claim groups
+    //    dynamically: groups of different shapes cost different amounts) and
+    //    emit: the u8 code, the idempotent bit (shared atomics into the tile's
+    //    bit words) and the histogram (match_any-aggregated shared atomics)
+    const uint32_t ngrp = s_ngrp;
+    for (uint32_t g = warp_claim(&s_next); g < ngrp; g = warp_claim(&s_next)) {
+      const uint32_t e = s_grp[g];
+      const uint32_t key = e >> 8, j = e & 255u;
+      const uint32_t cnt = s_cnt[key] - 32u * j;
+      const bool on = (uint32_t)lane < cnt;
+      uint8_t code = 0;
+      uint32_t li = 0;
+      if (on) {
+        li = s_perm[s_off[key] + 32u * j + lane];
+        const picker_rec_t r = rec_from_smem(hdr + 32 * li);
+        const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                           (uint64_t)r.nargs <= si.hi - r.arg_off;
+        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                 : B.args + r.arg_off;
+        code = Dispatch::eval(key, s_bin[li], P, r, a, B);
+        flags[base + li] = code;
+        if (code <= V_IDEM_KERNEL) atomicOr(s_bits + (li >> 5), 1u << (li & 31));
       }
+      const int hb = on ? count_bin(code) : 16;
+      const unsigned same = __match_any_sync(0xffffffffu, hb);
+      if (on && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
+    }
+    __syncthreads();
+    // this tile's buffers are free: start the copy of the tile after next
+    if (tid == 0)
+      stage_tile(B, n, tile + 2 * G, smem + buf * kHdrBytes, smem + kArgOff + buf * kArgBufBytes,
+                 &s_bar[buf], &s_info[buf], nlo, nll, nnl);
+    if (tid < (m + 31) / 32) {
+      if (bits) bits[(base >> 5) + tid] = s_bits[tid];
+      s_bits[tid] = 0;
     }
   }
   __syncthreads();

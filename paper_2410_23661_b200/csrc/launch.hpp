@@ -19,7 +19,7 @@ struct Options {
   bool bucket = true;  // group each tile's records by kernel before evaluating
   int force_path = 0;  // 0 auto, 1 generic (table-driven) for every COND kernel
   // geometry of the specialised kernel (tuning; k_bucket.cuh)
-  int tile = 512, threads = 512, ctas = 1, args_per_rec = 8, stages = 4, bwarps = 4;
+  int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;
 };
 
 struct JitModule;

@@ -130,8 +130,6 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "threads") c->opt.threads = (int)v;
   else if (k == "ctas") c->opt.ctas = (int)v;
   else if (k == "args_per_rec") c->opt.args_per_rec = (int)v;
-  else if (k == "stages") c->opt.stages = (int)v;
-  else if (k == "bwarps") c->opt.bwarps = (int)v;
 
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;

@@ -159,43 +159,29 @@ struct BucketParams {
 #define PICKER_TILE 512
 #endif
 #ifndef PICKER_THREADS
-#define PICKER_THREADS 512
+#define PICKER_THREADS 256
 #endif
 #ifndef PICKER_CTAS
-#define PICKER_CTAS 1
+#define PICKER_CTAS 2
 #endif
 #ifndef PICKER_ARGS_PER_REC
 #define PICKER_ARGS_PER_REC 8
 #endif
-#ifndef PICKER_STAGES
-#define PICKER_STAGES 4
-#endif
-constexpr int kTile = PICKER_TILE;        // records per tile (<= 2048: group entries use 11 bits)
-constexpr int kThreads = PICKER_THREADS;  // warp 0 producer, warps 1-2 bucketers, the rest consumers
+constexpr int kTile = PICKER_TILE;
+constexpr int kThreads = PICKER_THREADS;
 constexpr int kWarps = kThreads / 32;
 constexpr int kCtasPerSm = PICKER_CTAS;
-constexpr int kStages = PICKER_STAGES;    // staged tiles in flight per CTA
-#ifndef PICKER_BWARPS
-#define PICKER_BWARPS 4
-#endif
-constexpr int kBucketWarps = PICKER_BWARPS;  // warps 1..kBucketWarps group each tile
-constexpr int kBucketThreads = 32 * kBucketWarps;
-static_assert(kThreads >= 32 * (kBucketWarps + 2), "need a producer, the bucketers and consumers");
 constexpr int kArgCap = PICKER_TILE * PICKER_ARGS_PER_REC;  // staged argument slots per tile
 constexpr int kArgBufBytes = kArgCap * 8 + 16;              // + alignment slack
 constexpr size_t kMaxSmem = 227 * 1024;
-// one stage: headers | args | perm (u32 / record) | bit words | group table (tile/32 + nkeys)
-constexpr size_t stage_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec) {
-  return ((size_t)tile * 32 + ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 4 + (size_t)tile / 32 * 4 +
-          ((size_t)tile / 32 + nkeys) * 4 + 127) & ~(size_t)127;
-}
-constexpr size_t stage_bytes(uint32_t nkeys) { return stage_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC); }
-constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec, uint32_t stages) {
-  // stages + the bucketers' scratch (key/bin per record, count and offset per key)
-  return (size_t)stages * stage_bytes_for(nkeys, tile, args_per_rec) + (size_t)(tile + 2 * nkeys) * 4 + 128;
+constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec) {
+  // 2 x (headers + args) staging buffers; s_key, s_bin, s_perm (u16) per record;
+  // s_cnt, s_off, s_cur (u32) per key; group table
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 6 +
+         (size_t)nkeys * 12 + ((size_t)tile / 32 + nkeys) * 4 + 128;
 }
 constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
-  return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC, kStages);
+  return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC);
 }
 
 // Generic-path limits (a kernel beyond them uses the wide path).

@@ -24,12 +24,11 @@ def main():
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     cnt = torch.empty(16, dtype=torch.int64, device=dev)
     ref = None
-    cfgs = os.environ.get("CONFIGS", "512/512/1/4/4")
+    cfgs = os.environ.get("CONFIGS", "512/256/2/8")
     for cfg in cfgs.split(","):
-        t, th, c, st, bw = (int(x) for x in cfg.split("/"))
-        apr = 8
+        t, th, c, apr = (int(x) for x in cfg.split("/"))
         try:
-            p = pk.Picker(0, tile=t, threads=th, ctas=c, args_per_rec=apr, stages=st, bwarps=bw)
+            p = pk.Picker(0, tile=t, threads=th, ctas=c, args_per_rec=apr)
             p.load(s)
         except Exception as e:  # noqa: BLE001
             print(f"{cfg}: {str(e)[:100]}")
@@ -47,7 +46,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 10
-        print(f"tile={t:5d} threads={th:4d} ctas={c} stages={st} bwarps={bw}: {ms:7.3f} ms  {n / ms / 1e6:7.2f} G inst/s  "
+        print(f"tile={t:5d} threads={th:4d} ctas={c} apr={apr}: {ms:7.3f} ms  {n / ms / 1e6:7.2f} G inst/s  "
               f"same={ok}", flush=True)
         p.close()
 
