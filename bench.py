@@ -94,16 +94,33 @@ class ClockSampler:
         self._t = None
 
     def start(self):
+        # NVML (what nvidia-smi reads) every ~2 ms: the timed region is tens of ms
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            bits = [0x8, 0x40, 0x20, 0x4]  # hw_slowdown, hw_thermal, sw_thermal, sw_power_cap
+
+            def sample():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                rs = pynvml.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                return [str(sm), str(mx)] + ["Active" if rs & b else "Not Active" for b in bits]
+        except Exception:
+            def sample():
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+                return [x.strip() for x in out.strip().split(",")]
+
         def run():
             while not self._stop.is_set():
                 try:
-                    out = subprocess.run(
-                        ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                         "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
-                    self.rows.append([x.strip() for x in out.strip().split(",")])
+                    self.rows.append(sample())
                 except Exception:
                     pass
-                self._stop.wait(0.1)
+                self._stop.wait(0.002)
 
         self._t = threading.Thread(target=run, daemon=True)
         self._t.start()

@@ -1,0 +1,242 @@
+// Table-driven per-descriptor helpers (shared by the exact verifier and the
+// wide path) and K2: the warp-cooperative wide evaluator.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace picker {
+
+static __device__ __forceinline__ int64_t prod_val(const Tables& T, const DKernel& K, const RecVals& X,
+                                                   uint16_t j) {
+  const DProd p = T.prods[K.prod + j];
+  return mul64(mul64(p.k, X.get(p.a)), X.get(p.b));
+}
+
+// [lo, hi] of variable slot s: structural bounds tightened by the declared
+// bound expressions.
+static __device__ __forceinline__ void slot_bounds(const Tables& T, const DKernel& K, const RecVals& X,
+                                                   uint16_t s, int64_t& lo, int64_t& hi) {
+  const DVar v = T.vars[K.var + s];
+  lo = (-9223372036854775807LL - 1);
+  hi = 9223372036854775807LL;
+  if (v.skind != SK_NONE) {
+    const int64_t g = X.get(OPD_GX + v.axis), b = X.get(OPD_BX + v.axis);
+    lo = 0;
+    hi = (v.skind == SK_TID ? b : v.skind == SK_BID ? g : g * b) - 1;
+  }
+  auto B = [&](const DBexpr& e) {
+    int64_t x = e.k0;
+    if (e.p0 != kNone16) x = add64(x, prod_val(T, K, X, e.p0));
+    if (e.p1 != kNone16) x = add64(x, prod_val(T, K, X, e.p1));
+    return x;
+  };
+  for (int j = 0; j < v.nlo; ++j) lo = max64(lo, B(T.bexprs[v.bex + j]));
+  for (int j = 0; j < v.nhi; ++j) hi = min64(hi, B(T.bexprs[v.bex + v.nlo + j]));
+}
+
+// guard holds and no variable range is empty
+static __device__ __forceinline__ bool desc_active(const Tables& T, const DKernel& K, const DDesc& D,
+                                                   const RecVals& X) {
+  for (int g = 0; g < D.nguard; ++g) {
+    const DGuard G = T.guards[D.guard + g];
+    if (!cmp64(X.get(G.a), G.cmp, G.b == OPD_NONE ? G.bconst : X.get(G.b))) return false;
+  }
+  for (int v = 0; v < D.nvar; ++v) {
+    int64_t lo, hi;
+    slot_bounds(T, K, X, T.varlist[D.var + v], lo, hi);
+    if (lo > hi) return false;
+  }
+  return true;
+}
+
+// byte extent [lb, ub] of a non-opaque descriptor
+static __device__ void desc_extent(const Tables& T, const DKernel& K, const DDesc& D, const RecVals& X,
+                                   int64_t& lb, int64_t& ub) {
+  lb = D.base == OPD_NONE ? 0 : X.get(D.base);
+  ub = lb;
+  for (int t = 0; t < D.nterm; ++t) {
+    const DTerm tm = T.terms[D.term + t];
+    const int64_t c = prod_val(T, K, X, tm.prod);
+    if (tm.var == kNone16) {
+      lb = add64(lb, c), ub = add64(ub, c);
+      continue;
+    }
+    int64_t lo, hi;
+    slot_bounds(T, K, X, tm.var, lo, hi);
+    const int64_t a = mul64(c, floordiv64(lo, tm.div)), b = mul64(c, floordiv64(hi, tm.div));
+    lb = add64(lb, min64(a, b));
+    ub = add64(ub, max64(a, b));
+  }
+  ub = add64(ub, (int64_t)D.width - 1);
+}
+
+// The checks that precede any address (kernel id, arity, class, launch limits,
+// preconditions, global condition).  Returns the verdict, or kContinue.
+constexpr uint32_t kContinue = 0x100;
+static __device__ __forceinline__ uint32_t record_prefix(const Tables& T, const picker_rec_t& r,
+                                                         uint64_t alo, uint64_t ahi, DKernel& K,
+                                                         const RecVals& X) {
+  const uint32_t kid = r.kernel_id;
+  if (kid >= T.nkernel_slots) return V_ERR_KERNEL;
+  K = T.kernels[kid];
+  if (K.shortcut == V_ERR_KERNEL) return V_ERR_KERNEL;
+  if (!args_in_range(r, K.nparams, alo, ahi)) return V_ERR_ARITY;
+  if (K.shortcut) return K.shortcut;
+  if (!launch_limits_ok(X)) return V_NI_PRECOND;
+  for (int c = 0; c < K.npre + K.nglob; ++c) {
+    const DCheck ch = T.checks[K.check + c];
+    const int64_t v = X.get(ch.op);
+    if (v < ch.lo || v > ch.hi) return c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
+  }
+  return kContinue;
+}
+
+// ---------------------------------------------------------------------------
+// K2: one warp evaluates one instance with many read/write sites (SURVEY §2.5:
+// cuDNN-like kernels with 16+ pointer arguments).  Lanes compute descriptor
+// extents in parallel; the read/write test is a sweep-line over the extents
+// sorted by lower bound: an extent overlaps an extent of the other kind iff,
+// in lb order, the running maximum ub of the other kind seen so far reaches
+// its lb (closed byte intervals; equal lbs overlap in any order).  Up to
+// 2 x 32 extents are sorted in registers by a warp bitonic network; records
+// with more active extents fall back to lanes over all read x write pairs.
+// The verdict equals the pairwise definition -- checked
+// against the oracle (tests, wide path forced).
+// ---------------------------------------------------------------------------
+struct Ext {
+  int64_t lb, ub;
+  uint32_t kind;  // 0 read, 1 write, 2 none (padding)
+};
+
+static __device__ __forceinline__ Ext shfl_ext(const Ext& e, int src) {
+  Ext o;
+  o.lb = __shfl_sync(0xffffffffu, e.lb, src);
+  o.ub = __shfl_sync(0xffffffffu, e.ub, src);
+  o.kind = __shfl_sync(0xffffffffu, e.kind, src);
+  return o;
+}
+static __device__ __forceinline__ Ext shfl_xor_ext(const Ext& e, int m) {
+  Ext o;
+  o.lb = __shfl_xor_sync(0xffffffffu, e.lb, m);
+  o.ub = __shfl_xor_sync(0xffffffffu, e.ub, m);
+  o.kind = __shfl_xor_sync(0xffffffffu, e.kind, m);
+  return o;
+}
+static __device__ __forceinline__ bool ext_less(const Ext& a, const Ext& b) {
+  // padding sorts last; order among equal lbs is irrelevant to the sweep
+  return a.kind != 2 && (b.kind == 2 || a.lb < b.lb);
+}
+
+// Bitonic sort of 64 elements held as (e0 = element lane, e1 = element 32 + lane).
+static __device__ __forceinline__ void warp_sort64(Ext& e0, Ext& e1, int lane) {
+  for (int k = 2; k <= 64; k <<= 1) {
+    for (int j = k >> 1; j > 0; j >>= 1) {
+      if (j == 32) {  // partner is the other register of the same lane
+        const bool up = true;  // k == 64 here: the whole sequence ascends
+        if (ext_less(e1, e0) == up) {
+          Ext t = e0;
+          e0 = e1;
+          e1 = t;
+        }
+        continue;
+      }
+      // element indices i = lane (+32); partner i ^ j lives in lane ^ j, same register
+      for (int h = 0; h < 2; ++h) {
+        Ext& e = h ? e1 : e0;
+        const int i = lane + 32 * h;
+        const Ext p = shfl_xor_ext(e, j);
+        const bool ascending = ((i & k) == 0);
+        const bool lower = (i & j) == 0;
+        // the lower index keeps the smaller (ascending) / larger (descending) element
+        const bool p_smaller = ext_less(p, e);
+        const bool take = lower ? (ascending ? p_smaller : ext_less(e, p)) : (ascending ? ext_less(e, p) : p_smaller);
+        if (take) e = p;
+      }
+    }
+  }
+}
+
+static __device__ __forceinline__ int64_t warp_incl_max(int64_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int64_t o = __shfl_up_sync(0xffffffffu, v, d);
+    if (lane >= d) v = max64(v, o);
+  }
+  return v;
+}
+
+// Overlap test over the sorted 64 elements: exclusive prefix max of ub per kind.
+static __device__ __forceinline__ bool sweep64(const Ext& e0, const Ext& e1, int lane) {
+  const int64_t NEG = (-9223372036854775807LL - 1);
+  bool hit = false;
+  int64_t carry_r = NEG, carry_w = NEG;
+  for (int h = 0; h < 2; ++h) {
+    const Ext& e = h ? e1 : e0;
+    const int64_t vr = e.kind == 0 ? e.ub : NEG, vw = e.kind == 1 ? e.ub : NEG;
+    const int64_t ir = max64(warp_incl_max(vr, lane), carry_r), iw = max64(warp_incl_max(vw, lane), carry_w);
+    int64_t xr = __shfl_up_sync(0xffffffffu, ir, 1), xw = __shfl_up_sync(0xffffffffu, iw, 1);
+    if (lane == 0) xr = carry_r, xw = carry_w;
+    if (e.kind == 0 && xw >= e.lb) hit = true;  // a write before it reaches its first byte
+    if (e.kind == 1 && xr >= e.lb) hit = true;
+    carry_r = __shfl_sync(0xffffffffu, ir, 31);
+    carry_w = __shfl_sync(0xffffffffu, iw, 31);
+  }
+  return __any_sync(0xffffffffu, hit);
+}
+
+// Verdict of one record, computed by the whole warp (all lanes return it).
+static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r, const int64_t* a,
+                                         uint64_t alo, uint64_t ahi, int lane) {
+  DKernel K;
+  const RecVals X(r, a, T.kernels[r.kernel_id < T.nkernel_slots ? r.kernel_id : 0].i32mask);
+  const uint32_t pre = record_prefix(T, r, alo, ahi, K, X);
+  if (pre != kContinue) return (uint8_t)pre;
+  // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags, extents
+  bool act_r = false, act_w = false, opq_r = false, opq_w = false;
+  int nact = 0;
+  for (int d = lane; d < K.ndesc; d += 32) {
+    const DDesc D = T.descs[K.desc + d];
+    if (!desc_active(T, K, D, X)) continue;
+    (D.kind == KIND_R ? act_r : act_w) = true;
+    if (D.opaque) (D.kind == KIND_R ? opq_r : opq_w) = true;
+    else ++nact;
+  }
+  act_r = __any_sync(0xffffffffu, act_r);
+  act_w = __any_sync(0xffffffffu, act_w);
+  opq_r = __any_sync(0xffffffffu, opq_r);
+  opq_w = __any_sync(0xffffffffu, opq_w);
+  if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
+  if (!__any_sync(0xffffffffu, nact > 2)) {
+    // <= 64 active extents in total (<= 2 per lane): sort + sweep
+    Ext e[2];
+    int c = 0;
+    e[0].kind = e[1].kind = 2;
+    e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
+    for (int d = lane; d < K.ndesc; d += 32) {
+      const DDesc D = T.descs[K.desc + d];
+      if (D.opaque || !desc_active(T, K, D, X)) continue;
+      desc_extent(T, K, D, X, e[c].lb, e[c].ub);
+      e[c].kind = D.kind == KIND_R ? 0 : 1;
+      ++c;
+    }
+    // element index of e[0] is lane, of e[1] is 32 + lane
+    warp_sort64(e[0], e[1], lane);
+    return sweep64(e[0], e[1], lane) ? V_NI_OVERLAP : V_IDEM_CHECKED;
+  }
+  // many active extents: lanes over all (read, write) descriptor pairs
+  const int nd = K.ndesc;
+  bool hit = false;
+  for (int p = lane; p < nd * nd && !__any_sync(__activemask(), hit); p += 32) {
+    const int i = p / nd, j = p % nd;
+    const DDesc Di = T.descs[K.desc + i], Dj = T.descs[K.desc + j];
+    if (Di.kind != KIND_R || Dj.kind != KIND_W || Di.opaque || Dj.opaque) continue;
+    if (!desc_active(T, K, Di, X) || !desc_active(T, K, Dj, X)) continue;
+    int64_t rl, ru, wl, wu;
+    desc_extent(T, K, Di, X, rl, ru);
+    desc_extent(T, K, Dj, X, wl, wu);
+    if (rl <= wu && wl <= ru) hit = true;
+  }
+  return __any_sync(0xffffffffu, hit) ? V_NI_OVERLAP : V_IDEM_CHECKED;
+}
+
+}  // namespace picker

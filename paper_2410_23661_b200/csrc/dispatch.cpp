@@ -30,18 +30,17 @@ void select_paths(std::vector<IrKernel>& ks, const Options& opt) {
       (d.kind == KIND_R ? nr : nw)++;
       nvars += d.vars.size();
     }
-    const bool fits_generic =
-        nr <= (size_t)kGenMaxDesc && nw <= (size_t)kGenMaxDesc && nvars <= (size_t)kGenMaxVar;
-    const bool fits_jit = (int64_t)(nr * nw) <= kJitMaxPairs;
-    if (opt.jit && fits_jit && opt.force_path != 1) {
+    (void)nvars;
+    const int64_t pairs = (int64_t)(nr * nw);
+    // many read x write pairs (cuDNN-like kernels with 16+ pointer arguments):
+    // the warp-cooperative sort + sweep path (K2, desc_eval.cuh)
+    const bool wide = opt.force_path == 3 || pairs > opt.wide_pairs || pairs > kJitMaxPairs;
+    if (wide && opt.force_path != 1 && opt.force_path != 2) {
+      k.path = PATH_WIDE;
+    } else if (opt.jit && opt.force_path != 1 && pairs <= kJitMaxPairs) {
       k.path = PATH_JIT;
-    } else if (fits_generic) {
-      k.path = PATH_GENERIC;
     } else {
-      throw LoadError{PICKER_EFORMAT,
-                      "kernel " + std::to_string(k.id) +
-                          ": too many descriptors for the table-driven path and the "
-                          "specialised path is disabled or the pair count is too large"};
+      k.path = PATH_GENERIC;  // eval_generic also handles kernels beyond its register arrays
     }
   }
 }
@@ -59,7 +58,7 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
   if (n == 0) return cudaSuccess;
   *launches += 1;
   if (jit) return launch_jit(jit, P, b, n, flags, bits, counts, num_sms, s);
-  if (opt.bucket && bucket_smem_bytes(P.nbins + 1) <= kMaxSmem)
+  if (opt.bucket && bucket_smem_bytes(P.nbins + 2) <= kMaxSmem)
     return launch_bucket_generic(P, b, n, flags, bits, counts, num_sms, s);
   return launch_generic(P.T, b, n, flags, bits, counts, num_sms, s);
 }

@@ -10,9 +10,37 @@
 // static kernels and by the NVRTC module (as the fallback of its dispatch).
 #pragma once
 
+#include "desc_eval.cuh"
 #include "device_common.cuh"
 
 namespace picker {
+
+// Kernels beyond the register arrays below: recompute extents per pair instead
+// of storing them (same verdict, slower; only reached on the table path).
+static __device__ __noinline__ uint8_t eval_nostore(const Tables& T, const DKernel& K, const RecVals& X) {
+  bool act_r = false, act_w = false, opq_r = false, opq_w = false;
+  for (int d = 0; d < K.ndesc; ++d) {
+    const DDesc D = T.descs[K.desc + d];
+    if (!desc_active(T, K, D, X)) continue;
+    (D.kind == KIND_R ? act_r : act_w) = true;
+    if (D.opaque) (D.kind == KIND_R ? opq_r : opq_w) = true;
+  }
+  if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
+  for (int i = 0; i < K.ndesc; ++i) {
+    const DDesc Di = T.descs[K.desc + i];
+    if (Di.kind != KIND_R || Di.opaque || !desc_active(T, K, Di, X)) continue;
+    int64_t rl, ru;
+    desc_extent(T, K, Di, X, rl, ru);
+    for (int j = 0; j < K.ndesc; ++j) {
+      const DDesc Dj = T.descs[K.desc + j];
+      if (Dj.kind != KIND_W || Dj.opaque || !desc_active(T, K, Dj, X)) continue;
+      int64_t wl, wu;
+      desc_extent(T, K, Dj, X, wl, wu);
+      if (rl <= wu && wl <= ru) return V_NI_OVERLAP;
+    }
+  }
+  return V_IDEM_CHECKED;
+}
 
 // `rec_args` = the record's argument slots (args + r.arg_off, or its staged
 // shared-memory copy); [args_lo, args_hi) is the valid slot range of the pool.
@@ -33,6 +61,7 @@ static __device__ __noinline__ uint8_t eval_generic(const Tables& T, const picke
     const int64_t v = X.get(ch.op);
     if (v < ch.lo || v > ch.hi) return c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
   }
+  if (K.nr > kGenMaxDesc || K.nw > kGenMaxDesc || K.nvar > kGenMaxVar) return eval_nostore(T, K, X);
 
   auto P = [&](uint16_t j) -> int64_t {
     const DProd p = T.prods[K.prod + j];

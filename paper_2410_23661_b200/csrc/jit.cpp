@@ -58,7 +58,8 @@ struct JitModule {
 
 namespace {
 
-constexpr uint32_t SHAPE_UNKNOWN = 0, SHAPE_GENERIC = 1, SHAPE_SHORTCUT = 2, SHAPE_FIRST = 3;
+constexpr uint32_t SHAPE_UNKNOWN = 0, SHAPE_GENERIC = 1, SHAPE_SHORTCUT = 2, SHAPE_WIDE = 3,
+                   SHAPE_FIRST = 4;
 
 std::string lit(int64_t v) {
   if (v == (int64_t)(-9223372036854775807LL - 1)) return "(-9223372036854775807LL - 1)";
@@ -366,7 +367,9 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
   for (size_t i = 0; i < ks.size(); ++i) {
     const IrKernel& k = ks[i];
     JitMeta m{SHAPE_GENERIC, (uint32_t)P.consts.size(), (uint32_t)k.param_names.size(), 0};
-    if (k.path == PATH_SHORTCUT) {
+    if (k.path == PATH_WIDE) {
+      m.shape = SHAPE_WIDE;  // evaluated warp-cooperatively by the bucket kernel itself
+    } else if (k.path == PATH_SHORTCUT) {
       m.shape = SHAPE_SHORTCUT;
       P.consts.push_back(k.shortcut);
     } else if (k.path == PATH_JIT) {
@@ -512,6 +515,7 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
   P.kb_of = m->d_kb;
   P.kb_unknown = m->kb_unknown;
   P.nkeys = m->nkeys;
+  P.wide_key = SHAPE_WIDE;
   const uint64_t ntiles = (n + m->tile - 1) / m->tile;
   const uint64_t cap = (uint64_t)num_sms * m->ctas;
   const uint64_t grid = ntiles < cap ? ntiles : cap;

@@ -28,6 +28,7 @@
 #pragma once
 
 #include "device_common.cuh"
+#include "desc_eval.cuh"
 #include "eval_generic.cuh"
 
 namespace picker {
@@ -45,9 +46,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
-      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
       : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
+      : "r"(smem_u32(bar)), "r"(parity), "r"(1000000u)  // suspend-time hint (ns): sleep, do not spin
       : "memory");
   return ok != 0;
 }
@@ -203,8 +204,37 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     __syncthreads();
 
-    // 2. scans: record offsets and 32-record groups per key
-    {
+    // 2. scans: record offsets and 32-record groups per key.  Few keys (the
+    //    specialised module: one per shape): one warp scans, the others wait.
+    if (nk <= 32 * 64) {
+      if (warp == 0) {
+        const uint32_t per = (nk + 31) / 32;
+        const uint32_t b0 = min(nk, lane * per), b1 = min(nk, b0 + per);
+        uint32_t rs = 0, gs = 0;
+        for (uint32_t b = b0; b < b1; ++b) {
+          const uint32_t c = s_cnt[b];
+          rs += c;
+          gs += (c + 31) >> 5;
+        }
+        uint32_t ri = rs, gi = gs;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t r2 = __shfl_up_sync(0xffffffffu, ri, d), g2 = __shfl_up_sync(0xffffffffu, gi, d);
+          if (lane >= d) ri += r2, gi += g2;
+        }
+        uint32_t ro = ri - rs, go = gi - gs;
+        for (uint32_t b = b0; b < b1; ++b) {
+          const uint32_t c = s_cnt[b];
+          s_off[b] = ro;
+          s_cur[b] = ro;
+          const uint32_t ng = (c + 31) >> 5;
+          for (uint32_t j = 0; j < ng; ++j) s_grp[go + j] = (b << 8) | j;
+          ro += c;
+          go += ng;
+        }
+        if (lane == 31) s_ngrp = go, s_next = 0;
+      }
+    } else {
       const uint32_t per = (nk + kThreads - 1) / kThreads;
       const uint32_t b0 = min(nk, tid * per), b1 = min(nk, b0 + per);
       uint32_t rs = 0, gs = 0;
@@ -252,6 +282,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t e = s_grp[g];
       const uint32_t key = e >> 8, j = e & 255u;
       const uint32_t cnt = s_cnt[key] - 32u * j;
+      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+        for (uint32_t q = 0; q < min(cnt, 32u); ++q) {
+          const uint32_t wi = s_perm[s_off[key] + 32u * j + q];
+          const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
+          const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                             (uint64_t)r.nargs <= si.hi - r.arg_off;
+          const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                   : B.args + r.arg_off;
+          const uint8_t c = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+          if (lane == 0) {
+            flags[base + wi] = c;
+            if (c <= V_IDEM_KERNEL) atomicOr(s_bits + (wi >> 5), 1u << (wi & 31));
+            atomicAdd(s_hist + count_bin(c), 1u);
+          }
+        }
+        continue;
+      }
       const bool on = (uint32_t)lane < cnt;
       uint8_t code = 0;
       uint32_t li = 0;

@@ -25,6 +25,7 @@
 #include <string>
 #include <vector>
 
+#include "desc_eval.cuh"
 #include "eval_generic.cuh"
 #include "launch.hpp"
 
@@ -34,67 +35,9 @@ constexpr uint32_t kPending = 0x100;
 constexpr uint64_t kExactWindowCap = 1ULL << 31;  // bytes (oracle: EXACT_WINDOW_CAP)
 constexpr int kExactThreads = 256;
 
-__device__ __forceinline__ int64_t prod_val(const Tables& T, const DKernel& K, const RecVals& X, uint16_t j) {
-  const DProd p = T.prods[K.prod + j];
-  return mul64(mul64(p.k, X.get(p.a)), X.get(p.b));
-}
-
-__device__ __forceinline__ void slot_bounds(const Tables& T, const DKernel& K, const RecVals& X, uint16_t s,
-                                            int64_t& lo, int64_t& hi) {
-  const DVar v = T.vars[K.var + s];
-  lo = (-9223372036854775807LL - 1);
-  hi = 9223372036854775807LL;
-  if (v.skind != SK_NONE) {
-    const int64_t g = X.get(OPD_GX + v.axis), b = X.get(OPD_BX + v.axis);
-    lo = 0;
-    hi = (v.skind == SK_TID ? b : v.skind == SK_BID ? g : g * b) - 1;
-  }
-  auto B = [&](const DBexpr& e) {
-    int64_t x = e.k0;
-    if (e.p0 != kNone16) x = add64(x, prod_val(T, K, X, e.p0));
-    if (e.p1 != kNone16) x = add64(x, prod_val(T, K, X, e.p1));
-    return x;
-  };
-  for (int j = 0; j < v.nlo; ++j) lo = max64(lo, B(T.bexprs[v.bex + j]));
-  for (int j = 0; j < v.nhi; ++j) hi = min64(hi, B(T.bexprs[v.bex + v.nlo + j]));
-}
-
 __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t lim) {
   if (a == 0 || b == 0) return 0;
   return a > lim / b ? lim : min(a * b, lim);
-}
-
-__device__ __forceinline__ bool desc_active(const Tables& T, const DKernel& K, const DDesc& D, const RecVals& X) {
-  for (int g = 0; g < D.nguard; ++g) {
-    const DGuard G = T.guards[D.guard + g];
-    if (!cmp64(X.get(G.a), G.cmp, G.b == OPD_NONE ? G.bconst : X.get(G.b))) return false;
-  }
-  for (int v = 0; v < D.nvar; ++v) {
-    int64_t lo, hi;
-    slot_bounds(T, K, X, T.varlist[D.var + v], lo, hi);
-    if (lo > hi) return false;
-  }
-  return true;
-}
-
-__device__ void desc_extent(const Tables& T, const DKernel& K, const DDesc& D, const RecVals& X, int64_t& lb,
-                            int64_t& ub) {
-  lb = D.base == OPD_NONE ? 0 : X.get(D.base);
-  ub = lb;
-  for (int t = 0; t < D.nterm; ++t) {
-    const DTerm tm = T.terms[D.term + t];
-    const int64_t c = prod_val(T, K, X, tm.prod);
-    if (tm.var == kNone16) {
-      lb = add64(lb, c), ub = add64(ub, c);
-      continue;
-    }
-    int64_t lo, hi;
-    slot_bounds(T, K, X, tm.var, lo, hi);
-    const int64_t a = mul64(c, floordiv64(lo, tm.div)), b = mul64(c, floordiv64(hi, tm.div));
-    lb = add64(lb, min64(a, b));
-    ub = add64(ub, max64(a, b));
-  }
-  ub = add64(ub, (int64_t)D.width - 1);
 }
 
 // X1: final code, or kPending with the window [wlo, whi] to enumerate.

@@ -55,7 +55,7 @@ cudaError_t launch_bucket_generic(const BucketParams& P0, const DevBatch& B, uin
                                   int num_sms, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   BucketParams P = P0;  // kb_of / kb_unknown: key = bin (set at load time)
-  P.nkeys = P.nbins + 1;
+  P.nkeys = P.nbins + 2;  // kernels, unknown ids, wide kernels (P.wide_key = nbins + 1)
   const size_t smem = bucket_smem_bytes(P.nkeys);
   if (smem > kMaxSmem) return cudaErrorInvalidValue;
   static size_t configured = 0;

@@ -17,7 +17,8 @@ struct IrKernel;
 struct Options {
   bool jit = true;     // NVRTC-specialised functions for every COND kernel
   bool bucket = true;  // group each tile's records by kernel before evaluating
-  int force_path = 0;  // 0 auto, 1 generic (table-driven) for every COND kernel
+  int force_path = 0;  // 0 auto, 1 generic (table-driven), 2 jit, 3 wide, for every COND kernel
+  int64_t wide_pairs = 1 << 20;  // read x write pairs above which a kernel takes the wide path
   // geometry of the specialised kernel (tuning; k_bucket.cuh)
   int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;
 };

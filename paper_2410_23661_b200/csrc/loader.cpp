@@ -471,7 +471,8 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
   const uint32_t nb = (uint32_t)ks.size();
   t.kb_unknown = nb | (nb << 16);
   t.kb.assign(t.kernels.size(), t.kb_unknown);
-  for (uint32_t i = 0; i < nb; ++i) t.kb[ks[i].id] = i | (i << 16);
+  for (uint32_t i = 0; i < nb; ++i)  // key = bin; every wide kernel shares key nb + 1
+    t.kb[ks[i].id] = i | ((ks[i].path == PATH_WIDE ? nb + 1 : i) << 16);
   for (auto& k : ks) {
     DKernel dk{};
     dk.shortcut = k.shortcut;

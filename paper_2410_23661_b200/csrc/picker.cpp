@@ -126,6 +126,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   if (k == "jit") c->opt.jit = v != 0;
   else if (k == "bucket") c->opt.bucket = v != 0;
   else if (k == "force_path") c->opt.force_path = (int)v;
+  else if (k == "wide_pairs") c->opt.wide_pairs = v;
   else if (k == "tile") c->opt.tile = (int)v;
   else if (k == "threads") c->opt.threads = (int)v;
   else if (k == "ctas") c->opt.ctas = (int)v;
@@ -202,6 +203,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.T.term_lvar = (const uint8_t*)(b + o_tl);
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
+  c->P.wide_key = c->P.nbins + 1;  // table-driven grouping (the JIT module uses its own)
   c->ir = std::move(ks);
   c->ht = std::move(ht);
   c->loaded = true;

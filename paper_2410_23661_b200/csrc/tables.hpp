@@ -149,6 +149,7 @@ struct BucketParams {
   uint32_t kb_unknown;     // bin | key << 16 of an id that is not loaded
   const JitMeta* jit_meta;     // [nbins + 1] (specialised module only)
   const int64_t* jit_consts;   // per-kernel constants (specialised module only)
+  uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads

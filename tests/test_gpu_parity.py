@@ -50,7 +50,8 @@ def _check_outputs(flags, bits, counts, want):
         assert np.array_equal(counts.cpu().numpy(), exp_c)
 
 
-PATH_OPTS = [dict(jit=0, bucket=0), dict(jit=0, bucket=1), dict(jit=1)]
+PATH_OPTS = [dict(jit=0, bucket=0), dict(jit=0, bucket=1), dict(jit=1),
+             dict(jit=0, force_path=3), dict(jit=1, wide_pairs=4)]
 
 
 @pytest.mark.parametrize("opt", PATH_OPTS, ids=str)
@@ -175,3 +176,19 @@ def test_exact_random(pk, seed):
     assert ((inter == 10) & (got == 0)).sum() > 0
     # no false positives: interval idempotent => exact idempotent
     assert not ((inter == 0) & (got == 10)).any()
+
+
+# ---- C4: cuDNN-like kernels with 16-48 pointer arguments ------------------------
+
+@pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, force_path=3), dict(jit=0, force_path=3),
+                                 dict(jit=0, bucket=0)], ids=str)
+def test_c4_many_pointers(pk, opt):
+    """Specialised pairwise, the K2 sort+sweep path and the table path agree
+    with the oracle on cuDNN-like records (sweep == pairwise)."""
+    from tracegen.workloads import make_c4
+    s, rec, args, _ = make_c4(n=3000, n_kernels=12)
+    want = _oracle_codes(s, rec, args)
+    p = _make(pk, s, **opt)
+    flags, bits, counts = p.validate(rec, args)
+    _check_outputs(flags, bits, counts, want)
+    assert (want == 10).sum() > 0 and (want == 0).sum() > 0
