@@ -45,7 +45,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--replicas", type=int, default=REPLICAS)
+    ap.add_argument("--replicas", type=int, default=None, help="default: per workload")
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
@@ -61,15 +62,34 @@ def dist_env():
     return rank, world, local
 
 
-def workload_config(args, world):
+# name -> (base generator kwargs, default replicas, description); SURVEY §8F / BASELINE.json configs
+WORKLOADS = {
+    "c2": (dict(), REPLICAS,
+           "C2 paper-shaped trace (547 kernels / 18,217 instances / 6 apps)"),
+    "c3": (dict(n=1 << 14, n_kernels=64), 64,
+           "C3 TVM-style tiled GEMM/conv kernels with affine strided ranges (64 kernels, 16,384-record base)"),
+    "c4": (dict(n=1 << 13, n_kernels=32), 512,
+           "C4 cuDNN-like kernels with 16-48 pointer args (32 kernels, 8,192-record base)"),
+}
+
+
+def make_base(workload):
+    from tracegen import workloads as W
+    kw = WORKLOADS[workload][0]
+    return {"c2": W.make_c2, "c3": W.make_c3, "c4": W.make_c4}[workload](**kw)
+
+
+def workload_config(args, world, n_base=None, flush=False):
+    kw, _, desc = WORKLOADS[args.workload]
+    n_base = n_base or (18217 if args.workload == "c2" else kw["n"])
     return {
-        "workload": "C2 paper-shaped trace (547 kernels / 18,217 instances / 6 apps) tiled "
-                    f"x{args.replicas} per GPU with pointer relocation" + (" (C5 stream)" if world > 1 else ""),
-        "records_per_gpu": 18217 * args.replicas,
-        "records_total": 18217 * args.replicas * world,
-        "kernels": 547,
-        "seed": 23661,
-        "l2": "inputs 6.6x L2 per GPU, no flush needed",
+        "workload": f"{desc} tiled x{args.replicas} per GPU with pointer relocation"
+                    + (" (C5 stream)" if world > 1 and args.workload == "c2" else ""),
+        "records_per_gpu": n_base * args.replicas,
+        "records_total": n_base * args.replicas * world,
+        "seed": {"c2": 23661, "c3": 23662, "c4": 23663}[args.workload],
+        "l2": "L2 flushed (512 MB write) before every timed step" if flush
+              else "inputs > 6x the 126 MB L2 per GPU, no flush needed",
         "parallelism": f"dp{world} (instance shards, all-gather of flag bits)" if world > 1 else "single GPU",
     }
 
@@ -139,9 +159,9 @@ class ClockSampler:
 
 
 def build_inputs(args, rank):
-    from tracegen.workloads import make_c2, replicate
+    from tracegen.workloads import replicate
 
-    s, rec, a, meta = make_c2()
+    s, rec, a, meta = make_base(args.workload)
     # this rank's replicas: r in [rank*R, (rank+1)*R)
     R = args.replicas
     rr, aa = replicate(rec, a, meta["ptr_mask"], R, DELTA)
@@ -174,9 +194,10 @@ def run_reference(args):
     if rank != 0:
         return
     import oracle.picker_oracle as O
-    from tracegen.workloads import make_c2
 
-    s, rec, a, meta = make_c2()
+    s, rec, a, meta = make_base(args.workload)
+    if args.workload != "c2":
+        rec = rec[:2048]  # bounded sample: the oracle takes ~ms per many-descriptor record
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
         O.oracle_batch_mp(s, rec[:2048], a, processes=cores)
@@ -193,7 +214,7 @@ def run_reference(args):
         "scaling": "weak", "vs_baseline": None, "dtype": "int (exact Python integers)",
         "data": "synthetic", "config": workload_config(args, world),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": f"each step: the full C2 base trace ({len(rec)} records), "
+                         "sample": f"each step: {len(rec)} records of the {args.workload.upper()} base trace, "
                                    f"{cores}-process pool"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "p50_us_per_instance": 1e3 * ms / len(rec),
@@ -203,6 +224,8 @@ def run_reference(args):
 
 def main():
     args = parse()
+    if args.replicas is None:
+        args.replicas = WORKLOADS[args.workload][1]
     if args.impl == "reference":
         run_reference(args)
         return
@@ -252,7 +275,7 @@ def main():
     got = flags.cpu().numpy()
     mism = int((got != np.tile(base_codes, args.replicas)).sum())
     # plus a directly-checked random sample of the relocated records
-    idx = np.random.default_rng(rank).choice(n, size=2000, replace=False)
+    idx = np.random.default_rng(rank).choice(n, size=2000 if args.workload == "c2" else 200, replace=False)
     direct = np.array(O.oracle_batch(s, rec[idx], a), np.uint8)
     mism += int((direct != got[idx]).sum())
 
@@ -261,6 +284,10 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    # inputs smaller than 2 x L2: flush L2 between timed steps
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    flush = rec.nbytes + a.nbytes < 2 * l2
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device=dev) if flush else None
     clk = ClockSampler(local)
     clk.start()
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -271,6 +298,8 @@ def main():
     t_all1 = torch.cuda.Event(enable_timing=True)
     t_all0.record(stream)
     for i in range(args.steps):
+        if flush:
+            scratch.zero_()  # evict the inputs from L2 (outside the step's events)
         ev[i][0].record(stream)
         kev[i][0].record(stream)
         p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
@@ -288,6 +317,8 @@ def main():
     total_ms = t_all0.elapsed_time(t_all1)
     step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
     kern_ms = [e0.elapsed_time(e1) for e0, e1 in kev]
+    if flush:  # the flushes sit between the steps' events
+        total_ms = float(sum(step_ms))
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -343,7 +374,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            traffic = json.load(open(tp)).get(args.workload, {}).get("bytes_per_launch")
         except Exception:
             traffic = None
     cpu = None
@@ -363,7 +394,7 @@ def main():
         "vs_baseline": None,
         "dtype": "int64",
         "data": "synthetic",
-        "config": workload_config(args, world),
+        "config": workload_config(args, world, len(base_rec), flush),
         "p50_us_per_instance": 1e3 * float(np.median(step_ms)) / n,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,

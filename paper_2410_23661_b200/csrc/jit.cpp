@@ -178,29 +178,38 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
     s << "  const int64_t vl" << i << " = " << lo << ", vh" << i << " = " << hi << ";\n";
     return (int)i;
   };
-  std::vector<int> rd, wr, rd_opq, wr_opq;
-  for (size_t di = 0; di < k.desc.size(); ++di) {
+  // Every variable slot first: the streamed descriptors below live in block
+  // scopes.  Then the extents of the smaller side (usually the writes) are kept
+  // in registers and the other side is streamed through the overlap test, so
+  // many-pointer kernels do not keep every extent live (register spills).
+  std::vector<std::vector<int>> sids(k.desc.size());
+  for (size_t di = 0; di < k.desc.size(); ++di)
+    for (auto& v : k.desc[di].vars) sids[di].push_back(slot_of(v));
+  size_t nr = 0, nw = 0;
+  for (auto& d : k.desc)
+    if (!d.opaque) (d.kind == KIND_R ? nr : nw)++;
+  const uint8_t kept_kind = nw <= nr ? KIND_W : KIND_R;
+  auto on_expr = [&](size_t di) {
     const IrDesc& d = k.desc[di];
-    std::vector<int> sid;
-    for (auto& v : d.vars) sid.push_back(slot_of(v));
     std::string on = "true";
     for (auto& gd : d.guard)
       on += " && (" + opnd(gd.a) + " " + kCmp[gd.cmp] + " " + (gd.b == OPD_NONE ? g.k(gd.bconst) : opnd(gd.b)) + ")";
-    for (int x : sid) on += " && (vl" + std::to_string(x) + " <= vh" + std::to_string(x) + ")";
-    s << "  const bool on" << di << " = " << on << ";\n";
-    if (d.opaque) {
-      (d.kind == KIND_R ? rd_opq : wr_opq).push_back((int)di);
-      continue;
-    }
+    for (int x : sids[di]) on += " && (vl" + std::to_string(x) + " <= vh" + std::to_string(x) + ")";
+    return on;
+  };
+  // emits the extent of descriptor di as `const int64_t lb<di>, ub<di>` at indent `ind`
+  auto extent = [&](size_t di, const char* ind) {
+    const IrDesc& d = k.desc[di];
     std::string lb = d.base == OPD_NONE ? "0LL" : opnd(d.base), ub = lb;
-    for (auto& t : d.terms) {
+    for (size_t ti = 0; ti < d.terms.size(); ++ti) {
+      const IrTerm& t = d.terms[ti];
       std::string c = g.prod(t.c);
       if (t.var < 0) {
         lb = "add64(" + lb + ", " + c + ")";
         ub = "add64(" + ub + ", " + c + ")";
         continue;
       }
-      const int x = sid[t.var];
+      const int x = sids[di][t.var];
       auto phi = [&](const std::string& v) {
         return t.div == 1 ? v : "floordiv64(" + v + ", " + std::to_string(t.div) + "u)";
       };
@@ -212,34 +221,50 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
       } else if (sign < 0) {
         lb = "add64(" + lb + ", mul64(" + c + ", " + phi(H) + "))";
         if (!lo0[x]) ub = "add64(" + ub + ", mul64(" + c + ", " + phi(L) + "))";
-      } else {
-        s << "  const int64_t c" << di << "_" << &t - &d.terms[0] << " = " << c << ";\n";
-        const std::string cv = "c" + std::to_string(di) + "_" + std::to_string(&t - &d.terms[0]);
+      } else {  // one term of unknown sign: both ends
+        const std::string cv = "c" + std::to_string(di) + "_" + std::to_string(ti);
+        s << ind << "const int64_t " << cv << " = " << c << ";\n";
         std::string A = "mul64(" + cv + ", " + phi(L) + ")", Bv = "mul64(" + cv + ", " + phi(H) + ")";
         lb = "add64(" + lb + ", min64(" + A + ", " + Bv + "))";
         ub = "add64(" + ub + ", max64(" + A + ", " + Bv + "))";
       }
     }
     if (d.width > 1) ub = "add64(" + ub + ", " + g.k((int64_t)d.width - 1) + ")";
-    s << "  const int64_t lb" << di << " = " << lb << ", ub" << di << " = " << ub << ";\n";
-    (d.kind == KIND_R ? rd : wr).push_back((int)di);
+    s << ind << "const int64_t lb" << di << " = " << lb << ", ub" << di << " = " << ub << ";\n";
+  };
+  std::vector<int> kept, opq_r, opq_w;
+  s << "  bool act_r = false, act_w = false, ov = false;\n";
+  for (size_t di = 0; di < k.desc.size(); ++di) {  // opaque sites and the kept side
+    const IrDesc& d = k.desc[di];
+    if (!d.opaque && d.kind != kept_kind) continue;
+    s << "  const bool on" << di << " = " << on_expr(di) << ";\n";
+    s << "  act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
+    if (d.opaque) {
+      (d.kind == KIND_R ? opq_r : opq_w).push_back((int)di);
+      continue;
+    }
+    extent(di, "  ");
+    kept.push_back((int)di);
   }
-  auto any = [&](const std::vector<int>& a, const std::vector<int>& b) {
+  for (size_t di = 0; di < k.desc.size(); ++di) {  // the streamed side
+    const IrDesc& d = k.desc[di];
+    if (d.opaque || d.kind == kept_kind) continue;
+    s << "  {\n    const bool on" << di << " = " << on_expr(di) << ";\n";
+    s << "    act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
+    extent(di, "    ");
+    std::string hit = "false";
+    for (int j : kept)
+      hit += " | (on" + std::to_string(j) + " & (lb" + std::to_string(di) + " <= ub" + std::to_string(j) +
+             ") & (lb" + std::to_string(j) + " <= ub" + std::to_string(di) + "))";
+    s << "    ov |= on" << di << " & (" << hit << ");\n  }\n";
+  }
+  auto any = [&](const std::vector<int>& a) {
     std::string e = "false";
     for (int i : a) e += " || on" + std::to_string(i);
-    for (int i : b) e += " || on" + std::to_string(i);
     return e;
   };
-  if (!rd_opq.empty() || !wr_opq.empty()) {
-    s << "  {\n    const bool act_r = " << any(rd, rd_opq) << ", act_w = " << any(wr, wr_opq) << ";\n";
-    s << "    const bool opq_r = " << any(rd_opq, {}) << ", opq_w = " << any(wr_opq, {}) << ";\n";
-    s << "    if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;\n  }\n";
-  }
-  s << "  bool ov = false;\n";
-  for (int i : rd)
-    for (int j : wr)
-      s << "  ov |= on" << i << " & on" << j << " & (lb" << i << " <= ub" << j << ") & (lb" << j
-        << " <= ub" << i << ");\n";
+  if (!opq_r.empty() || !opq_w.empty())  // opaque rule before overlap (precedence 9 < 10)
+    s << "  if (((" << any(opq_r) << ") && act_w) || ((" << any(opq_w) << ") && act_r)) return V_NI_OPAQUE;\n";
   s << "  return ov ? V_NI_OVERLAP : V_IDEM_CHECKED;\n}\n";
   return s.str();
 }
@@ -443,7 +468,25 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
   return true;
 }
 
-JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt, std::string& err) {
+// tile = 0 (auto): the largest tile (<= 512 records, a multiple of 32) whose
+// argument span fits the 4096-slot staging buffer when records carry 1.25x the
+// mean parameter count of the loaded COND kernels; args_per_rec = 4096 / tile.
+Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
+  if (opt.tile != 0) return opt;
+  double sum = 0;
+  int cnt = 0;
+  for (auto& k : ks)
+    if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC) sum += k.param_names.size(), ++cnt;
+  const double apr = std::max(4.0, 1.25 * (cnt ? sum / cnt : 4.0));
+  int tile = (int)(4096.0 / apr) / 32 * 32;
+  tile = std::max(32, std::min(512, tile));
+  opt.tile = tile;
+  opt.args_per_rec = 4096 / tile;
+  return opt;
+}
+
+JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std::string& err) {
+  const Options opt = resolve_geometry(ks, opt_in);
   if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
       opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1) {
     err = "invalid tile / threads / ctas / args_per_rec options";

@@ -20,7 +20,7 @@ struct Options {
   int force_path = 0;  // 0 auto, 1 generic (table-driven), 2 jit, 3 wide, for every COND kernel
   int64_t wide_pairs = 1 << 20;  // read x write pairs above which a kernel takes the wide path
   // geometry of the specialised kernel (tuning; k_bucket.cuh)
-  int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;
+  int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;  // tile 0: chosen at load (jit.cpp)
 };
 
 struct JitModule;
@@ -39,6 +39,8 @@ struct JitPlan {
   int nshapes = 0;
 };
 JitPlan jit_plan(const std::vector<IrKernel>& ks);
+// Fills in the automatic geometry (tile = 0) from the summaries.
+Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
 // Stable-sort kernels by generated shape so neighbouring bins share code.
 void order_by_shape(std::vector<IrKernel>& ks);
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,

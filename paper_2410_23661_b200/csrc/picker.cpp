@@ -254,7 +254,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     order_by_shape(ks);
     JitPlan plan = jit_plan(ks);
     std::string cubin, lowered, err;
-    if (!jit_compile(plan, opt, cubin, lowered, false, err)) {
+    if (!jit_compile(plan, resolve_geometry(ks, opt), cubin, lowered, false, err)) {
       put(msg, msg_len, err);
       put(src_out, src_len, plan.src);
       return PICKER_ECUDA;
