@@ -181,6 +181,20 @@ int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t 
                        uint8_t* exact_out, uint64_t* counts_out,
                        uint64_t max_points_per_instance, void* stream);
 
+/* Multi-kernel idempotency: the stream is cut into
+ * consecutive windows of `window` launches (1..1024; record order = launch
+ * order) and each window is validated as one unit.  mode 0 (sequential list):
+ * NI when a write of instance j can clobber a byte read by instance i <= j
+ * ("checks the clobber anti-dependency across the instances"); mode 1
+ * (concurrent set): NI when any read and any write of the window overlap.  The
+ * first record whose own check is decided before any address (0xFF, 0xFE, 2-8;
+ * kernel-level idempotent instances take part with their writes) decides the
+ * window; then the opaque rule (9); then the overlap (10); else 0.
+ * out[ceil(n/window)] is a device pointer.  Kernels with more than 64
+ * descriptors are rejected (PICKER_EINVAL).  Asynchronous on `stream`.        */
+int picker_validate_sequence(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
+                             uint32_t window, uint32_t mode, uint8_t* out, void* stream);
+
 /* Number of kernels loaded and the path each kernel was compiled to
  * (per-kernel introspection for tests): path_out[i] for kernel id ids_out[i];
  * path 0 = shortcut, 1 = generic table path, 2 = specialised (JIT) path,

@@ -226,12 +226,14 @@ def interval_extent(d, vals, box):
 
 # ---- the shared prefix of both validators -------------------------------------
 
-def _prefix(kernels, rec):
+def _prefix(kernels, rec, through_idem=False):
     """Steps common to oracle_interval and oracle_exact.
 
     Returns (code, None) when the verdict is decided before any address is
     computed, else (None, (kernel, vals, active)) where active is a list of
     (descriptor, box) for descriptors whose guard holds and whose box is nonempty.
+    ``through_idem``: evaluate a kernel-level idempotent kernel like a COND one
+    (its writes matter to a multi-kernel window, reading Q23).
     """
     k = kernels.get(rec["kernel_id"])
     if k is None:
@@ -240,7 +242,7 @@ def _prefix(kernels, rec):
         return ERR_ARITY, None
     # Kernel-level shortcuts: "The validator directly returns kernel-level
     # idempotency without performing the validation".
-    if k["class"] == "IDEM":
+    if k["class"] == "IDEM" and not through_idem:
         return IDEM_KERNEL, None
     if k["class"] == "NONIDEM":
         return NI_KERNEL[k["reason"]], None
@@ -408,3 +410,66 @@ def oracle_batch_mp(summary, rec_array, args, fn=oracle_interval, processes=None
     with pool:
         parts = pool.map(_mp_chunk, jobs)
     return [c for p in parts for c in p]
+
+
+# ---- multi-kernel idempotency (reading Q23) ----------------
+
+SEQ_SEQUENTIAL, SEQ_CONCURRENT = 0, 1
+
+
+def oracle_sequence(kernels, recs, mode=SEQ_SEQUENTIAL):
+    """Idempotency of a list of launches as one unit.
+
+    "First, Picker predicts the read and write addresses of each GPU kernel
+    instance.  Second, [it] sorts the instances by their launch order, and then
+    checks the clobber anti-dependency across the instances" (sequential list);
+    for "concurrently executed GPU kernel instances, [it checks] the overlap of
+    read and write addresses among all concurrent instances".
+
+    Reading Q23: the first instance (launch order) whose single-instance check is
+    decided before any address (unknown kernel, arity, kernel-level NI class,
+    precondition, global condition) decides the list; kernel-level idempotent
+    instances take part with their writes.  Otherwise, with instances i (reads)
+    and j (writes): sequential requires i <= j (a write can clobber a byte read
+    by the same or an earlier instance; an earlier write cannot be trusted to
+    cover the byte, the extents over-approximate), concurrent takes every pair.
+    Opaque rule first (9), then overlap (10), else 0.
+    """
+    inst = []
+    for rec in recs:
+        code, st = _prefix(kernels, rec, through_idem=True)
+        if code is not None:
+            return code
+        _, vals, active = st
+        inst.append([(d["kind"], d["opaque"], None if d["opaque"] else interval_extent(d, vals, box))
+                     for d, box in active])
+
+    def ordered(i, j):
+        return mode == SEQ_CONCURRENT or i <= j
+
+    for i, a in enumerate(inst):  # reads of i
+        for j, b in enumerate(inst):  # writes of j
+            if not ordered(i, j):
+                continue
+            if any(k == "R" and o for k, o, _ in a) and any(k == "W" for k, _, _ in b):
+                return NI_OPAQUE
+            if any(k == "R" for k, _, _ in a) and any(k == "W" and o for k, o, _ in b):
+                return NI_OPAQUE
+    for i, a in enumerate(inst):
+        for j, b in enumerate(inst):
+            if not ordered(i, j):
+                continue
+            for kr, orr, r in a:
+                if kr != "R" or orr:
+                    continue
+                for kw, ow, w in b:
+                    if kw == "W" and not ow and r[0] <= w[1] and w[0] <= r[1]:
+                        return NI_OVERLAP
+    return IDEM_CHECKED
+
+
+def oracle_windows(summary, rec_array, args, window, mode=SEQ_SEQUENTIAL):
+    """oracle_sequence over consecutive windows of ``window`` records."""
+    kernels = index_summary(summary)
+    recs = [decode_record(r, args) for r in rec_array]
+    return [oracle_sequence(kernels, recs[w:w + window], mode) for w in range(0, len(recs), window)]

@@ -49,6 +49,8 @@ SIGNATURES = {
     "picker_validate_batch_host": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P,
                                                   P]),
     "picker_exact_check": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, U64, P]),
+    "picker_validate_sequence": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, ctypes.c_uint32,
+                                                ctypes.c_uint32, P, P]),
     "picker_kernel_info": (ctypes.c_int, [P, P, P, ctypes.c_uint32]),
     "picker_set_option": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.c_int64]),
     "picker_last_launch_count": (ctypes.c_int, [P]),

@@ -51,6 +51,9 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches);
 
+cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
+                            uint8_t* out, int num_sms, cudaStream_t s, std::string& err);
+
 cudaError_t launch_exact(const Tables& T, const DevBatch& b, uint64_t n, uint8_t* out,
                          unsigned long long* counts, uint64_t max_points, int num_sms,
                          cudaStream_t s, int* launches, std::string& err);

@@ -322,7 +322,9 @@ void verify_kernel(IrKernel& k) {
   if (k.shortcut == V_IDEM_KERNEL)
     for (auto& d : k.desc)
       if (d.kind == KIND_R) uerr(who + "class IDEM but the kernel reads memory");
-  if (k.shortcut != 0) {
+  // kernel-level NI kernels are never evaluated; IDEM kernels are verified too,
+  // because their writes take part in multi-kernel windows (reading Q23)
+  if (k.shortcut != 0 && k.shortcut != V_IDEM_KERNEL) {
     k.path = PATH_SHORTCUT;
     return;
   }

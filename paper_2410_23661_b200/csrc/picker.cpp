@@ -411,6 +411,23 @@ int picker_validate_batch_host(picker_ctx_t* c, const picker_batch_t* b, uint64_
   return PICKER_OK;
 }
 
+int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint32_t window,
+                             uint32_t mode, uint8_t* out, void* stream) {
+  int st = check_batch(c, b, n, out);
+  if (st) return st;
+  if (window < 1 || window > 1024 || mode > 1) return fail(c, PICKER_EINVAL, "window must be 1..1024, mode 0/1");
+  for (auto& k : c->ir)
+    if (k.desc.size() > 64)
+      return fail(c, PICKER_EINVAL, "kernel " + std::to_string(k.id) + " has more than 64 descriptors");
+  DevGuard g(c->device);
+  DevBatch db{b->rec, b->args, 0, b->args_len};
+  std::string err;
+  cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, out, c->num_sms, (cudaStream_t)stream, err);
+  if (e != cudaSuccess) return cuda_fail(c, e, ("sequence: " + err).c_str());
+  c->last_launches = n ? 2 : 0;
+  return PICKER_OK;
+}
+
 int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* out,
                        uint64_t* counts, uint64_t max_points, void* stream) {
   int st = check_batch(c, b, n, out);

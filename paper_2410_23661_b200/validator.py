@@ -163,6 +163,21 @@ class Picker:
             cnt.data_ptr() if cnt is not None else None, _stream_handle(stream)))
         return flags, bw, cnt
 
+    def validate_sequence(self, rec, args, window, *, concurrent=False, stream=None):
+        """Multi-kernel idempotency of consecutive windows of ``window`` launches
+        (sequential list, or concurrent set).  Returns u8[ceil(n/window)] codes."""
+        rec = records_tensor(rec, self.device)
+        if not torch.is_tensor(args):
+            args = torch.from_numpy(np.asarray(args, dtype=np.int64))
+        args = args.to(self.device)
+        n = rec.shape[0]
+        out = torch.empty((n + window - 1) // window, dtype=torch.uint8, device=self.device)
+        b = self._batch(rec, args, True)
+        self._check(lib.picker_validate_sequence(self._h, ctypes.byref(b), n, int(window),
+                                                 1 if concurrent else 0, out.data_ptr(),
+                                                 _stream_handle(stream)))
+        return out
+
     def exact_check(self, rec, args, *, max_points=1 << 20, counts=True, stream=None):
         """Exact (enumerating) verdicts for device-resident records (Fig. 3 strawman)."""
         rec = records_tensor(rec, self.device)

@@ -1,0 +1,90 @@
+"""Multi-kernel idempotency: oracle pins
+(CPU) and GPU parity of picker_validate_sequence."""
+import numpy as np
+import pytest
+
+import oracle.picker_oracle as O
+from tracegen import golden
+from tracegen.records import RecordBuilder
+from tracegen.synth import random_records, random_summary
+
+G = O.index_summary(golden.golden_summary())
+
+
+def _recs(rows):
+    b = RecordBuilder()
+    for kid, args, grid, block in rows:
+        b.add(kid, args, grid=grid, block=block)
+    rec, args = b.build()
+    return [O.decode_record(r, args) for r in rec]
+
+
+VA = dict(grid=(4, 1, 1), block=(128, 1, 1))  # vectorAdd: A = B + C, 0x800-byte buffers
+
+
+def _va(a, b, c):
+    return (0, [a, b, c], VA["grid"], VA["block"])
+
+
+def test_clobber_of_an_earlier_read():
+    """k1: A1 = B1 + C1; k2: B1 = A1 + C1 -- k2 overwrites B1, an input of k1:
+    a clobber anti-dependency across the list."""
+    r = _recs([_va(0x10000, 0x20000, 0x30000), _va(0x20000, 0x10000, 0x30000)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.NI_OVERLAP
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OVERLAP
+
+
+def test_read_after_write_is_not_a_clobber():
+    """k1: A = B + C; k2: D = A + C -- k2 reads what k1 wrote (RAW), no input of
+    the list is overwritten: idempotent as a sequence, but not as a concurrent set
+    (concurrent = any read/write overlap)."""
+    r = _recs([_va(0x10000, 0x20000, 0x30000), _va(0x40000, 0x10000, 0x30000)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.IDEM_CHECKED
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OVERLAP
+
+
+def test_disjoint_list_is_idempotent():
+    r = _recs([_va(0x10000 * (3 * i + 1), 0x10000 * (3 * i + 2), 0x10000 * (3 * i + 3)) for i in range(5)])
+    for m in (O.SEQ_SEQUENTIAL, O.SEQ_CONCURRENT):
+        assert O.oracle_sequence(G, r, m) == O.IDEM_CHECKED
+
+
+def test_write_only_kernel_clobbers_earlier_input():
+    """vectorSet (kernel-level idempotent alone) still overwrites a byte read by an
+    earlier instance of the list."""
+    r = _recs([_va(0x10000, 0x20000, 0x30000), (1, [0x20000], VA["grid"], VA["block"])])
+    assert O.oracle_sequence(G, r) == O.NI_OVERLAP
+    r = _recs([(1, [0x20000], VA["grid"], VA["block"]), _va(0x10000, 0x20000, 0x30000)])
+    assert O.oracle_sequence(G, r) == O.IDEM_CHECKED  # the set happens first: RAW
+
+
+def test_first_decisive_instance_decides():
+    r = _recs([_va(0x10000, 0x20000, 0x30000), (2, [0x50000], VA["grid"], VA["block"]),
+               _va(1 << 56, 0x20000, 0x30000)])
+    assert O.oracle_sequence(G, r) == 2  # vectorInc (SO) precedes the precondition failure
+
+
+def test_window_of_one_matches_single_instance():
+    s = random_summary(5, n_kernels=20)
+    rec, args = random_records(6, s, 300, max_threads=16, max_grid=2)
+    w1 = O.oracle_windows(s, rec, args, 1)
+    iv = O.oracle_batch(s, rec, args)
+    for a, b in zip(w1, iv):
+        assert a == b or (a, b) == (0, 1)  # a write-only kernel is idempotent either way
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window", [1, 3, 8, 32])
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_gpu_sequence_parity(window, concurrent):
+    import paper_2410_23661_b200 as pk
+    s = random_summary(31, n_kernels=24)
+    rec, args = random_records(32, s, 2000 + window, max_threads=32, max_grid=4)
+    want = np.array(O.oracle_windows(s, rec, args, window, O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL),
+                    np.uint8)
+    p = pk.Picker(0)
+    p.load(s)
+    got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+    assert len(set(want.tolist())) > 2
