@@ -49,7 +49,7 @@ struct JitModule {
   size_t smem = 0;
   JitMeta* d_meta = nullptr;
   int64_t* d_consts = nullptr;
-  uint32_t* d_kb = nullptr;
+  KbEntry* d_kb = nullptr;
   uint32_t kb_unknown = 0;
   uint32_t nkeys = 0;
   int nshapes = 0;
@@ -410,14 +410,15 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
   for (auto& m : P.meta) P.key_of.push_back((uint16_t)m.shape);
   for (size_t s = 0; s < shapes.size(); ++s)
     src << "__device__ __forceinline__ uint8_t ks" << s << shapes[s];
-  // key = shape (warp-uniform); bin = the lane's kernel (its constants)
+  // key = shape (warp-uniform); kn = the lane's kernel: constants offset |
+  // nparams << 24 (KbEntry, read in the grouping phase)
   src << "struct JitDispatch {\n  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, "
-         "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
+         "uint32_t kn, const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
+         "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
          "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n"
-         "    const JitMeta m = P.jit_meta[bin];\n"
-         "    if (!args_in_range(r, m.nparams, B.args_lo, B.args_hi)) return V_ERR_ARITY;\n"
-         "    const int64_t* __restrict__ K = P.jit_consts + m.koff;\n"
+         "    if (!args_in_range(r, kn >> 24, B.args_lo, B.args_hi)) return V_ERR_ARITY;\n"
+         "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n"
          "      case 2: return (uint8_t)__ldg(K);\n";
   for (size_t s = 0; s < shapes.size(); ++s)
@@ -509,11 +510,19 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   for (auto& k : ks) maxid = std::max(maxid, k.id);
   const uint32_t nbins = (uint32_t)ks.size();
   m->kb_unknown = nbins | ((uint32_t)SHAPE_UNKNOWN << 16);
-  std::vector<uint32_t> kb(ks.empty() ? 1 : (size_t)maxid + 1, m->kb_unknown);
-  for (uint32_t i = 0; i < nbins; ++i) kb[ks[i].id] = i | ((uint32_t)plan.key_of[i] << 16);
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_kb, kb.size() * sizeof(uint32_t));
+  std::vector<KbEntry> kb(ks.empty() ? 1 : (size_t)maxid + 1, KbEntry{m->kb_unknown, 0});
+  for (uint32_t i = 0; i < nbins; ++i) {
+    const JitMeta& jm = plan.meta[i];
+    if (jm.koff >= (1u << 24) || jm.nparams > 255) {
+      err = "specialised module: constant table exceeds 2^24 entries";
+      jit_destroy(m);
+      return nullptr;
+    }
+    kb[ks[i].id] = KbEntry{i | ((uint32_t)plan.key_of[i] << 16), jm.koff | (jm.nparams << 24)};
+  }
+  if (e == cudaSuccess) e = cudaMalloc(&m->d_kb, kb.size() * sizeof(KbEntry));
   if (e == cudaSuccess)
-    e = cudaMemcpy(m->d_kb, kb.data(), kb.size() * sizeof(uint32_t), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(m->d_kb, kb.data(), kb.size() * sizeof(KbEntry), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(m->d_meta, plan.meta.data(), plan.meta.size() * sizeof(JitMeta), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)

@@ -138,7 +138,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   uint16_t* s_key = reinterpret_cast<uint16_t*>(smem + kArgOff + 2 * kArgBufBytes);
   uint16_t* s_bin = s_key + kTile;
   uint16_t* s_perm = s_bin + kTile;
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_perm + kTile);
+  uint32_t* s_kn = reinterpret_cast<uint32_t*>(s_perm + kTile);  // KbEntry.kn per record
+  uint32_t* s_cnt = s_kn + kTile;
   uint32_t* s_off = s_cnt + nk;
   uint32_t* s_cur = s_off + nk;
   uint32_t* s_grp = s_cur + nk;
@@ -196,9 +197,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // 1. keys
     for (int i = tid; i < m; i += kThreads) {
       const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
-      const uint32_t kb = kid < P.T.nkernel_slots ? __ldg(P.kb_of + kid) : P.kb_unknown;
+      KbEntry e{P.kb_unknown, 0};
+      if (kid < P.T.nkernel_slots) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
+        e.kb = v.x, e.kn = v.y;
+      }
+      const uint32_t kb = e.kb;
       const uint32_t key = kb >> 16;
       s_bin[i] = (uint16_t)(kb & 0xFFFFu);
+      s_kn[i] = e.kn;
       s_key[i] = (uint16_t)key;
       atomicAdd(s_cnt + key, 1u);
     }
@@ -307,9 +314,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const picker_rec_t r = rec_from_smem(hdr + 32 * li);
         const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
                            (uint64_t)r.nargs <= si.hi - r.arg_off;
-        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
-                                 : B.args + r.arg_off;
-        code = Dispatch::eval(key, s_bin[li], P, r, a, B);
+        // two instantiations: with a pointer the compiler can prove is shared
+        // memory (LDS), and with a global one (unstaged tiles)
+        if (local)
+          code = Dispatch::eval(key, s_bin[li], s_kn[li], P, r,
+                                reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo)), B);
+        else
+          code = Dispatch::eval(key, s_bin[li], s_kn[li], P, r, B.args + r.arg_off, B);
         flags[base + li] = code;
         if (code <= V_IDEM_KERNEL) atomicOr(s_bits + (li >> 5), 1u << (li & 31));
       }
@@ -335,10 +346,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // Dispatch used by the static library: every bin through the table-driven
 // evaluator (grouping by kernel makes its table reads warp-uniform).
 struct GenericDispatch {
-  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, const BucketParams& P,
-                                                 const picker_rec_t& r, const int64_t* a,
-                                                 const DevBatch& B) {
-    (void)key;
+  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn,
+                                                 const BucketParams& P, const picker_rec_t& r,
+                                                 const int64_t* a, const DevBatch& B) {
+    (void)key, (void)kn;
     if (bin >= P.nbins) return V_ERR_KERNEL;
     return eval_generic(P.T, r, a, B.args_lo, B.args_hi);
   }

@@ -472,9 +472,9 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
   for (size_t i = 0; i < ks.size() && i < kNone16; ++i) t.bin_of[ks[i].id] = (uint16_t)i;
   const uint32_t nb = (uint32_t)ks.size();
   t.kb_unknown = nb | (nb << 16);
-  t.kb.assign(t.kernels.size(), t.kb_unknown);
+  t.kb.assign(t.kernels.size(), KbEntry{t.kb_unknown, 0});
   for (uint32_t i = 0; i < nb; ++i)  // key = bin; every wide kernel shares key nb + 1
-    t.kb[ks[i].id] = i | ((ks[i].path == PATH_WIDE ? nb + 1 : i) << 16);
+    t.kb[ks[i].id] = KbEntry{i | ((ks[i].path == PATH_WIDE ? nb + 1 : i) << 16), 0};
   for (auto& k : ks) {
     DKernel dk{};
     dk.shortcut = k.shortcut;

@@ -198,7 +198,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.T.descs = (const DDesc*)(b + o_d);
   c->P.T.varlist = (const uint16_t*)(b + o_l);
   c->P.bin_of = (const uint16_t*)(b + o_m);
-  c->P.kb_of = (const uint32_t*)(b + o_kb);
+  c->P.kb_of = (const KbEntry*)(b + o_kb);
   c->P.T.vardef = (const DVarDef*)(b + o_vd);
   c->P.T.term_lvar = (const uint8_t*)(b + o_tl);
   c->P.kb_unknown = ht.kb_unknown;

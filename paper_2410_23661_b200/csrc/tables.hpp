@@ -139,14 +139,21 @@ struct JitMeta {
   uint32_t shape, koff, nparams, pad;
 };
 
+// Per kernel id, read once per record when a tile is grouped (k_bucket.cuh):
+// kb = bin | key << 16 (key: the grouping key), kn = offset of the kernel's
+// constants | nparams << 24 (specialised module; 0 on the table path).
+struct KbEntry {
+  uint32_t kb, kn;
+};
+
 // Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
 struct BucketParams {
   Tables T;
   const uint16_t* bin_of;  // [T.nkernel_slots]: dense bin of each loaded kernel id, kNone16 if none
   uint32_t nbins;          // bins 0..nbins-1 are kernels; bin nbins collects unknown ids
   uint32_t nkeys;          // grouping keys 0..nkeys-1
-  const uint32_t* kb_of;   // [T.nkernel_slots]: bin | key << 16 of each kernel id
-  uint32_t kb_unknown;     // bin | key << 16 of an id that is not loaded
+  const struct KbEntry* kb_of;  // [T.nkernel_slots]: per kernel id, see KbEntry
+  uint32_t kb_unknown;          // kb of an id that is not loaded
   const JitMeta* jit_meta;     // [nbins + 1] (specialised module only)
   const int64_t* jit_consts;   // per-kernel constants (specialised module only)
   uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
@@ -178,7 +185,7 @@ constexpr size_t kMaxSmem = 227 * 1024;
 constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec) {
   // 2 x (headers + args) staging buffers; s_key, s_bin, s_perm (u16) per record;
   // s_cnt, s_off, s_cur (u32) per key; group table
-  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 6 +
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 +
          (size_t)nkeys * 12 + ((size_t)tile / 32 + nkeys) * 4 + 128;
 }
 constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
