@@ -311,7 +311,9 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
     err = nvrtcGetErrorString(r);
     return false;
   }
-  const char* name_expr = "picker::k_validate_bucket<picker::JitDispatch>";
+  const char* name_expr = src.find("k_validate_pipe<JitDispatch>") != std::string::npos
+                              ? "picker::k_validate_pipe<picker::JitDispatch>"
+                              : "picker::k_validate_bucket<picker::JitDispatch>";
   nvrtcAddNameExpression(prog, name_expr);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
                                    "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
@@ -424,7 +426,8 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
   for (size_t s = 0; s < shapes.size(); ++s)
     src << "      case " << SHAPE_FIRST + s << ": return ks" << s << "(r, a, K);\n";
   src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
-         "template __global__ void k_validate_bucket<JitDispatch>(const __grid_constant__ BucketParams, "
+         "template __global__ void " << (SHAPE_FIRST + shapes.size() <= kPipeKeys ? "k_validate_pipe" : "k_validate_bucket")
+      << "<JitDispatch>(const __grid_constant__ BucketParams, "
          "const __grid_constant__ DevBatch, uint64_t, "
          "uint8_t*, uint32_t*, unsigned long long*);\n}  // namespace picker\n";
   P.src = src.str();
@@ -479,8 +482,9 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   for (auto& k : ks)
     if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC) sum += k.param_names.size(), ++cnt;
   const double apr = std::max(4.0, 1.25 * (cnt ? sum / cnt : 4.0));
-  int tile = (int)(4096.0 / apr) / 32 * 32;
-  tile = std::max(32, std::min(512, tile));
+  // a multiple of the CTA size (k_validate_pipe hands each thread tile/threads records)
+  int tile = (int)(4096.0 / apr) / opt.threads * opt.threads;
+  tile = std::max(opt.threads, std::min(std::max(512, opt.threads), tile));
   opt.tile = tile;
   opt.args_per_rec = 4096 / tile;
   return opt;
@@ -494,6 +498,10 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     return nullptr;
   }
   JitPlan plan = jit_plan(ks);
+  if (SHAPE_FIRST + (uint32_t)plan.nshapes <= kPipeKeys && opt.tile % opt.threads) {
+    err = "tile must be a multiple of threads";
+    return nullptr;
+  }
   std::string cubin, lowered;
   if (!jit_compile(plan, opt, cubin, lowered, true, err)) return nullptr;
   JitModule* m = new JitModule();
@@ -534,7 +542,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     return nullptr;
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes;
-  m->smem = bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
+  m->smem = m->nkeys <= kPipeKeys ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec)
+                                  : bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {
     err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";
     jit_destroy(m);

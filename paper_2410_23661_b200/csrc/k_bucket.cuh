@@ -409,6 +409,213 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
 }
 
+// Pipelined bucketed kernel for at most kPipeKeys grouping keys (the
+// specialised module groups by shape: C2's 547 kernels have 31 shapes).
+//
+// Same per-tile work as k_validate_bucket, with two barriers per tile instead
+// of four and no per-key tables in shared memory:
+//   - the key pass of tile t+1 runs right after a warp's last group of tile t,
+//     so it fills the tail where warps wait for the slowest group; its results
+//     (key, rank within key, bin, kn) stay in registers until the scatter;
+//   - every warp scans the <= 64 key counters itself (lane l holds keys l and
+//     32 + l) and maps a claimed group index to its key with two ballots;
+//   - the scatter writes {record | bin << 16, kn} per sorted slot, so an
+//     evaluating lane needs one shared load to find its record and kernel.
+// Per tile t (B = __syncthreads):
+//   B_a | emit(t-1), restage (t-1)'s buffer with t+1, scan + scatter(t) | B_b |
+//   eval(t), keys(t+1)
+template <class Dispatch>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+    k_validate_pipe(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B, uint64_t n,
+                    uint8_t* __restrict__ flags, uint32_t* __restrict__ bits,
+                    unsigned long long* __restrict__ counts) {
+  static_assert(kTile % kThreads == 0, "tile must be a multiple of the CTA size");
+  static_assert(kTile <= 8192, "ranks and record indices are 13-bit");
+  constexpr int kPer = kTile / kThreads;
+  extern __shared__ __align__(128) unsigned char smem[];
+  constexpr uint32_t kHdrBytes = kTile * 32;
+  constexpr uint32_t kArgOff = 2 * kHdrBytes;
+  uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + 2 * kArgBufBytes);
+  uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);
+  __shared__ uint32_t s_cnt[2][kPipeKeys];
+  __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
+  __shared__ uint32_t s_next[2];
+  __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ StageInfo s_info[2];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  const uint64_t ntiles = (n + kTile - 1) / kTile;
+  const uint64_t G = gridDim.x;
+  if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
+  for (int b = tid; b < 2 * (int)kPipeKeys; b += kThreads) (&s_cnt[0][0])[b] = 0;
+  if (tid < 2) s_next[tid] = 0;
+  auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& lo_last, uint64_t& n_last) {
+    const uint64_t base = tile * kTile;
+    lo = lo_last = n_last = 0;
+    if (base < n) {
+      const uint64_t m = min((uint64_t)kTile, n - base);
+      lo = __ldg(&B.rec[base].arg_off);
+      lo_last = __ldg(&B.rec[base + m - 1].arg_off);
+      n_last = __ldg(&B.rec[base + m - 1].nargs);
+    }
+  };
+  if (tid == 0) {
+    mbar_init(&s_bar[0], 1);
+    mbar_init(&s_bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    for (int b = 0; b < 2; ++b) {
+      uint64_t lo, ll, nl;
+      bounds(blockIdx.x + b * G, lo, ll, nl);
+      stage_tile(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, smem + kArgOff + b * kArgBufBytes,
+                 &s_bar[b], &s_info[b], lo, ll, nl);
+    }
+  }
+  __syncthreads();
+
+  // key pass of one tile: results in registers (key | rank << 8, record | bin << 16, kn)
+  uint32_t kr[kPer], rb[kPer], kn[kPer];
+  auto keys = [&](uint64_t tile, uint32_t it) {
+    const uint32_t buf = it & 1;
+    const uint64_t base = tile * kTile;
+    const int m = (int)min((uint64_t)kTile, n - base);
+    mbar_wait(&s_bar[buf], (it >> 1) & 1);
+    const unsigned char* hdr = smem + buf * kHdrBytes;
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = q * kThreads + warp * 32 + lane;
+      const bool valid = i < m;
+      uint32_t key = 0xFFu, kb = 0, e = 0;
+      if (valid) {
+        const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
+        kb = P.kb_unknown;
+        if (kid < P.T.nkernel_slots) {
+          const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
+          kb = v.x, e = v.y;
+        }
+        key = kb >> 16;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = __ffs(peers) - 1;
+      uint32_t b = 0;
+      if (valid && lane == leader) b = atomicAdd(&s_cnt[buf][key], (uint32_t)__popc(peers));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      kr[q] = valid ? key | (b + __popc(peers & lt_mask)) << 8 : 0xFFu;
+      rb[q] = (uint32_t)i | (kb & 0xFFFFu) << 16;
+      kn[q] = e;
+    }
+  };
+  // codes of one tile in record order: u8 flags, idempotent bit words, histogram
+  auto emit = [&](uint64_t base, int m) {
+    for (int i0 = warp * 32; i0 < m; i0 += kThreads) {
+      const int i = i0 + lane;
+      const bool valid = i < m;
+      const uint32_t c = valid ? s_code[i] : 0u;
+      const unsigned idem = __ballot_sync(0xffffffffu, valid && c <= V_IDEM_KERNEL);
+      if (valid) flags[base + i] = (uint8_t)c;
+      if (bits != nullptr && lane == 0) bits[(base + i0) >> 5] = idem;
+      const int hb = valid ? count_bin((uint8_t)c) : 16;
+      const unsigned same = __match_any_sync(0xffffffffu, hb);
+      if (valid && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
+    }
+  };
+
+  if ((uint64_t)blockIdx.x < ntiles) keys(blockIdx.x, 0);
+  uint64_t nlo = 0, nll = 0, nnl = 0;  // thread 0: arg bounds of the next tile to stage
+  if (tid == 0) bounds(blockIdx.x + 2 * G, nlo, nll, nnl);
+  uint32_t it = 0;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
+    const uint32_t buf = it & 1;
+    const uint64_t base = tile * kTile;
+    const int m = (int)min((uint64_t)kTile, n - base);
+    __syncthreads();  // B_a: eval(t-1) and keys(t) done
+    if (it > 0) {
+      if (tid == 0) {
+        stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
+                   &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
+        bounds(tile + 2 * G, nlo, nll, nnl);
+      }
+      emit(base - G * kTile, kTile);  // tiles before the last are full
+    }
+    // counters and claim index of the other parity: last used before B_b of
+    // t-1, next used after B_b of t
+    if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
+    if (tid == 0) s_next[buf ^ 1] = 0;
+    // scan (every warp, registers): lane l holds keys l and 32 + l as
+    // count | groups << 16, inclusive
+    const uint32_t c0 = s_cnt[buf][lane], c1 = s_cnt[buf][lane + 32];
+    uint32_t v0 = c0 | ((c0 + 31) >> 5) << 16, v1 = c1 | ((c1 + 31) >> 5) << 16;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t a0 = __shfl_up_sync(0xffffffffu, v0, d), a1 = __shfl_up_sync(0xffffffffu, v1, d);
+      if (lane >= d) v0 += a0, v1 += a1;
+    }
+    v1 += __shfl_sync(0xffffffffu, v0, 31);
+    const uint32_t off0 = (v0 & 0xFFFFu) - c0, off1 = (v1 & 0xFFFFu) - c1;
+    const uint32_t ginc0 = v0 >> 16, ginc1 = v1 >> 16;
+    const uint32_t ngrp = __shfl_sync(0xffffffffu, ginc1, 31);
+    // scatter
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const uint32_t key = kr[q] & 0xFFu;
+      const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31), o1 = __shfl_sync(0xffffffffu, off1, key & 31);
+      if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
+    }
+    __syncthreads();  // B_b
+
+    const unsigned char* hdr = smem + buf * kHdrBytes;
+    const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
+    const StageInfo si = s_info[buf];
+    for (uint32_t g = warp_claim(&s_next[buf]); g < ngrp; g = warp_claim(&s_next[buf])) {
+      const uint32_t key =
+          __popc(__ballot_sync(0xffffffffu, ginc0 <= g)) + __popc(__ballot_sync(0xffffffffu, ginc1 <= g));
+      const int kl = (int)(key & 31);
+      const uint32_t gi0 = __shfl_sync(0xffffffffu, ginc0, kl), gi1 = __shfl_sync(0xffffffffu, ginc1, kl);
+      const uint32_t ca = __shfl_sync(0xffffffffu, c0, kl), cb = __shfl_sync(0xffffffffu, c1, kl);
+      const uint32_t oa = __shfl_sync(0xffffffffu, off0, kl), ob = __shfl_sync(0xffffffffu, off1, kl);
+      const uint32_t c = key < 32 ? ca : cb;
+      const uint32_t j = g - ((key < 32 ? gi0 : gi1) - ((c + 31) >> 5));
+      const uint32_t start = (key < 32 ? oa : ob) + 32u * j, rem = c - 32u * j;
+      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+        for (uint32_t q = 0; q < min(rem, 32u); ++q) {
+          const uint32_t wi = s_perm[start + q].x & 0xFFFFu;
+          const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
+          const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                             (uint64_t)r.nargs <= si.hi - r.arg_off;
+          const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                   : B.args + r.arg_off;
+          const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+          if (lane == 0) s_code[wi] = cw;
+        }
+        continue;
+      }
+      if ((uint32_t)lane < rem) {
+        const uint2 pe = s_perm[start + lane];
+        const uint32_t li = pe.x & 0xFFFFu;
+        const picker_rec_t r = rec_from_smem(hdr + 32 * li);
+        const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                           (uint64_t)r.nargs <= si.hi - r.arg_off;
+        uint8_t code;
+        if (local)
+          code = Dispatch::eval(key, pe.x >> 16, pe.y, P, r,
+                                reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo)), B);
+        else
+          code = Dispatch::eval(key, pe.x >> 16, pe.y, P, r, B.args + r.arg_off, B);
+        s_code[li] = code;
+      }
+    }
+    if (tile + G < ntiles) keys(tile + G, it + 1);
+    if (tile + G >= ntiles) {  // last tile of this CTA
+      __syncthreads();
+      emit(base, m);
+    }
+  }
+  __syncthreads();
+  if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid])
+    atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+}
+
 // Dispatch used by the static library: every bin through the table-driven
 // evaluator (grouping by kernel makes its table reads warp-uniform).
 struct GenericDispatch {

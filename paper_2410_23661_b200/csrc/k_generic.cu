@@ -46,6 +46,9 @@ __global__ void __launch_bounds__(256) k_validate_generic(Tables T, DevBatch B, 
 template __global__ void k_validate_bucket<GenericDispatch>(const __grid_constant__ BucketParams,
                                                             const __grid_constant__ DevBatch, uint64_t,
                                                             uint8_t*, uint32_t*, unsigned long long*);
+template __global__ void k_validate_pipe<GenericDispatch>(const __grid_constant__ BucketParams,
+                                                          const __grid_constant__ DevBatch, uint64_t,
+                                                          uint8_t*, uint32_t*, unsigned long long*);
 
 // Table-driven evaluation through the staged + bucketed kernel (key = kernel).
 // Returns cudaErrorInvalidValue when the per-key arrays do not fit in shared
@@ -56,19 +59,23 @@ cudaError_t launch_bucket_generic(const BucketParams& P0, const DevBatch& B, uin
   if (n == 0) return cudaSuccess;
   BucketParams P = P0;  // kb_of / kb_unknown: key = bin (set at load time)
   P.nkeys = P.nbins + 2;  // kernels, unknown ids, wide kernels (P.wide_key = nbins + 1)
-  const size_t smem = bucket_smem_bytes(P.nkeys);
+  const bool pipe = P.nkeys <= kPipeKeys;
+  const size_t smem = pipe ? pipe_smem_bytes_for(kTile, PICKER_ARGS_PER_REC) : bucket_smem_bytes(P.nkeys);
   if (smem > kMaxSmem) return cudaErrorInvalidValue;
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(k_validate_bucket<GenericDispatch>,
+  static size_t configured[2] = {0, 0};
+  if (smem > configured[pipe]) {
+    cudaError_t e = cudaFuncSetAttribute(pipe ? k_validate_pipe<GenericDispatch> : k_validate_bucket<GenericDispatch>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
+    configured[pipe] = smem;
   }
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t cap = (uint64_t)num_sms * kCtasPerSm;
   const uint64_t grid = ntiles < cap ? ntiles : cap;
-  k_validate_bucket<GenericDispatch><<<(unsigned)grid, kThreads, smem, s>>>(P, B, n, flags, bits, counts);
+  if (pipe)
+    k_validate_pipe<GenericDispatch><<<(unsigned)grid, kThreads, smem, s>>>(P, B, n, flags, bits, counts);
+  else
+    k_validate_bucket<GenericDispatch><<<(unsigned)grid, kThreads, smem, s>>>(P, B, n, flags, bits, counts);
   return cudaGetLastError();
 }
 

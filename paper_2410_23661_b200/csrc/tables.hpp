@@ -192,6 +192,13 @@ constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t a
 constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
   return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC);
 }
+// Pipelined variant for at most kPipeKeys grouping keys (k_validate_pipe):
+// staging buffers, s_perm (u32 x 2) and s_code (u8) per record; the per-key
+// counters are static shared memory.
+constexpr uint32_t kPipeKeys = 64;
+constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec) {
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 9 + 128;
+}
 
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind
