@@ -422,7 +422,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 //   - the scatter writes {record | bin << 16, kn} per sorted slot, so an
 //     evaluating lane needs one shared load to find its record and kernel.
 // Per tile t (B = __syncthreads):
-//   B_a | emit(t-1), restage (t-1)'s buffer with t+1, scan + scatter(t) | B_b |
+//   B_a | emit(t-1), scan + scatter(t) | B_b | restage (t-1)'s buffer with t+1,
 //   eval(t), keys(t+1)
 template <class Dispatch>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
@@ -530,14 +530,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const uint64_t base = tile * kTile;
     const int m = (int)min((uint64_t)kTile, n - base);
     __syncthreads();  // B_a: eval(t-1) and keys(t) done
-    if (it > 0) {
-      if (tid == 0) {
-        stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
-                   &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
-        bounds(tile + 2 * G, nlo, nll, nnl);
-      }
-      emit(base - G * kTile, kTile);  // tiles before the last are full
-    }
+    if (it > 0) emit(base - G * kTile, kTile);  // tiles before the last are full
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
     if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
@@ -563,6 +556,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
     }
     __syncthreads();  // B_b
+    // the previous tile's buffers are free: start the copy of the next tile
+    // (after B_b, so this serial thread-0 work is not waited for at a barrier)
+    if (it > 0 && tid == 0) {
+      stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
+                 &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
+      bounds(tile + 2 * G, nlo, nll, nnl);
+    }
 
     const unsigned char* hdr = smem + buf * kHdrBytes;
     const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
