@@ -97,11 +97,14 @@ __device__ __forceinline__ bool launch_limits_ok(const RecVals& X) {
   return X.d[3] * X.d[4] * X.d[5] <= kBlockMaxThreads;
 }
 
-__device__ __forceinline__ bool launch_limits_ok6(int64_t gx, int64_t gy, int64_t gz, int64_t bx,
-                                                  int64_t by, int64_t bz) {
-  if (gx < 1 || gx > 2147483647LL || gy < 1 || gz < 1) return false;
-  if (bx < 1 || bx > 1024 || by < 1 || by > 1024 || bz < 1 || bz > 64) return false;
-  return bx * by * bz <= kBlockMaxThreads;
+// The same limits on the header fields in 32-bit arithmetic (unsigned
+// wrap-around turns each two-sided range test into one compare).
+__device__ __forceinline__ bool launch_limits_rec(const picker_rec_t& r) {
+  const uint32_t gx = r.grid_x, gy = r.grid_y, gz = r.grid_z;
+  const uint32_t bx = r.block_x, by = r.block_y, bz = r.block_z;
+  if (gx - 1u > 2147483646u || gy == 0u || gz == 0u) return false;
+  if (bx - 1u > 1023u || by - 1u > 1023u || bz - 1u > 63u) return false;
+  return bx * by * bz <= (uint32_t)kBlockMaxThreads;  // <= 2^26: no wrap
 }
 
 __device__ __forceinline__ int count_bin(uint8_t code) { return code <= 11 ? code : 15; }

@@ -115,7 +115,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
   s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K) {\n";
   s << "  const int64_t d0 = r.grid_x, d1 = r.grid_y, d2 = r.grid_z, d3 = r.block_x, d4 = r.block_y,"
        " d5 = r.block_z;\n";
-  s << "  if (!launch_limits_ok6(d0, d1, d2, d3, d4, d5)) return V_NI_PRECOND;\n";
+  s << "  if (!launch_limits_rec(r)) return V_NI_PRECOND;\n";
   std::vector<bool> used(np, false);
   for (auto* lst : {&k.pre, &k.glob})
     for (auto& c : *lst) uses(c.op, used);
@@ -419,12 +419,16 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
     src << "__device__ __forceinline__ uint8_t ks" << s << shapes[s];
   // key = shape (warp-uniform); kn = the lane's kernel: constants offset |
   // nparams << 24 (KbEntry, read in the grouping phase)
-  src << "struct JitDispatch {\n  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, "
-         "uint32_t kn, const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
+  // local: the record's args are in the staged span (inside the pool), so
+  // only the arity needs a test
+  src << "struct JitDispatch {\n"
+         "  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local, "
+         "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
          "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
          "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n"
-         "    if (!args_in_range(r, kn >> 24, B.args_lo, B.args_hi)) return V_ERR_ARITY;\n"
+         "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
+         "      return V_ERR_ARITY;\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n"
          "      case " << shape_shortcut << ": return (uint8_t)__ldg(K);\n";

@@ -376,11 +376,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         uint8_t code;
         // two instantiations: with a pointer the compiler can prove is shared
         // memory (LDS), and with a global one (unstaged tiles)
-        if (local)
-          code = Dispatch::eval(key, s_bin[li], s_kn[li], P, r,
-                                reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo)), B);
-        else
-          code = Dispatch::eval(key, s_bin[li], s_kn[li], P, r, B.args + r.arg_off, B);
+        code = Dispatch::eval(key, s_bin[li], s_kn[li], local, P, r,
+                              local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                    : B.args + r.arg_off,
+                              B);
         s_code[li] = code;
       }
     }
@@ -438,6 +437,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + 2 * kArgBufBytes);
   uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);
   __shared__ uint32_t s_cnt[2][kPipeKeys];
+  __shared__ uint32_t s_grp[kTile / 32 + kPipeKeys];  // group -> start | rem << 13 | key << 19
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   __shared__ uint32_t s_next[2];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -555,6 +555,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31), o1 = __shfl_sync(0xffffffffu, off1, key & 31);
       if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
     }
+    // group table: warp w writes groups j = w, w + kWarps, ... of every key
+    {
+      const uint32_t gs0 = ginc0 - ((c0 + 31) >> 5), gs1 = ginc1 - ((c1 + 31) >> 5);
+      for (uint32_t j = warp; 32 * j < c0; j += kWarps)
+        s_grp[gs0 + j] = (off0 + 32 * j) | min(32u, c0 - 32 * j) << 13 | (uint32_t)lane << 19;
+      for (uint32_t j = warp; 32 * j < c1; j += kWarps)
+        s_grp[gs1 + j] = (off1 + 32 * j) | min(32u, c1 - 32 * j) << 13 | (uint32_t)(lane + 32) << 19;
+    }
     __syncthreads();  // B_b
     // the previous tile's buffers are free: start the copy of the next tile
     // (after B_b, so this serial thread-0 work is not waited for at a barrier)
@@ -567,16 +575,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const unsigned char* hdr = smem + buf * kHdrBytes;
     const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
     const StageInfo si = s_info[buf];
+    // (claiming one group ahead was measured slower: a warp holding a claimed
+    // group lengthens the tail, C4 1.04 -> 0.32 G inst/s)
     for (uint32_t g = warp_claim(&s_next[buf]); g < ngrp; g = warp_claim(&s_next[buf])) {
-      const uint32_t key =
-          __popc(__ballot_sync(0xffffffffu, ginc0 <= g)) + __popc(__ballot_sync(0xffffffffu, ginc1 <= g));
-      const int kl = (int)(key & 31);
-      const uint32_t gi0 = __shfl_sync(0xffffffffu, ginc0, kl), gi1 = __shfl_sync(0xffffffffu, ginc1, kl);
-      const uint32_t ca = __shfl_sync(0xffffffffu, c0, kl), cb = __shfl_sync(0xffffffffu, c1, kl);
-      const uint32_t oa = __shfl_sync(0xffffffffu, off0, kl), ob = __shfl_sync(0xffffffffu, off1, kl);
-      const uint32_t c = key < 32 ? ca : cb;
-      const uint32_t j = g - ((key < 32 ? gi0 : gi1) - ((c + 31) >> 5));
-      const uint32_t start = (key < 32 ? oa : ob) + 32u * j, rem = c - 32u * j;
+      const uint32_t e = s_grp[g];
+      const uint32_t key = e >> 19, start = e & 0x1FFFu, rem = (e >> 13) & 63u;
       if (key == P.wide_key) {  // K2: the whole warp on one record at a time
         for (uint32_t q = 0; q < min(rem, 32u); ++q) {
           const uint32_t wi = s_perm[start + q].x & 0xFFFFu;
@@ -596,12 +599,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const picker_rec_t r = rec_from_smem(hdr + 32 * li);
         const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
                            (uint64_t)r.nargs <= si.hi - r.arg_off;
-        uint8_t code;
-        if (local)
-          code = Dispatch::eval(key, pe.x >> 16, pe.y, P, r,
-                                reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo)), B);
-        else
-          code = Dispatch::eval(key, pe.x >> 16, pe.y, P, r, B.args + r.arg_off, B);
+        // one call site: a second inlined copy of every shape function (shared
+        // vs global pointer) doubles the code and thrashes the instruction
+        // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
+        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                 : B.args + r.arg_off;
+        const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
         s_code[li] = code;
       }
     }
@@ -619,10 +622,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 // Dispatch used by the static library: every bin through the table-driven
 // evaluator (grouping by kernel makes its table reads warp-uniform).
 struct GenericDispatch {
-  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn,
+  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local,
                                                  const BucketParams& P, const picker_rec_t& r,
                                                  const int64_t* a, const DevBatch& B) {
-    (void)key, (void)kn;
+    (void)key, (void)kn, (void)local;
     if (bin >= P.nbins) return V_ERR_KERNEL;
     return eval_generic(P.T, r, a, B.args_lo, B.args_hi);
   }
