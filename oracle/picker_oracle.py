@@ -284,8 +284,60 @@ def _opaque_rule(active):
     return (("R", True) in kinds and has_w) or (("W", True) in kinds and has_r)
 
 
-def oracle_interval(kernels, rec):
-    """Verdict code of the range-based validator for one instance."""
+def congruence(d, vals, box):
+    """Stride-aware range (reading Q24): every address of an
+    active descriptor is congruent to r modulo g.
+
+    The terms on one variable with one divisor form a group C * phi(x), C the sum
+    of their coefficients.  g = gcd of |C| over the groups whose phi takes more
+    than one value on the box; the other groups are constants.  g = 0: the
+    descriptor is a single address r.  Otherwise 0 <= r < g.  This is the
+    congruence class the paper's RO example needs (reads
+    {1,3,5} and writes {0,2,4} are both stride 2, residues 1 and 0).
+    """
+    const = vals[d["base"]] if d["base"] is not None else 0
+    groups = {}
+    for t in d["terms"]:
+        c = t["k"] * _prod(vals, t["f"])
+        if t["var"] is None:
+            const += c
+        else:
+            key = (t["var"], t.get("div", 1))
+            groups[key] = groups.get(key, 0) + c
+    g = 0
+    for (v, div), c in groups.items():
+        lo, hi = box[v]
+        if _phi(lo, div) == _phi(hi, div):
+            const += c * _phi(lo, div)
+        else:
+            g = _gcd(g, abs(c))
+    return g, (const % g if g else const)
+
+
+def _gcd(a, b):
+    while b:
+        a, b = b, a % b
+    return a
+
+
+def may_collide(r_cong, r_width, w_cong, w_width):
+    """Can an address a = r (mod gR) touching [a, a + wR - 1] share a byte with
+    an address b = r' (mod gW) touching [b, b + wW - 1]?  b - a ranges over
+    (r' - r) + gcd(gR, gW) * Z; a shared byte needs -(wW - 1) <= b - a <= wR - 1."""
+    (gr, rr), (gw, rw) = r_cong, w_cong
+    G = _gcd(gr, gw)
+    lo, hi = -(w_width - 1), r_width - 1
+    if G == 0:
+        return lo <= rw - rr <= hi
+    return (rw - rr - lo) % G <= hi - lo
+
+
+def oracle_interval(kernels, rec, stride=False):
+    """Verdict code of the range-based validator for one instance.
+
+    ``stride``: the stride-aware variant (row f4): a read/write pair whose byte
+    intervals intersect is an overlap only if their congruence classes can also
+    share a byte (``may_collide``)."""
     code, st = _prefix(kernels, rec)
     if code is not None:
         return code
@@ -295,14 +347,16 @@ def oracle_interval(kernels, rec):
     reads, writes = [], []
     for d, box in active:
         e = interval_extent(d, vals, box)
-        (reads if d["kind"] == "R" else writes).append(e)
+        cg = congruence(d, vals, box) if stride else None
+        (reads if d["kind"] == "R" else writes).append((e, cg, d["width"]))
     # "an instance is considered non-idempotent if there exists any overlap in the
     # read and write addresses ... regardless of the access order";
     # closed byte intervals, touching is not overlapping (reading Q4).
-    for r in reads:
-        for w in writes:
+    for r, rc, rw in reads:
+        for w, wc, ww in writes:
             if r[0] <= w[1] and w[0] <= r[1]:
-                return NI_OVERLAP
+                if not stride or may_collide(rc, rw, wc, ww):
+                    return NI_OVERLAP
     return IDEM_CHECKED
 
 

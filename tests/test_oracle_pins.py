@@ -36,6 +36,7 @@ def _cases():
 def test_paper_examples(G, case):
     r = _rec(case["kernel_id"], case["args"], case["grid"], case["block"])
     assert O.oracle_interval(G, r) == case["interval"]
+    assert O.oracle_interval(G, r, stride=True) == case.get("stride", case["interval"])
     assert O.oracle_exact(G, r) == case["exact"]
     if "extents" in case:
         code, ext = O.extents(G, r)

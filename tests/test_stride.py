@@ -1,0 +1,137 @@
+"""Row f4 (stride-aware ranges, reading Q24): pins for the oracle's congruence
+refinement and GPU parity of the library's stride mode.
+
+Pins (none retypes the oracle's formula): the paper's RO example
+(PAPER.md l.1174-1177), brute-force enumeration of the pair test over explicit
+address sets, the gcd of enumerated address differences, and soundness against
+the exact (enumerating) oracle on random summaries."""
+import itertools
+import math
+
+import numpy as np
+import pytest
+
+import oracle.picker_oracle as O
+from tracegen import golden
+from tracegen.records import RecordBuilder
+from tracegen.synth import random_records, random_summary
+
+
+def _rec(kid, args, grid=(1, 1, 1), block=(1, 1, 1)):
+    b = RecordBuilder()
+    b.add(kid, args, grid=grid, block=block)
+    rec, pool = b.build()
+    return O.decode_record(rec[0], pool)
+
+
+def test_paper_ro_example():
+    """read {1,3,5} and write {0,2,4} do not overlap; the
+    range model says they do, the stride-aware model recovers I."""
+    G = O.index_summary(golden.golden_summary())
+    r = _rec(4, [0], (1, 1, 1), (3, 1, 1))
+    assert O.oracle_interval(G, r) == O.NI_OVERLAP
+    assert O.oracle_interval(G, r, stride=True) == O.IDEM_CHECKED
+    assert O.oracle_exact(G, r) == O.IDEM_CHECKED
+
+
+@pytest.mark.parametrize("gr,gw", [(0, 0), (0, 3), (4, 0), (2, 2), (4, 6), (6, 9), (8, 12), (5, 7), (16, 16)])
+def test_may_collide_brute_force(gr, gw):
+    """The pair test equals an explicit search over the two progressions
+    (widths 1..5, every residue pair): a in rR + gR*Z, b in rW + gW*Z, touching
+    [a, a+wR-1] and [b, b+wW-1]."""
+    span = 120
+    for wr, ww in itertools.product(range(1, 6), repeat=2):
+        for rr in (range(gr) if gr else range(-7, 8)):
+            for rw in (range(gw) if gw else range(-7, 8)):
+                A = [rr] if gr == 0 else range(rr - span * gr // max(gr, 1), span, gr)
+                B = [rw] if gw == 0 else range(rw - span * gw // max(gw, 1), span, gw)
+                Bs = set()
+                for b in B:
+                    Bs.update(range(b, b + ww))
+                truth = any(x in Bs for a in A for x in range(a, a + wr))
+                assert O.may_collide((gr, rr), wr, (gw, rw), ww) == truth, (gr, gw, rr, rw, wr, ww)
+
+
+def _random_batch(seed, n=300):
+    s = random_summary(seed, n_kernels=12)
+    rec, args = random_records(seed + 1000, s, n, max_threads=24, max_grid=3)
+    return s, O.index_summary(s), rec, args
+
+
+@pytest.mark.parametrize("seed", [51, 52])
+def test_congruence_is_gcd_of_address_differences(seed):
+    """Every enumerated address is = r (mod g), and g is exactly the gcd of the
+    differences of the enumerated addresses when every variable's terms share
+    one divisor (descriptors without fresh definitions): a dropped or extra term
+    changes g.  With mixed divisors g only divides that gcd."""
+    s, K, rec, args = _random_batch(seed, n=150)
+    checked = 0
+    for row in rec:
+        r = O.decode_record(row, args)
+        code, st = O._prefix(K, r)
+        if code is not None:
+            continue
+        _, vals, active = st
+        for d, box in active:
+            if d["opaque"] or any("def" in spec for spec in d["vars"].values()):
+                continue
+            if O._box_points(box) > 4096:
+                continue
+            addrs = [O._addr(d, vals, p) for p in O._points(d, box)]
+            g, res = O.congruence(d, vals, box)
+            diff_gcd = 0
+            for a in addrs:
+                diff_gcd = math.gcd(diff_gcd, abs(a - addrs[0]))
+            divs = {}
+            for t in d["terms"]:
+                if t["var"] is not None:
+                    divs.setdefault(t["var"], set()).add(t.get("div", 1))
+            if all(len(v) == 1 for v in divs.values()):
+                assert g == diff_gcd
+            else:
+                assert diff_gcd % g == 0 if g else diff_gcd == 0
+            if g == 0:
+                assert addrs == [res] * len(addrs)
+            else:
+                assert all(a % g == res for a in addrs)
+            checked += 1
+    assert checked > 50
+
+
+@pytest.mark.parametrize("seed", [53, 54, 55])
+def test_stride_between_interval_and_exact(seed):
+    """Soundness and refinement: exact NI => stride NI => interval NI, and the
+    stride variant never changes a code other than 10 -> 0."""
+    s, K, rec, args = _random_batch(seed)
+    same = 0
+    for row in rec:
+        r = O.decode_record(row, args)
+        ci = O.oracle_interval(K, r)
+        cs = O.oracle_interval(K, r, stride=True)
+        ce = O.oracle_exact(K, r, cap=1 << 13)
+        if ci != cs:
+            assert (ci, cs) == (O.NI_OVERLAP, O.IDEM_CHECKED)
+        if ce == O.NI_OVERLAP:
+            assert cs == O.NI_OVERLAP
+        same += ci == cs
+    assert same > 100
+
+
+def test_stride_recovers_ro_on_synthetic_traces():
+    """The interleaved template of the C2 trace (reads even elements, writes odd
+    ones) is the RO shape: the stride variant turns those records into I and the
+    exact verifier agrees."""
+    from tracegen import workloads
+    s, rec, args, meta = workloads.make_c2()
+    K = O.index_summary(s)
+    rng = np.random.default_rng(7)
+    idx = rng.choice(len(rec), size=1500, replace=False)
+    recovered = 0
+    for i in idx:
+        r = O.decode_record(rec[i], args)
+        ci = O.oracle_interval(K, r)
+        cs = O.oracle_interval(K, r, stride=True)
+        if ci != cs:
+            recovered += 1
+            assert O.oracle_exact(K, r, cap=1 << 16) in (O.IDEM_CHECKED, O.EXACT_SKIPPED)
+    assert recovered > 0
