@@ -201,12 +201,21 @@ int picker_validate_sequence(picker_ctx_t* ctx, const picker_batch_t* batch, uin
  * 3 = wide (sort + sweep) path.  Either array may be NULL; cap bounds both.  */
 int picker_kernel_info(picker_ctx_t* ctx, uint32_t* ids_out, uint8_t* path_out, uint32_t cap);
 
-/* Tuning options (semantics never depend on them).  Keys:
+/* Options.  Tuning keys (semantics never depend on them; they take effect at
+ * the next picker_load_summaries):
  *   "jit"          0 = table-driven kernels only, 1 = NVRTC-specialised (default 1)
  *   "wide_pairs"   R*W pair count above which a kernel uses the wide path
  *   "force_path"   0 = automatic, 1 = generic, 2 = jit, 3 = wide
- *   "tile"         records per CTA super-tile in the specialised kernel
- * Takes effect at the next picker_load_summaries.                            */
+ *   "tile", "threads", "ctas", "args_per_rec"   specialised kernel geometry
+ * Semantic key (takes effect at the next picker_validate_batch[_host]):
+ *   "stride"       1 = stride-aware ranges (reading Q24 of
+ *                  DESIGN.md): a read/write pair whose byte intervals intersect
+ *                  is an overlap only if their congruence classes (every address
+ *                  of a descriptor = its lb mod the gcd of its varying
+ *                  coefficients) can share a byte.  Refines code 10 -> 0 on
+ *                  strided sets; every other code is
+ *                  unchanged.  Default 0 (the paper's range model).
+ * Unknown keys: PICKER_EINVAL.                                                */
 int picker_set_option(picker_ctx_t* ctx, const char* key, int64_t value);
 
 /* Per-kernel-launch statistics of the last validate call: number of device

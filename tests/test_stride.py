@@ -135,3 +135,68 @@ def test_stride_recovers_ro_on_synthetic_traces():
             recovered += 1
             assert O.oracle_exact(K, r, cap=1 << 16) in (O.IDEM_CHECKED, O.EXACT_SKIPPED)
     assert recovered > 0
+
+
+# ---- GPU parity of the library's stride mode (picker_set_option "stride") -----
+
+def _gpu_codes(summary, rec, args, **opt):
+    import paper_2410_23661_b200 as pk
+    p = pk.Picker(0, **opt)
+    p.load(summary)
+    p.set_option("stride", 1)
+    flags, bits, counts = p.validate(rec, args)
+    return flags.cpu().numpy(), bits.cpu().numpy().view(np.uint32), counts.cpu().numpy()
+
+
+def _want(summary, rec, args):
+    return np.array(O.oracle_batch_mp(summary, rec, args, O.oracle_interval, stride=True), np.uint8)
+
+
+def _check(got, want):
+    flags, bits, counts = got
+    bad = np.nonzero(flags != want)[0]
+    assert bad.size == 0, f"{bad.size} mismatches at {bad[:8]}: gpu {flags[bad[:8]]} oracle {want[bad[:8]]}"
+    n = len(want)
+    idem = (want <= 1).astype(np.uint8)
+    words = np.packbits(np.pad(idem, (0, (-n) % 32)).reshape(-1, 32)[:, ::-1], axis=1).view(">u4").reshape(-1)
+    assert np.array_equal(bits, words.astype(np.uint32))
+    exp = np.zeros(16, np.int64)
+    for c in want:
+        exp[c if c <= 11 else 15] += 1
+    assert np.array_equal(counts, exp)
+
+
+STRIDE_OPTS = [dict(jit=0), dict(jit=1), dict(jit=1, wide_pairs=4)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("opt", STRIDE_OPTS, ids=str)
+def test_gpu_stride_paper_examples(opt):
+    import json
+    import os
+    s = golden.golden_summary()
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))["cases"]
+    b = RecordBuilder()
+    for c in cases:
+        b.add(c["kernel_id"], c["args"], c["grid"], c["block"])
+    rec, args = b.build()
+    want = np.array([c.get("stride", c["interval"]) for c in cases], np.uint8)
+    _check(_gpu_codes(s, rec, args, **opt), want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [61, 62, 63])
+def test_gpu_stride_random(seed):
+    s = random_summary(seed, n_kernels=40)
+    rec, args = random_records(seed + 1000, s, 3000, max_threads=256, max_grid=64)
+    _check(_gpu_codes(s, rec, args), _want(s, rec, args))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("which", ["c2", "c3"])
+def test_gpu_stride_workloads(which):
+    """The C2 trace (547 kernels: the bucketed kernel) and the C3 base (64
+    kernels), every record against the oracle's stride variant."""
+    from tracegen import workloads
+    s, rec, args, _ = workloads.make_c2() if which == "c2" else workloads.make_c3(n=1 << 12, n_kernels=64)
+    _check(_gpu_codes(s, rec, args), _want(s, rec, args))
