@@ -298,14 +298,20 @@ def t_scan(rng):
     return ("scan", params, ds, pre, []), sample
 
 
-def t_gemm_tvm(rng, *, concat=False):
+def t_gemm_tvm(rng, *, concat=False, small=False):
     """TVM-generated tiled GEMM / implicit-GEMM conv: constant shapes, only
     pointer arguments, fixed launch (TVM kernels are
-    induction-variable loops over loop-invariant expressions)."""
+    induction-variable loops over loop-invariant expressions).  ``small``: shapes
+    the exact (enumerating) verifier finishes on (row f2's Base)."""
     es = rng_pick(rng, [2, 4])
-    M = int(rng_pick(rng, [64, 128, 256, 512, 1024, 3136, 784, 196, 49]))
-    N = int(rng_pick(rng, [64, 128, 256, 512, 1024, 2048]))
-    K = int(rng_pick(rng, [64, 128, 256, 576, 1152, 2304]))
+    if small:
+        M = int(rng_pick(rng, [16, 32, 49, 64]))
+        N = int(rng_pick(rng, [16, 32, 64]))
+        K = int(rng_pick(rng, [16, 32, 64]))
+    else:
+        M = int(rng_pick(rng, [64, 128, 256, 512, 1024, 3136, 784, 196, 49]))
+        N = int(rng_pick(rng, [64, 128, 256, 512, 1024, 2048]))
+        K = int(rng_pick(rng, [64, 128, 256, 576, 1152, 2304]))
     TM, TN = rng_pick(rng, [(32, 32), (64, 64), (16, 64), (64, 16), (8, 8)])
     M = ((M + TM - 1) // TM) * TM
     N = ((N + TN - 1) // TN) * TN
@@ -345,11 +351,11 @@ def t_gemm_tvm(rng, *, concat=False):
     return (name, params, ds, pre, []), sample
 
 
-def t_tvm_fused_ew(rng):
+def t_tvm_fused_ew(rng, small=False):
     """TVM fused elementwise/pooling with constant sizes (no scalar arguments)."""
     w = rng_pick(rng, [2, 4])
     nin = int(rng.integers(1, 4))
-    n = int(rng_pick(rng, [50176, 100352, 200704, 401408, 802816]))
+    n = int(rng_pick(rng, [1024, 2048, 4096] if small else [50176, 100352, 200704, 401408, 802816]))
     bd = rng_pick(rng, [256, 512, 1024])
     g = (n + bd - 1) // bd
     params = [("out", "ptr")] + [(f"in{i}", "ptr") for i in range(nin)]
@@ -577,20 +583,21 @@ def make_c4(seed=23663, n=1 << 12, n_kernels=32):
     return {"version": 1, "kernels": ks}, rec, args, {"ptr_mask": np.array(ptr_mask, bool)}
 
 
-def make_c3(seed=23662, n=1 << 14, n_kernels=64):
+def make_c3(seed=23662, n=1 << 14, n_kernels=64, small=False):
     """C3 base: TVM-style tiled GEMM/conv and fused elementwise kernels with
-    affine strided ranges, some RO-prone (concatenated outputs)."""
+    affine strided ranges, some RO-prone (concatenated outputs).  ``small``:
+    the small-grid subset the exact verifier enumerates (rows a10, f2)."""
     rng = np.random.default_rng(seed)
     alloc = Alloc(rng)
     ks, smps = [], []
     for kid in range(n_kernels):
         r = rng.random()
         if r < 0.1:
-            (nm, p, d, pre, gl), smp = t_gemm_tvm(rng, concat=True)
+            (nm, p, d, pre, gl), smp = t_gemm_tvm(rng, concat=True, small=small)
         elif r < 0.75:
-            (nm, p, d, pre, gl), smp = t_gemm_tvm(rng)
+            (nm, p, d, pre, gl), smp = t_gemm_tvm(rng, small=small)
         else:
-            (nm, p, d, pre, gl), smp = t_tvm_fused_ew(rng)
+            (nm, p, d, pre, gl), smp = t_tvm_fused_ew(rng, small=small)
         ks.append(_finish(kid, f"{nm}{kid}", p, d, pre, gl))
         smps.append(smp)
     st = ProgState(rng, alloc, dict(p_alias=0.0, ni_share=0, p_opaque_on=0), 512)
