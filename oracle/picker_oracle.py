@@ -527,3 +527,73 @@ def oracle_windows(summary, rec_array, args, window, mode=SEQ_SEQUENTIAL):
     kernels = index_summary(summary)
     recs = [decode_record(r, args) for r in rec_array]
     return [oracle_sequence(kernels, recs[w:w + window], mode) for w in range(0, len(recs), window)]
+
+
+# ---- row f3: consumer models on the verdicts (§7.5 l.1612-1690) ------
+
+MODEL_MAX_READS = 128  # reading Q25: more active read extents -> input size unknown
+MODEL_HIST_BUCKETS = 129  # preemption-latency histogram: 1 us buckets, last = >= 128 us
+
+
+def oracle_input_bytes(kernels, rec):
+    """Bytes an Asymmetric-Resilience checkpoint copies for one instance: "AR
+    checkpoints the input buffer of every GPU kernel instance" (PAPER.md
+    l.1620-1622), read as the length of the union of the instance's active,
+    non-opaque read extents (reading Q25).  Returns None (unknown) when the
+    extents are not computable: unknown kernel, arity, a kernel-level NONIDEM
+    class (no verified summary), a failing launch limit / precondition / global
+    condition, an opaque read, or more than MODEL_MAX_READS read extents."""
+    code, st = _prefix(kernels, rec, through_idem=True)
+    if code is not None:
+        return None
+    _, vals, active = st
+    ext = []
+    for d, box in active:
+        if d["kind"] != "R":
+            continue
+        if d["opaque"]:
+            return None
+        ext.append(interval_extent(d, vals, box))
+    if len(ext) > MODEL_MAX_READS:
+        return None
+    merged = []  # union of closed intervals: merge in lb order
+    for lb, ub in sorted(ext):
+        if merged and lb <= merged[-1][1] + 1:
+            merged[-1][1] = max(merged[-1][1], ub)
+        else:
+            merged.append([lb, ub])
+    return sum(ub - lb + 1 for lb, ub in merged)
+
+
+def oracle_models(summary, rec_array, args, codes, ctx_bytes, kill_ns=1000, save_bytes_per_us=1000):
+    """AR checkpoint bytes and Chimera preemption latency.
+
+    AR: without idempotency every instance's input is checkpointed; with it only
+    the non-idempotent ones (codes other than 0 and 1).  Instances whose input
+    size is unknown count 0 bytes and are counted in ``unknown_input``.
+    Chimera: preempting an idempotent instance kills it (``kill_ns``, "less than
+    1 microsecond", l.1677-1679); a non-idempotent one saves its context,
+    ``ctx_bytes * 1000 // save_bytes_per_us`` ns.  Integer nanoseconds; the
+    histogram has 1 us buckets (bucket 128 = 128 us and above)."""
+    K = index_summary(summary)
+    out = {"n": len(rec_array), "n_idem": 0, "ckpt_bytes_all": 0, "ckpt_bytes_ni": 0, "unknown_input": 0,
+           "preempt_ns_without": 0, "preempt_ns_with": 0,
+           "hist_without": [0] * MODEL_HIST_BUCKETS, "hist_with": [0] * MODEL_HIST_BUCKETS}
+    for row, code, cb in zip(rec_array, codes, ctx_bytes):
+        r = decode_record(row, args)
+        idem = int(code) in IDEMPOTENT_CODES
+        b = oracle_input_bytes(K, r)
+        if b is None:
+            out["unknown_input"] += 1
+            b = 0
+        out["ckpt_bytes_all"] += b
+        if not idem:
+            out["ckpt_bytes_ni"] += b
+        out["n_idem"] += idem
+        save = int(cb) * 1000 // save_bytes_per_us
+        lat = kill_ns if idem else save
+        out["preempt_ns_without"] += save
+        out["preempt_ns_with"] += lat
+        out["hist_without"][min(save // 1000, MODEL_HIST_BUCKETS - 1)] += 1
+        out["hist_with"][min(lat // 1000, MODEL_HIST_BUCKETS - 1)] += 1
+    return out
