@@ -195,6 +195,40 @@ int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t 
 int picker_validate_sequence(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                              uint32_t window, uint32_t mode, uint8_t* out, void* stream);
 
+/* ---- row f3: consumer models on the verdicts (§7.5) ------------- */
+#define PICKER_MODEL_HIST 129 /* 1-us latency buckets; the last holds >= 128 us */
+typedef struct {
+  uint64_t kill_ns;           /* preemption latency of an idempotent instance:
+                               * "less than 1 microsecond" (l.1677-1679) -> 1000 */
+  uint64_t save_bytes_per_us; /* context-save bandwidth (> 0), bytes per us     */
+} picker_model_params_t;
+typedef struct {
+  uint64_t n, n_idem;            /* records; records with code 0 or 1           */
+  uint64_t ckpt_bytes_all;       /* AR without idempotency: sum of input bytes  */
+  uint64_t ckpt_bytes_ni;        /* AR with Picker: over non-idempotent records */
+  uint64_t unknown_input;        /* records whose input bytes are unknown (0)   */
+  uint64_t preempt_ns_without;   /* Chimera: sum of context-save latencies      */
+  uint64_t preempt_ns_with;      /* kill_ns for idempotent records instead      */
+  uint64_t hist_without[PICKER_MODEL_HIST], hist_with[PICKER_MODEL_HIST];
+} picker_model_out_t;
+
+/* Checkpoint and preemption models of the paper's case studies, evaluated on
+ * the device in one pass over the records and their verdict codes:
+ *   Asymmetric Resilience (l.1618-1640, "AR checkpoints the input buffer of
+ *   every GPU kernel instance ... For idempotent instances, AR avoids the memory
+ *   checkpointing"): input bytes of a record = length of the union of its
+ *   active non-opaque read extents; unknown (counted as 0, reported) for
+ *   unknown kernels, arity errors, kernel-level NONIDEM classes, failed
+ *   launch limits / preconditions / global conditions, opaque reads, or more
+ *   than 128 read extents (reading Q25).
+ *   Chimera (l.1666-1690): latency = kill_ns if the record's code is 0 or 1,
+ *   else ctx_bytes[i] * 1000 / save_bytes_per_us ns (ctx_bytes < 2^54).
+ * codes: device u8[n] (e.g. picker_validate_batch's flags); ctx_bytes: device
+ * u64[n] or NULL (all 0); out: HOST struct.  SYNCHRONOUS on `stream`.         */
+int picker_consumer_models(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n, const uint8_t* codes,
+                           const uint64_t* ctx_bytes, const picker_model_params_t* params,
+                           picker_model_out_t* out, void* stream);
+
 /* Number of kernels loaded and the path each kernel was compiled to
  * (per-kernel introspection for tests): path_out[i] for kernel id ids_out[i];
  * path 0 = shortcut, 1 = generic table path, 2 = specialised (JIT) path,

@@ -33,6 +33,19 @@ class picker_batch_t(ctypes.Structure):
 
 assert ctypes.sizeof(picker_rec_t) == 32
 
+MODEL_HIST = 129
+
+
+class picker_model_params_t(ctypes.Structure):
+    _fields_ = [("kill_ns", ctypes.c_uint64), ("save_bytes_per_us", ctypes.c_uint64)]
+
+
+class picker_model_out_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_uint64), ("n_idem", ctypes.c_uint64), ("ckpt_bytes_all", ctypes.c_uint64),
+                ("ckpt_bytes_ni", ctypes.c_uint64), ("unknown_input", ctypes.c_uint64),
+                ("preempt_ns_without", ctypes.c_uint64), ("preempt_ns_with", ctypes.c_uint64),
+                ("hist_without", ctypes.c_uint64 * MODEL_HIST), ("hist_with", ctypes.c_uint64 * MODEL_HIST)]
+
 P = ctypes.c_void_p
 U64 = ctypes.c_uint64
 
@@ -51,6 +64,9 @@ SIGNATURES = {
     "picker_exact_check": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, U64, P]),
     "picker_validate_sequence": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, ctypes.c_uint32,
                                                 ctypes.c_uint32, P, P]),
+    "picker_consumer_models": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P,
+                                              ctypes.POINTER(picker_model_params_t),
+                                              ctypes.POINTER(picker_model_out_t), P]),
     "picker_kernel_info": (ctypes.c_int, [P, P, P, ctypes.c_uint32]),
     "picker_set_option": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.c_int64]),
     "picker_last_launch_count": (ctypes.c_int, [P]),

@@ -55,6 +55,10 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
                             uint8_t* out, int num_sms, cudaStream_t s, std::string& err);
 
+cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const uint8_t* codes,
+                          const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,
+                          int num_sms, cudaStream_t s);
+
 cudaError_t launch_exact(const Tables& T, const DevBatch& b, uint64_t n, uint8_t* out,
                          unsigned long long* counts, uint64_t max_points, int num_sms,
                          cudaStream_t s, int* launches, std::string& err);

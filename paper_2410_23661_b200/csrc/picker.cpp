@@ -428,6 +428,22 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
   return PICKER_OK;
 }
 
+int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, const uint8_t* codes,
+                           const uint64_t* ctx_bytes, const picker_model_params_t* prm, picker_model_out_t* out,
+                           void* stream) {
+  int st = check_batch(c, b, n, codes);
+  if (st) return st;
+  if (!prm || !out || prm->save_bytes_per_us == 0)
+    return fail(c, PICKER_EINVAL, "params/out must be non-null and save_bytes_per_us > 0");
+  DevGuard g(c->device);
+  DevBatch db{b->rec, b->args, 0, b->args_len};
+  cudaError_t e = launch_models(c->P.T, db, n, codes, ctx_bytes, prm->kill_ns, prm->save_bytes_per_us, out,
+                                c->num_sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "consumer models");
+  c->last_launches = n ? 1 : 0;
+  return PICKER_OK;
+}
+
 int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* out,
                        uint64_t* counts, uint64_t max_points, void* stream) {
   int st = check_batch(c, b, n, out);

@@ -12,7 +12,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from ._lib import PickerError, lib, picker_batch_t
+from ._lib import PickerError, lib, picker_batch_t, picker_model_out_t, picker_model_params_t
 
 NUM_COUNTS = 16
 CODE_NAMES = {0: "IDEM_CHECKED", 1: "IDEM_KERNEL", 2: "NI_KERNEL_SO", 3: "NI_KERNEL_ATOMIC",
@@ -193,3 +193,30 @@ class Picker:
             cnt.data_ptr() if cnt is not None else None, int(max_points),
             _stream_handle(stream)))
         return out, cnt
+
+    def consumer_models(self, rec, args, codes, ctx_bytes=None, *, kill_ns=1000, save_bytes_per_us=1000,
+                        stream=None):
+        """Row f3 (picker_consumer_models): AR checkpoint bytes and Chimera
+        preemption latency for a batch and its verdict codes.  Synchronous;
+        returns a dict of Python ints (histograms as lists)."""
+        rec = records_tensor(rec, self.device)
+        if not torch.is_tensor(args):
+            args = torch.from_numpy(np.asarray(args, dtype=np.int64))
+        args = args.to(self.device)
+        codes = codes.to(self.device) if torch.is_tensor(codes) else torch.from_numpy(
+            np.asarray(codes, np.uint8)).to(self.device)
+        n = rec.shape[0]
+        cb = None
+        if ctx_bytes is not None:
+            cb = torch.from_numpy(np.asarray(ctx_bytes, np.uint64).view(np.int64)).to(self.device) \
+                if not torch.is_tensor(ctx_bytes) else ctx_bytes.to(self.device)
+        prm = picker_model_params_t(int(kill_ns), int(save_bytes_per_us))
+        out = picker_model_out_t()
+        b = self._batch(rec, args, True)
+        self._check(lib.picker_consumer_models(
+            self._h, ctypes.byref(b), n, codes.data_ptr(), cb.data_ptr() if cb is not None else None,
+            ctypes.byref(prm), ctypes.byref(out), _stream_handle(stream)))
+        return {"n": out.n, "n_idem": out.n_idem, "ckpt_bytes_all": out.ckpt_bytes_all,
+                "ckpt_bytes_ni": out.ckpt_bytes_ni, "unknown_input": out.unknown_input,
+                "preempt_ns_without": out.preempt_ns_without, "preempt_ns_with": out.preempt_ns_with,
+                "hist_without": list(out.hist_without), "hist_with": list(out.hist_with)}
