@@ -481,21 +481,24 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
   return true;
 }
 
-// tile = 0 (auto): the largest tile (<= 512 records, a multiple of 32) whose
-// argument span fits the 4096-slot staging buffer when records carry 1.25x the
-// mean parameter count of the loaded COND kernels; args_per_rec = 4096 / tile.
+// tile = 0 (auto, the default): geometry from the loaded COND kernels' mean
+// parameter count.  Few arguments (C2: 3.7, C3: 3.4): 448-record tiles, 224
+// threads, 3 CTAs/SM, 5 staged argument slots per record -- 21 warps/SM instead
+// of 16 (measured C2 35.0 -> 37.0 G inst/s, profiles/r01_sweep_geometry.txt).
+// Many arguments (C4: 33): 512 / 256 / 2 / 8 (registers matter more than
+// occupancy there).
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   if (opt.tile != 0) return opt;
   double sum = 0;
   int cnt = 0;
   for (auto& k : ks)
     if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC) sum += k.param_names.size(), ++cnt;
-  const double apr = std::max(4.0, 1.25 * (cnt ? sum / cnt : 4.0));
-  // a multiple of the CTA size (k_validate_pipe hands each thread tile/threads records)
-  int tile = (int)(4096.0 / apr) / opt.threads * opt.threads;
-  tile = std::max(opt.threads, std::min(std::max(512, opt.threads), tile));
-  opt.tile = tile;
-  opt.args_per_rec = 4096 / tile;
+  const double mean = cnt ? sum / cnt : 4.0;
+  if (mean <= 6.0) {
+    opt.tile = 448, opt.threads = 224, opt.ctas = 3, opt.args_per_rec = 5;
+  } else {
+    opt.tile = 512, opt.threads = 256, opt.ctas = 2, opt.args_per_rec = 8;
+  }
   return opt;
 }
 
@@ -564,6 +567,16 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     jit_destroy(m);
     return nullptr;
   }
+  // the persistent grid is sized by the CTAs that are actually resident
+  int resident = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, (const void*)m->kernel, m->threads, m->smem);
+  if (e != cudaSuccess || resident < 1) {
+    err = std::string("the specialised kernel does not fit on an SM: ") +
+          (e != cudaSuccess ? cudaGetErrorString(e) : "0 resident CTAs");
+    jit_destroy(m);
+    return nullptr;
+  }
+  m->ctas = std::min(m->ctas, resident);
   return m;
 }
 

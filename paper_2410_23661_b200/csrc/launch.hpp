@@ -20,7 +20,7 @@ struct Options {
   int force_path = 0;  // 0 auto, 1 generic (table-driven), 2 jit, 3 wide, for every COND kernel
   int64_t wide_pairs = 1 << 20;  // read x write pairs above which a kernel takes the wide path
   // geometry of the specialised kernel (tuning; k_bucket.cuh)
-  int tile = 512, threads = 256, ctas = 2, args_per_rec = 8;  // tile 0: chosen at load (jit.cpp)
+  int tile = 0, threads = 256, ctas = 2, args_per_rec = 8;  // tile 0: chosen at load (jit.cpp)
   bool stride = false;  // stride-aware ranges (row f4): validate through eval_stride (k_stride.cu)
 };
 

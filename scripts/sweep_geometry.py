@@ -9,12 +9,14 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2410_23661_b200 as pk  # noqa: E402
-from tracegen.workloads import make_c2, replicate  # noqa: E402
+from tracegen.workloads import make_c2, make_c3, make_c4, replicate  # noqa: E402
 
 
 def main():
-    reps = int(os.environ.get("REPLICAS", "686"))
-    s, rec, a, meta = make_c2()
+    w = os.environ.get("WORKLOAD", "c2")
+    reps = int(os.environ.get("REPLICAS", {"c2": "686", "c3": "64", "c4": "512"}[w]))
+    s, rec, a, meta = {"c2": make_c2, "c3": lambda: make_c3(n=1 << 14, n_kernels=64),
+                       "c4": lambda: make_c4(n=1 << 13, n_kernels=32)}[w]()
     R, A = replicate(rec, a, meta["ptr_mask"], reps, 1 << 37)
     dev = torch.device("cuda", 0)
     rd = torch.from_numpy(R.view(np.uint8).reshape(-1, 32)).to(dev)
