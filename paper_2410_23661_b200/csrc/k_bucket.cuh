@@ -449,7 +449,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   const uint64_t G = gridDim.x;
   if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
   for (int b = tid; b < 2 * (int)kPipeKeys; b += kThreads) (&s_cnt[0][0])[b] = 0;
-  if (tid < 2) s_next[tid] = 0;
+  // warp w's first group of a tile is group w (no claim); the counter hands
+  // out the rest from kWarps on
+  if (tid < 2) s_next[tid] = kWarps;
   auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& lo_last, uint64_t& n_last) {
     const uint64_t base = tile * kTile;
     lo = lo_last = n_last = 0;
@@ -534,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
     if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
-    if (tid == 0) s_next[buf ^ 1] = 0;
+    if (tid == 0) s_next[buf ^ 1] = kWarps;
     // scan (every warp, registers): lane l holds keys l and 32 + l as
     // count | groups << 16, inclusive
     const uint32_t c0 = s_cnt[buf][lane], c1 = s_cnt[buf][lane + 32];
@@ -577,7 +579,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const StageInfo si = s_info[buf];
     // (claiming one group ahead was measured slower: a warp holding a claimed
     // group lengthens the tail, C4 1.04 -> 0.32 G inst/s)
-    for (uint32_t g = warp_claim(&s_next[buf]); g < ngrp; g = warp_claim(&s_next[buf])) {
+    for (uint32_t g = (uint32_t)warp; g < ngrp; g = warp_claim(&s_next[buf])) {
       const uint32_t e = s_grp[g];
       const uint32_t key = e >> 19, start = e & 0x1FFFu, rem = (e >> 13) & 63u;
       if (key == P.wide_key) {  // K2: the whole warp on one record at a time
@@ -597,8 +599,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const uint2 pe = s_perm[start + lane];
         const uint32_t li = pe.x & 0xFFFFu;
         const picker_rec_t r = rec_from_smem(hdr + 32 * li);
-        const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
-                           (uint64_t)r.nargs <= si.hi - r.arg_off;
+        // args inside the staged span [lo, hi) (span < 2^32 slots): one 64-bit
+        // subtraction, then 32-bit compares
+        const uint64_t rel = r.arg_off - si.lo;
+        const bool local = si.staged && (rel >> 32) == 0 && (uint32_t)rel <= (uint32_t)(si.hi - si.lo) &&
+                           r.nargs <= (uint32_t)(si.hi - si.lo) - (uint32_t)rel;
         // one call site: a second inlined copy of every shape function (shared
         // vs global pointer) doubles the code and thrashes the instruction
         // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
