@@ -485,8 +485,10 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 // parameter count.  Few arguments (C2: 3.7, C3: 3.4): 448-record tiles, 224
 // threads, 3 CTAs/SM, 5 staged argument slots per record -- 21 warps/SM instead
 // of 16 (measured C2 35.0 -> 37.0 G inst/s, profiles/r01_sweep_geometry.txt).
-// Many arguments (C4: 33): 512 / 256 / 2 / 8 (registers matter more than
-// occupancy there).
+// Many arguments (C4: 33): the argument spans do not fit a staging buffer
+// anyway, so the shared memory goes to 2048-record tiles of headers (512
+// threads, 1 CTA/SM, 1 staged slot per record): 4x more records per shape per
+// tile fill the warps (C4 1.09 -> 1.60 G inst/s, profiles/r01_sweep_geometry.txt).
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   if (opt.tile != 0) return opt;
   double sum = 0;
@@ -497,7 +499,7 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   if (mean <= 6.0) {
     opt.tile = 448, opt.threads = 224, opt.ctas = 3, opt.args_per_rec = 5;
   } else {
-    opt.tile = 512, opt.threads = 256, opt.ctas = 2, opt.args_per_rec = 8;
+    opt.tile = 2048, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1;
   }
   return opt;
 }
