@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-latency", action="store_true", help="skip the small-batch latency probe")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
     ap.add_argument("--path", default="auto", choices=["auto", "generic", "jit"])
     ap.add_argument("--opt", action="append", default=[], help="library option key=value (tuning)")
@@ -187,6 +188,49 @@ def cpu_baseline(s, rec, a, seconds):
     return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{copies} full copies of the C2 base trace ({len(rec)} records each), "
                       f"oracle_interval over a {cores}-process pool, {dt:.1f} s"}
+
+
+def small_batch_latency(p, rec_d, args_d, dev, sizes=(1, 32, 1024), reps=200):
+    """the paper-comparable latency of validating a few launches.
+    Each size is captured once in a CUDA graph (memset of the counts + the
+    validation kernel) and replayed; `device_us` = CUDA events around the
+    replay, `host_us` = host wall time of replay + D2H copy of the codes into
+    pinned memory + stream sync (what a launcher waiting on the verdict sees)."""
+    import torch
+
+    out = {}
+    for nb in sizes:
+        r = rec_d[:nb]
+        f = torch.empty(nb, dtype=torch.uint8, device=dev)
+        b = torch.empty((nb + 31) // 32, dtype=torch.int32, device=dev)
+        c = torch.empty(16, dtype=torch.int64, device=dev)
+        side = torch.cuda.Stream(dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            for _ in range(3):
+                p.validate(r, args_d, out=(f, b, c))
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            p.validate(r, args_d, out=(f, b, c))
+        hf = torch.empty(nb, dtype=torch.uint8).pin_memory()
+        st = torch.cuda.current_stream()
+        dev_us, host_us = [], []
+        for i in range(reps + 10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            t0 = time.perf_counter()
+            e0.record(st)
+            g.replay()
+            e1.record(st)
+            hf.copy_(f, non_blocking=True)
+            st.synchronize()
+            t1 = time.perf_counter()
+            if i >= 10:
+                dev_us.append(1e3 * e0.elapsed_time(e1))
+                host_us.append(1e6 * (t1 - t0))
+        out[str(nb)] = {"device_us_p50": float(np.median(dev_us)), "device_us_p90": float(np.percentile(dev_us, 90)),
+                        "host_us_p50": float(np.median(host_us)), "host_us_p90": float(np.percentile(host_us, 90))}
+    return out
 
 
 def run_reference(args):
@@ -357,6 +401,8 @@ def main():
         e2e_ok = bool((fh.numpy() == got).all())
         mism += 0 if e2e_ok else 1
 
+    latency = small_batch_latency(p, rec_d, args_d, dev) if rank == 0 and not args.no_latency else None
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -396,6 +442,8 @@ def main():
         "data": "synthetic",
         "config": workload_config(args, world, len(base_rec), flush),
         "p50_us_per_instance": 1e3 * float(np.median(step_ms)) / n,
+        "p90_us_per_instance": 1e3 * float(np.percentile(step_ms, 90)) / n,
+        "small_batch_latency": latency,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel_ms": kmean, "algorithmic_bytes_per_launch": abytes,
