@@ -259,6 +259,13 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
       put(src_out, src_len, plan.src);
       return PICKER_ECUDA;
     }
+    if (const char* dump = getenv("PICKER_DUMP_CUBIN")) {  // inspection aid (cuobjdump -sass / -res-usage)
+      FILE* f = fopen(dump, "wb");
+      if (f) {
+        fwrite(cubin.data(), 1, cubin.size(), f);
+        fclose(f);
+      }
+    }
     put(msg, msg_len, "cubin " + std::to_string(cubin.size()) + " bytes, " +
                           std::to_string(plan.consts.size()) + " constants, kernel " + lowered);
     put(src_out, src_len, plan.src);
