@@ -125,6 +125,8 @@ __device__ __forceinline__ uint32_t warp_claim(uint32_t* counter) {
   return __shfl_sync(0xffffffffu, g, 0);
 }
 
+// The bucketed kernel for more than kPipeKeys grouping keys (the table-driven
+// path groups by kernel: C2 with the specialised module off has 549 keys).
 template <class Dispatch>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k_validate_bucket(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B,
@@ -132,36 +134,28 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                       uint32_t* __restrict__ bits, unsigned long long* __restrict__ counts) {
   extern __shared__ __align__(128) unsigned char smem[];
   const uint32_t nk = P.nkeys;
-  // few keys (the specialised module: one per shape): every warp scans the key
-  // counts itself, in registers, and claims groups from them -- no group table
-  // and no barrier around the scan
-  const bool small = nk <= 64;
   // staging buffers: headers at smem + buf*kHdrBytes, args at smem + kArgOff + buf*kArgBufBytes
   constexpr uint32_t kHdrBytes = kTile * 32;
   constexpr uint32_t kArgOff = 2 * kHdrBytes;
   uint32_t* s_kn = reinterpret_cast<uint32_t*>(smem + kArgOff + 2 * kArgBufBytes);  // KbEntry.kn
   uint16_t* s_key = reinterpret_cast<uint16_t*>(s_kn + kTile);
   uint16_t* s_bin = s_key + kTile;
-  uint16_t* s_perm = s_bin + kTile;   // key-sorted slot -> record
-  uint16_t* s_rank = s_perm + kTile;  // record -> rank among the tile's records of its key
-  uint8_t* s_code = reinterpret_cast<uint8_t*>(s_rank + kTile);
-  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_code + kTile);  // [2][nk] (per tile parity)
-  uint32_t* s_off = s_cnt + 2 * nk;
+  uint16_t* s_perm = s_bin + kTile;  // key-sorted slot -> record
+  uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);
+  uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_code + kTile);  // kTile is a multiple of 32
+  uint32_t* s_off = s_cnt + nk;
   uint32_t* s_cur = s_off + nk;
   uint32_t* s_grp = s_cur + nk;
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   __shared__ uint32_t s_wsum[2][kWarps];
-  __shared__ uint32_t s_ngrp, s_next[2];
+  __shared__ uint32_t s_ngrp, s_next;
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ StageInfo s_info[2];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t lt_mask = (1u << lane) - 1u;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t G = gridDim.x;
   if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
-  for (uint32_t b = tid; b < 2 * nk; b += kThreads) s_cnt[b] = 0;
-  if (tid < 2) s_next[tid] = 0;
   // arg_off bounds of a tile, loaded ahead of its staging
   auto bounds = [&](uint64_t tile, uint64_t& lo, uint64_t& lo_last, uint64_t& n_last) {
     const uint64_t base = tile * kTile;
@@ -192,113 +186,39 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const uint32_t buf = it & 1, parity = (it >> 1) & 1;
     const uint64_t base = tile * kTile;
     const int m = (int)min((uint64_t)kTile, n - base);
-    uint32_t* cnt = s_cnt + buf * nk;
     uint64_t nlo = 0, nll = 0, nnl = 0;
     if (tid == 0) bounds(tile + 2 * G, nlo, nll, nnl);  // consumed after this tile
-    if (!small)
-      for (uint32_t b = tid; b < nk; b += kThreads) cnt[b] = 0;
+    for (uint32_t b = tid; b < nk; b += kThreads) s_cnt[b] = 0;
     mbar_wait(&s_bar[buf], parity);
     const unsigned char* hdr = smem + buf * kHdrBytes;
     const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
     const StageInfo si = s_info[buf];
-    // small: the other parity's counters and claim index were last used before
-    // the previous tile's scatter barrier and are next used after this tile's
-    if (small) {
-      for (uint32_t b = tid; b < nk; b += kThreads) s_cnt[(buf ^ 1) * nk + b] = 0;
-      if (tid == 0) s_next[buf ^ 1] = 0;
-    } else {
-      __syncthreads();
-    }
+    __syncthreads();
 
-    // 1. keys; per-key counts (small: match_any-aggregated, and each record's
-    //    rank within its key, so the scatter needs no atomics)
-    for (int i0 = warp * 32; i0 < m; i0 += kThreads) {
-      const int i = i0 + lane;
-      const bool valid = i < m;
-      uint32_t key = 0xFFFFu;
-      if (valid) {
-        const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
-        uint32_t kb = P.kb_unknown, kn = 0;
-        if (kid < P.T.nkernel_slots) {
-          const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
-          kb = v.x, kn = v.y;
-        }
-        key = kb >> 16;
-        s_bin[i] = (uint16_t)(kb & 0xFFFFu);
-        s_kn[i] = kn;
-        s_key[i] = (uint16_t)key;
-        if (!small) atomicAdd(cnt + key, 1u);
+    // 1. keys and per-key counts
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
+      uint32_t kb = P.kb_unknown, kn = 0;
+      if (kid < P.T.nkernel_slots) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
+        kb = v.x, kn = v.y;
       }
-      if (small) {
-        const unsigned peers = __match_any_sync(0xffffffffu, key);
-        const int leader = __ffs(peers) - 1;
-        uint32_t b = 0;
-        if (valid && lane == leader) b = atomicAdd(cnt + key, (uint32_t)__popc(peers));
-        b = __shfl_sync(0xffffffffu, b, leader);
-        if (valid) s_rank[i] = (uint16_t)(b + __popc(peers & lt_mask));
-      }
+      const uint32_t key = kb >> 16;
+      s_bin[i] = (uint16_t)(kb & 0xFFFFu);
+      s_kn[i] = kn;
+      s_key[i] = (uint16_t)key;
+      atomicAdd(s_cnt + key, 1u);
     }
     __syncthreads();
 
-    // 2.+3. offsets of each key's records and 32-record groups; scatter
-    uint32_t off0 = 0, off1 = 0, ginc0 = 0, ginc1 = 0, c0 = 0, c1 = 0, ngrp;
-    if (small) {
-      // lane l holds keys l and 32 + l: count | groups << 16, inclusive scans
-      c0 = (uint32_t)lane < nk ? cnt[lane] : 0u;
-      c1 = (uint32_t)lane + 32 < nk ? cnt[lane + 32] : 0u;
-      uint32_t v0 = c0 | ((c0 + 31) >> 5) << 16, v1 = c1 | ((c1 + 31) >> 5) << 16;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t a0 = __shfl_up_sync(0xffffffffu, v0, d), a1 = __shfl_up_sync(0xffffffffu, v1, d);
-        if (lane >= d) v0 += a0, v1 += a1;
-      }
-      v1 += __shfl_sync(0xffffffffu, v0, 31);
-      off0 = (v0 & 0xFFFFu) - c0;
-      off1 = (v1 & 0xFFFFu) - c1;
-      ginc0 = v0 >> 16;
-      ginc1 = v1 >> 16;
-      ngrp = __shfl_sync(0xffffffffu, ginc1, 31);
-      for (int i0 = warp * 32; i0 < m; i0 += kThreads) {
-        const int i = i0 + lane;
-        const uint32_t key = i < m ? s_key[i] : 0u;
-        const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31),
-                       o1 = __shfl_sync(0xffffffffu, off1, key & 31);
-        if (i < m) s_perm[(key < 32 ? o0 : o1) + s_rank[i]] = (uint16_t)i;
-      }
-    } else if (nk <= 32 * 64) {  // one warp scans, the others wait
-      if (warp == 0) {
-        const uint32_t per = (nk + 31) / 32;
-        const uint32_t b0 = min(nk, lane * per), b1 = min(nk, b0 + per);
-        uint32_t rs = 0, gs = 0;
-        for (uint32_t b = b0; b < b1; ++b) {
-          const uint32_t c = cnt[b];
-          rs += c;
-          gs += (c + 31) >> 5;
-        }
-        uint32_t ri = rs, gi = gs;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-          const uint32_t r2 = __shfl_up_sync(0xffffffffu, ri, d), g2 = __shfl_up_sync(0xffffffffu, gi, d);
-          if (lane >= d) ri += r2, gi += g2;
-        }
-        uint32_t ro = ri - rs, go = gi - gs;
-        for (uint32_t b = b0; b < b1; ++b) {
-          const uint32_t c = cnt[b];
-          s_off[b] = ro;
-          s_cur[b] = ro;
-          const uint32_t ng = (c + 31) >> 5;
-          for (uint32_t j = 0; j < ng; ++j) s_grp[go + j] = (b << 8) | j;
-          ro += c;
-          go += ng;
-        }
-        if (lane == 31) s_ngrp = go, s_next[buf] = 0;
-      }
-    } else {
+    // 2. scans over the CTA: record offsets and 32-record groups per key, and
+    //    the (key, group) work list
+    {
       const uint32_t per = (nk + kThreads - 1) / kThreads;
       const uint32_t b0 = min(nk, tid * per), b1 = min(nk, b0 + per);
       uint32_t rs = 0, gs = 0;
       for (uint32_t b = b0; b < b1; ++b) {
-        const uint32_t c = cnt[b];
+        const uint32_t c = s_cnt[b];
         rs += c;
         gs += (c + 31) >> 5;
       }
@@ -313,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       uint32_t ro = ri - rs, go = gi - gs;
       for (int w = 0; w < warp; ++w) ro += s_wsum[0][w], go += s_wsum[1][w];
       for (uint32_t b = b0; b < b1; ++b) {
-        const uint32_t c = cnt[b];
+        const uint32_t c = s_cnt[b];
         s_off[b] = ro;
         s_cur[b] = ro;
         const uint32_t ng = (c + 31) >> 5;
@@ -321,40 +241,25 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         ro += c;
         go += ng;
       }
-      if (tid == kThreads - 1) s_ngrp = go, s_next[buf] = 0;
-    }
-    if (!small) {
-      __syncthreads();
-      for (int i = tid; i < m; i += kThreads) {
-        const uint32_t pos = atomicAdd(s_cur + s_key[i], 1u);
-        s_perm[pos] = (uint16_t)i;
-      }
+      if (tid == kThreads - 1) s_ngrp = go, s_next = 0;
     }
     __syncthreads();
-    if (!small) ngrp = s_ngrp;
+
+    // 3. scatter record indices into key order
+    for (int i = tid; i < m; i += kThreads) {
+      const uint32_t pos = atomicAdd(s_cur + s_key[i], 1u);
+      s_perm[pos] = (uint16_t)i;
+    }
+    __syncthreads();
 
     // 4. evaluate one 32-record group of one key per warp (warps claim groups
-    //    dynamically: groups of different shapes cost different amounts); the
+    //    dynamically: groups of different kernels cost different amounts); the
     //    code goes to shared memory, emitted in record order below
-    for (uint32_t g = warp_claim(&s_next[buf]); g < ngrp; g = warp_claim(&s_next[buf])) {
-      uint32_t key, start, rem;
-      if (small) {
-        key = __popc(__ballot_sync(0xffffffffu, ginc0 <= g)) + __popc(__ballot_sync(0xffffffffu, ginc1 <= g));
-        const int kl = (int)(key & 31);
-        const uint32_t gi0 = __shfl_sync(0xffffffffu, ginc0, kl), gi1 = __shfl_sync(0xffffffffu, ginc1, kl);
-        const uint32_t ca = __shfl_sync(0xffffffffu, c0, kl), cb = __shfl_sync(0xffffffffu, c1, kl);
-        const uint32_t oa = __shfl_sync(0xffffffffu, off0, kl), ob = __shfl_sync(0xffffffffu, off1, kl);
-        const uint32_t c = key < 32 ? ca : cb;
-        const uint32_t j = g - ((key < 32 ? gi0 : gi1) - ((c + 31) >> 5));
-        start = (key < 32 ? oa : ob) + 32u * j;
-        rem = c - 32u * j;
-      } else {
-        const uint32_t e = s_grp[g];
-        key = e >> 8;
-        const uint32_t j = e & 255u;
-        start = s_off[key] + 32u * j;
-        rem = cnt[key] - 32u * j;
-      }
+    const uint32_t ngrp = s_ngrp;
+    for (uint32_t g = warp_claim(&s_next); g < ngrp; g = warp_claim(&s_next)) {
+      const uint32_t e = s_grp[g];
+      const uint32_t key = e >> 8, j = e & 255u;
+      const uint32_t start = s_off[key] + 32u * j, rem = s_cnt[key] - 32u * j;
       if (key == P.wide_key) {  // K2: the whole warp on one record at a time
         for (uint32_t q = 0; q < min(rem, 32u); ++q) {
           const uint32_t wi = s_perm[start + q];
@@ -373,14 +278,9 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         const picker_rec_t r = rec_from_smem(hdr + 32 * li);
         const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
                            (uint64_t)r.nargs <= si.hi - r.arg_off;
-        uint8_t code;
-        // two instantiations: with a pointer the compiler can prove is shared
-        // memory (LDS), and with a global one (unstaged tiles)
-        code = Dispatch::eval(key, s_bin[li], s_kn[li], local, P, r,
-                              local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
-                                    : B.args + r.arg_off,
-                              B);
-        s_code[li] = code;
+        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                 : B.args + r.arg_off;
+        s_code[li] = Dispatch::eval(key, s_bin[li], s_kn[li], local, P, r, a, B);
       }
     }
     __syncthreads();
@@ -402,8 +302,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const unsigned same = __match_any_sync(0xffffffffu, hb);
       if (valid && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
     }
+    __syncthreads();  // s_code and the per-key arrays are reused by the next tile
   }
-  __syncthreads();
   if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid])
     atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
 }

@@ -183,11 +183,10 @@ constexpr int kArgCap = PICKER_TILE * PICKER_ARGS_PER_REC;  // staged argument s
 constexpr int kArgBufBytes = kArgCap * 8 + 16;              // + alignment slack
 constexpr size_t kMaxSmem = 227 * 1024;
 constexpr size_t bucket_smem_bytes_for(uint32_t nkeys, uint32_t tile, uint32_t args_per_rec) {
-  // 2 x (headers + args) staging buffers; s_kn (u32), s_key, s_bin, s_perm,
-  // s_rank (u16), s_code (u8) per record; s_cnt[2], s_off, s_cur (u32) per key;
-  // group table
-  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 13 +
-         (size_t)nkeys * 16 + ((size_t)tile / 32 + nkeys) * 4 + 128;
+  // 2 x (headers + args) staging buffers; s_kn (u32), s_key, s_bin, s_perm
+  // (u16), s_code (u8) per record; s_cnt, s_off, s_cur (u32) per key; group table
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 11 +
+         (size_t)nkeys * 12 + ((size_t)tile / 32 + nkeys) * 4 + 128;
 }
 constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
   return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC);

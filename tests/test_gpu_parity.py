@@ -192,3 +192,15 @@ def test_c4_many_pointers(pk, opt):
     flags, bits, counts = p.validate(rec, args)
     _check_outputs(flags, bits, counts, want)
     assert (want == 10).sum() > 0 and (want == 0).sum() > 0
+
+
+@pytest.mark.parametrize("opt", [dict(jit=0), dict(jit=1)], ids=str)
+def test_c2_trace_every_record(pk, opt):
+    """The C2 trace (547 kernels): with the specialised module off the
+    table-driven path groups by kernel (549 keys: k_validate_bucket); on, by
+    shape (35 keys: k_validate_pipe).  Every record against the oracle."""
+    from tracegen import workloads
+    s, rec, args, _ = workloads.make_c2()
+    p = _make(pk, s, **opt)
+    flags, bits, counts = p.validate(rec, args)
+    _check_outputs(flags, bits, counts, _oracle_codes(s, rec, args))
