@@ -238,6 +238,9 @@ int picker_kernel_info(picker_ctx_t* ctx, uint32_t* ids_out, uint8_t* path_out, 
 /* Options.  Tuning keys (semantics never depend on them; they take effect at
  * the next picker_load_summaries):
  *   "jit"          0 = table-driven kernels only, 1 = NVRTC-specialised (default 1)
+ *   "bucket"       table-driven kernels: 1 = group each tile by kernel, 0 = one
+ *                  thread per record, -1 = by the summary (default; grouped when
+ *                  COND kernels average more than 8 descriptors)
  *   "wide_pairs"   R*W pair count above which a kernel uses the wide path
  *   "force_path"   0 = automatic, 1 = generic, 2 = jit, 3 = wide
  *   "tile", "threads", "ctas", "args_per_rec"   specialised kernel geometry

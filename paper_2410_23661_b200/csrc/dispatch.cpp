@@ -13,7 +13,7 @@ cudaError_t launch_bucket_generic(const BucketParams& P, const DevBatch& B, uint
                                   uint8_t* flags, uint32_t* bits, unsigned long long* counts,
                                   int num_sms, cudaStream_t s);
 cudaError_t launch_stride(const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags, uint32_t* bits,
-                          unsigned long long* counts, int num_sms, cudaStream_t s);
+                          unsigned long long* counts, bool bucket, int num_sms, cudaStream_t s);
 cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n,
                        uint8_t* flags, uint32_t* bits, unsigned long long* counts, int num_sms,
                        cudaStream_t s);
@@ -59,7 +59,7 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             int* launches) {
   if (n == 0) return cudaSuccess;
   *launches += 1;
-  if (opt.stride) return launch_stride(P, b, n, flags, bits, counts, num_sms, s);
+  if (opt.stride) return launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);
   if (jit) return launch_jit(jit, P, b, n, flags, bits, counts, num_sms, s);
   if (opt.bucket && bucket_smem_bytes(P.nbins + 2) <= kMaxSmem)
     return launch_bucket_generic(P, b, n, flags, bits, counts, num_sms, s);

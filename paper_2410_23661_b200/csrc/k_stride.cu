@@ -54,14 +54,14 @@ __global__ void __launch_bounds__(256) k_validate_stride_flat(Tables T, DevBatch
 }
 
 cudaError_t launch_stride(const BucketParams& P0, const DevBatch& B, uint64_t n, uint8_t* flags, uint32_t* bits,
-                          unsigned long long* counts, int num_sms, cudaStream_t s) {
+                          unsigned long long* counts, bool bucket, int num_sms, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
   BucketParams P = P0;  // key = bin (table path), no K2 interception
   P.nkeys = P.nbins + 2;
   P.wide_key = 0xFFFFFFFFu;
   const bool pipe = P.nkeys <= kPipeKeys;
   const size_t smem = pipe ? pipe_smem_bytes_for(kTile, PICKER_ARGS_PER_REC) : bucket_smem_bytes(P.nkeys);
-  if (smem <= kMaxSmem) {
+  if (bucket && smem <= kMaxSmem) {
     static size_t configured[2] = {0, 0};
     if (smem > configured[pipe]) {
       cudaError_t e = cudaFuncSetAttribute(pipe ? k_validate_pipe<StrideDispatch> : k_validate_bucket<StrideDispatch>,

@@ -16,7 +16,11 @@ struct IrKernel;
 
 struct Options {
   bool jit = true;     // NVRTC-specialised functions for every COND kernel
-  bool bucket = true;  // group each tile's records by kernel before evaluating
+  // table-driven paths: group each tile's records by kernel before evaluating
+  // (1), one thread per record (0), or -1: by the summary -- grouped when the
+  // mean descriptor count of the COND kernels exceeds 8 (measured: C2/C3
+  // kernels are faster ungrouped, 3.7 vs 1.6 G inst/s; C4 grouped, 0.14 vs 0.07)
+  int bucket = -1;
   int force_path = 0;  // 0 auto, 1 generic (table-driven), 2 jit, 3 wide, for every COND kernel
   int64_t wide_pairs = 1 << 20;  // read x write pairs above which a kernel takes the wide path
   // geometry of the specialised kernel (tuning; k_bucket.cuh)

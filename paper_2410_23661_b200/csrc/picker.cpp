@@ -31,6 +31,7 @@ struct picker_ctx {
   unsigned long long* dev_counts = nullptr;
   cudaStream_t aux = nullptr;
   int last_launches = 0;
+  bool bucket_auto = false;  // table-driven grouping when opt.bucket = -1 (launch.hpp)
 };
 
 static std::string g_create_err;
@@ -124,7 +125,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   if (!c || !key) return PICKER_EINVAL;
   std::string k(key);
   if (k == "jit") c->opt.jit = v != 0;
-  else if (k == "bucket") c->opt.bucket = v != 0;
+  else if (k == "bucket") c->opt.bucket = v < 0 ? -1 : (int)(v != 0);
   else if (k == "force_path") c->opt.force_path = (int)v;
   else if (k == "wide_pairs") c->opt.wide_pairs = v;
   else if (k == "tile") c->opt.tile = (int)v;
@@ -204,6 +205,12 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
   c->P.wide_key = c->P.nbins + 1;  // table-driven grouping (the JIT module uses its own)
+  {
+    size_t nd = 0, nc = 0;
+    for (auto& k : ks)
+      if (k.path != PATH_SHORTCUT) nd += k.desc.size(), ++nc;
+    c->bucket_auto = nc && nd > 8 * nc;
+  }
   c->ir = std::move(ks);
   c->ht = std::move(ht);
   c->loaded = true;
@@ -307,7 +314,9 @@ int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, 
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
-  cudaError_t e = launch_validate(c->P, c->jit, c->opt, db, n, flags, bits,
+  Options o = c->opt;
+  if (o.bucket < 0) o.bucket = c->bucket_auto;
+  cudaError_t e = launch_validate(c->P, c->jit, o, db, n, flags, bits,
                                   (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
   if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
   return PICKER_OK;
@@ -393,7 +402,9 @@ int picker_validate_batch_host(picker_ctx_t* c, const picker_batch_t* b, uint64_
     DevBatch db = packed ? DevBatch{d_rec, d_args - lo, lo, hi}
                          : DevBatch{d_rec, whole_args, 0, b->args_len};
     int launches = 0;
-    e = launch_validate(c->P, c->jit, c->opt, db, m, d_flags, bits ? d_bits : nullptr,
+    Options o = c->opt;
+    if (o.bucket < 0) o.bucket = c->bucket_auto;
+    e = launch_validate(c->P, c->jit, o, db, m, d_flags, bits ? d_bits : nullptr,
                         c->dev_counts, c->num_sms, ss, &launches);
     if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
     c->last_launches += launches;
