@@ -59,7 +59,10 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             int* launches) {
   if (n == 0) return cudaSuccess;
   *launches += 1;
-  if (opt.stride) return launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);
+  // stride mode: the specialised module if it was built stride-aware (option
+  // set before picker_load_summaries), else the table-driven evaluator
+  if (opt.stride && !jit_is_stride(jit)) return launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);
+  if (!opt.stride && jit_is_stride(jit)) jit = nullptr;  // stride-aware module, plain verdicts wanted
   if (jit) return launch_jit(jit, P, b, n, flags, bits, counts, num_sms, s);
   if (opt.bucket && bucket_smem_bytes(P.nbins + 2) <= kMaxSmem)
     return launch_bucket_generic(P, b, n, flags, bits, counts, num_sms, s);

@@ -19,7 +19,7 @@
 
 namespace picker {
 
-static __device__ __forceinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
+static __device__ __noinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
   if (a == 0) return b;
   if (b == 0) return a;
   const int sh = __ffsll((long long)(a | b)) - 1;
@@ -73,7 +73,7 @@ static __device__ uint64_t desc_stride(const Tables& T, const DKernel& K, const 
 }
 
 // can the two congruence classes share a byte (intervals already intersect)?
-static __device__ __forceinline__ bool may_collide(int64_t lb_r, uint64_t g_r, uint32_t w_r, int64_t lb_w,
+static __device__ __noinline__ bool may_collide(int64_t lb_r, uint64_t g_r, uint32_t w_r, int64_t lb_w,
                                                    uint64_t g_w, uint32_t w_w) {
   const uint64_t G = gcd64(g_r, g_w);
   if (G == 0) return true;  // two single addresses: the interval test is exact

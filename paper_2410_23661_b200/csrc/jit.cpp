@@ -54,6 +54,7 @@ struct JitModule {
   uint32_t nkeys = 0;
   int nshapes = 0;
   int tile = 0, threads = 0, ctas = 0;
+  bool stride = false;  // built with stride-aware shapes (row f4)
 };
 
 namespace {
@@ -108,7 +109,10 @@ struct Gen {
   }
 };
 
-std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
+// stride: the stride-aware variant (row f4, eval_stride.cuh): a read/write pair
+// whose intervals intersect is an overlap only if may_collide() holds for the
+// two descriptors' congruence classes (computed lazily, on intersection).
+std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
   Gen g(K);
   std::ostringstream& s = g.s;
   const int np = (int)k.param_names.size();
@@ -235,6 +239,29 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
     }
     if (d.width > 1) ub = "add64(" + ub + ", " + g.k((int64_t)d.width - 1) + ")";
     s << ind << "const int64_t lb" << di << " = " << lb << ", ub" << di << " = " << ub << ";\n";
+    if (stride) {  // g = gcd of |sum of coefficients| of the varying (variable, divisor) groups
+      std::vector<std::pair<std::pair<int, uint32_t>, std::string>> groups;
+      for (const IrTerm& t : d.terms) {
+        if (t.var < 0) continue;
+        const std::pair<int, uint32_t> key{t.var, (uint32_t)t.div};
+        const std::string cc = g.prod(t.c);
+        auto it = std::find_if(groups.begin(), groups.end(), [&](auto& e) { return e.first == key; });
+        if (it == groups.end()) groups.push_back({key, cc});
+        else it->second = "add64(" + it->second + ", " + cc + ")";
+      }
+      s << ind << "auto G" << di << " = [&]() -> uint64_t {\n" << ind << "  uint64_t gg = 0;\n";
+      for (auto& e : groups) {
+        const int x = sids[di][e.first.first];
+        const uint32_t dv = e.first.second;
+        const std::string L = "vl" + std::to_string(x), H = "vh" + std::to_string(x);
+        const std::string vary = dv == 1 ? L + " != " + H
+                                         : "floordiv64(" + L + ", " + std::to_string(dv) + "u) != floordiv64(" + H +
+                                               ", " + std::to_string(dv) + "u)";
+        s << ind << "  if (" << vary << ") gg = gcd64(gg, uabs64(" << e.second << "));\n";
+      }
+      s << ind << "  return gg;\n" << ind << "};\n";
+      s << ind << "const uint32_t W" << di << " = (uint32_t)" << g.k((int64_t)d.width) << ";\n";
+    }
   };
   std::vector<int> kept, opq_r, opq_w;
   s << "  bool act_r = false, act_w = false, ov = false;\n";
@@ -257,9 +284,12 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K) {
     s << "    act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
     extent(di, "    ");
     std::string hit = "false";
-    for (int j : kept)
-      hit += " | (on" + std::to_string(j) + " & (lb" + std::to_string(di) + " <= ub" + std::to_string(j) +
-             ") & (lb" + std::to_string(j) + " <= ub" + std::to_string(di) + "))";
+    for (int j : kept) {
+      const std::string I = std::to_string(di), J = std::to_string(j);
+      std::string t = "(on" + J + " & (lb" + I + " <= ub" + J + ") & (lb" + J + " <= ub" + I + "))";
+      if (stride) t = "(" + t + " && may_collide(lb" + I + ", G" + I + "(), W" + I + ", lb" + J + ", G" + J + "(), W" + J + "))";
+      hit += " | " + t;
+    }
     s << "    ov |= on" << di << " & (" << hit << ");\n  }\n";
   }
   auto any = [&](const std::vector<int>& a) {
@@ -345,14 +375,15 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
   JitPlan P;
   std::ostringstream src;
   src << "// generated by picker jit.cpp\n"
          "typedef signed char int8_t; typedef short int16_t; typedef int int32_t; typedef long long int64_t;\n"
          "typedef unsigned char uint8_t; typedef unsigned short uint16_t; typedef unsigned int uint32_t;\n"
          "typedef unsigned long long uint64_t; typedef unsigned long size_t; typedef unsigned long uintptr_t;\n"
-         "#include \"eval_generic.cuh\"\n#include \"k_bucket.cuh\"\nnamespace picker {\n";
+         "#include \"eval_generic.cuh\"\n#include \"eval_stride.cuh\"\n#include \"k_bucket.cuh\"\n"
+         "namespace picker {\n";
   // pass 1: body text with every constant as a load, grouped into shapes
   std::map<std::string, uint32_t> shape_id;
   std::vector<std::string> shapes;
@@ -361,7 +392,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
   std::vector<int> shape_of(ks.size(), -1);
   for (size_t i = 0; i < ks.size(); ++i) {
     if (ks[i].path != PATH_JIT) continue;
-    std::string body = gen_body(ks[i], kconst[i]);
+    std::string body = gen_body(ks[i], kconst[i], stride);
     auto it = shape_id.find(body);
     if (it == shape_id.end()) {
       it = shape_id.emplace(body, (uint32_t)shapes.size()).first;
@@ -426,7 +457,9 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
          "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
          "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
-         "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n"
+      << (stride ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
+                 : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
+      <<
          "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
          "      return V_ERR_ARITY;\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
@@ -445,7 +478,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks) {
 }
 
 void order_by_shape(std::vector<IrKernel>& ks) {
-  JitPlan P = jit_plan(ks);
+  JitPlan P = jit_plan(ks, false);
   std::vector<size_t> idx(ks.size());
   for (size_t i = 0; i < idx.size(); ++i) idx[i] = i;
   std::stable_sort(idx.begin(), idx.end(), [&](size_t a, size_t b) { return P.meta[a].shape < P.meta[b].shape; });
@@ -511,7 +544,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks);
+  JitPlan plan = jit_plan(ks, opt.stride);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeys && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
     return nullptr;
@@ -520,6 +553,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   if (!jit_compile(plan, opt, cubin, lowered, true, err)) return nullptr;
   JitModule* m = new JitModule();
   m->nshapes = plan.nshapes;
+  m->stride = opt.stride;
   m->tile = opt.tile;
   m->threads = opt.threads;
   m->ctas = opt.ctas;
@@ -582,6 +616,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   return m;
 }
 
+bool jit_is_stride(const JitModule* m) { return m && m->stride; }
+
 void jit_destroy(JitModule* m) {
   if (!m) return;
   if (m->lib) cudaLibraryUnload(m->lib);
@@ -600,7 +636,7 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
   P.kb_of = m->d_kb;
   P.kb_unknown = m->kb_unknown;
   P.nkeys = m->nkeys;
-  P.wide_key = SHAPE_WIDE;
+  P.wide_key = m->stride ? 0xFFFFFFFFu : SHAPE_WIDE;  // stride mode: wide kernels through eval_stride
   const uint64_t ntiles = (n + m->tile - 1) / m->tile;
   const uint64_t cap = (uint64_t)num_sms * m->ctas;
   const uint64_t grid = ntiles < cap ? ntiles : cap;

@@ -43,7 +43,8 @@ struct JitPlan {
   std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
   int nshapes = 0;
 };
-JitPlan jit_plan(const std::vector<IrKernel>& ks);
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride);
+bool jit_is_stride(const JitModule* m);
 // Fills in the automatic geometry (tile = 0) from the summaries.
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
 // Stable-sort kernels by generated shape so neighbouring bins share code.

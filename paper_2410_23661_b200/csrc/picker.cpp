@@ -259,7 +259,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     Options opt;
     select_paths(ks, opt);
     order_by_shape(ks);
-    JitPlan plan = jit_plan(ks);
+    JitPlan plan = jit_plan(ks, false);
     std::string cubin, lowered, err;
     if (!jit_compile(plan, resolve_geometry(ks, opt), cubin, lowered, false, err)) {
       put(msg, msg_len, err);

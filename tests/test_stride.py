@@ -139,9 +139,13 @@ def test_stride_recovers_ro_on_synthetic_traces():
 
 # ---- GPU parity of the library's stride mode (picker_set_option "stride") -----
 
-def _gpu_codes(summary, rec, args, **opt):
+def _gpu_codes(summary, rec, args, at_load=False, **opt):
+    """at_load: option set before picker_load_summaries (the specialised module
+    is generated stride-aware); otherwise after it (table-driven stride path)."""
     import paper_2410_23661_b200 as pk
     p = pk.Picker(0, **opt)
+    if at_load:
+        p.set_option("stride", 1)
     p.load(summary)
     p.set_option("stride", 1)
     flags, bits, counts = p.validate(rec, args)
@@ -166,7 +170,8 @@ def _check(got, want):
     assert np.array_equal(counts, exp)
 
 
-STRIDE_OPTS = [dict(jit=0), dict(jit=1), dict(jit=1, wide_pairs=4)]
+STRIDE_OPTS = [dict(jit=0), dict(jit=1), dict(jit=1, wide_pairs=4), dict(jit=1, at_load=True),
+               dict(jit=1, wide_pairs=4, at_load=True)]
 
 
 @pytest.mark.gpu
@@ -185,18 +190,36 @@ def test_gpu_stride_paper_examples(opt):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("at_load", [False, True])
 @pytest.mark.parametrize("seed", [61, 62, 63])
-def test_gpu_stride_random(seed):
+def test_gpu_stride_random(seed, at_load):
     s = random_summary(seed, n_kernels=40)
     rec, args = random_records(seed + 1000, s, 3000, max_threads=256, max_grid=64)
-    _check(_gpu_codes(s, rec, args), _want(s, rec, args))
+    _check(_gpu_codes(s, rec, args, at_load=at_load), _want(s, rec, args))
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("at_load", [False, True])
 @pytest.mark.parametrize("which", ["c2", "c3"])
-def test_gpu_stride_workloads(which):
-    """The C2 trace (547 kernels: the bucketed kernel) and the C3 base (64
-    kernels), every record against the oracle's stride variant."""
+def test_gpu_stride_workloads(which, at_load):
+    """The C2 trace (547 kernels) and the C3 base (64 kernels), every record
+    against the oracle's stride variant; table-driven and specialised."""
     from tracegen import workloads
     s, rec, args, _ = workloads.make_c2() if which == "c2" else workloads.make_c3(n=1 << 12, n_kernels=64)
-    _check(_gpu_codes(s, rec, args), _want(s, rec, args))
+    _check(_gpu_codes(s, rec, args, at_load=at_load), _want(s, rec, args))
+
+
+@pytest.mark.gpu
+def test_gpu_stride_module_plain_verdicts():
+    """A module generated stride-aware still answers plain (range-model)
+    verdicts when the option is switched off after loading."""
+    import paper_2410_23661_b200 as pk
+    s = random_summary(64, n_kernels=30)
+    rec, args = random_records(1064, s, 2000, max_threads=256, max_grid=64)
+    p = pk.Picker(0)
+    p.set_option("stride", 1)
+    p.load(s)
+    p.set_option("stride", 0)
+    flags, _, _ = p.validate(rec, args)
+    want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
+    assert np.array_equal(flags.cpu().numpy(), want)
