@@ -70,27 +70,6 @@ static __device__ void desc_extent(const Tables& T, const DKernel& K, const DDes
   ub = add64(ub, (int64_t)D.width - 1);
 }
 
-// The checks that precede any address (kernel id, arity, class, launch limits,
-// preconditions, global condition).  Returns the verdict, or kContinue.
-constexpr uint32_t kContinue = 0x100;
-static __device__ __forceinline__ uint32_t record_prefix(const Tables& T, const picker_rec_t& r,
-                                                         uint64_t alo, uint64_t ahi, DKernel& K,
-                                                         const RecVals& X) {
-  const uint32_t kid = r.kernel_id;
-  if (kid >= T.nkernel_slots) return V_ERR_KERNEL;
-  K = T.kernels[kid];
-  if (K.shortcut == V_ERR_KERNEL) return V_ERR_KERNEL;
-  if (!args_in_range(r, K.nparams, alo, ahi)) return V_ERR_ARITY;
-  if (K.shortcut) return K.shortcut;
-  if (!launch_limits_ok(X)) return V_NI_PRECOND;
-  for (int c = 0; c < K.npre + K.nglob; ++c) {
-    const DCheck ch = T.checks[K.check + c];
-    const int64_t v = X.get(ch.op);
-    if (v < ch.lo || v > ch.hi) return c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
-  }
-  return kContinue;
-}
-
 // ---------------------------------------------------------------------------
 // K2: one warp evaluates one instance with many read/write sites (SURVEY §2.5:
 // cuDNN-like kernels with 16+ pointer arguments).  Lanes compute descriptor
@@ -184,22 +163,86 @@ static __device__ __forceinline__ bool sweep64(const Ext& e0, const Ext& e1, int
   return __any_sync(0xffffffffu, hit);
 }
 
+// Activity and (non-opaque) extent of one descriptor, each variable's bounds
+// evaluated once (desc_active + desc_extent re-evaluate them per term).
+constexpr int kWideVars = 8;
+static __device__ bool desc_active_extent(const Tables& T, const DKernel& K, const DDesc& D, const RecVals& X,
+                                          int64_t& lb, int64_t& ub) {
+  for (int g = 0; g < D.nguard; ++g) {
+    const DGuard G = T.guards[D.guard + g];
+    if (!cmp64(X.get(G.a), G.cmp, G.b == OPD_NONE ? G.bconst : X.get(G.b))) return false;
+  }
+  if (D.nvar > kWideVars) {
+    if (!desc_active(T, K, D, X)) return false;
+    if (!D.opaque) desc_extent(T, K, D, X, lb, ub);
+    return true;
+  }
+  int64_t vlo[kWideVars], vhi[kWideVars];
+  for (int v = 0; v < D.nvar; ++v) {
+    slot_bounds(T, K, X, T.varlist[D.var + v], vlo[v], vhi[v]);
+    if (vlo[v] > vhi[v]) return false;
+  }
+  if (D.opaque) return true;
+  lb = D.base == OPD_NONE ? 0 : X.get(D.base);
+  ub = lb;
+  for (int t = 0; t < D.nterm; ++t) {
+    const DTerm tm = T.terms[D.term + t];
+    const int64_t c = prod_val(T, K, X, tm.prod);
+    if (tm.var == kNone16) {
+      lb = add64(lb, c), ub = add64(ub, c);
+      continue;
+    }
+    const int lv = T.term_lvar[D.term + t];
+    const int64_t x0 = mul64(c, floordiv64(vlo[lv], tm.div)), x1 = mul64(c, floordiv64(vhi[lv], tm.div));
+    lb = add64(lb, min64(x0, x1));
+    ub = add64(ub, max64(x0, x1));
+  }
+  ub = add64(ub, (int64_t)D.width - 1);
+  return true;
+}
+
 // Verdict of one record, computed by the whole warp (all lanes return it).
 static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r, const int64_t* a,
                                          uint64_t alo, uint64_t ahi, int lane) {
-  DKernel K;
-  const RecVals X(r, a, T.kernels[r.kernel_id < T.nkernel_slots ? r.kernel_id : 0].i32mask);
-  const uint32_t pre = record_prefix(T, r, alo, ahi, K, X);
-  if (pre != kContinue) return (uint8_t)pre;
+  // prefix (Fig. 3 order); the preconditions / global condition are split over
+  // the lanes: the first failing check in order decides (pre before glob)
+  const uint32_t kid = r.kernel_id;
+  if (kid >= T.nkernel_slots) return V_ERR_KERNEL;
+  const DKernel K = T.kernels[kid];
+  if (K.shortcut == V_ERR_KERNEL) return V_ERR_KERNEL;
+  if (!args_in_range(r, K.nparams, alo, ahi)) return V_ERR_ARITY;
+  if (K.shortcut) return K.shortcut;
+  const RecVals X(r, a, K.i32mask);
+  if (!launch_limits_ok(X)) return V_NI_PRECOND;
+  int first_fail = 0x7FFFFFFF;
+  for (int c = lane; c < K.npre + K.nglob; c += 32) {
+    const DCheck ch = T.checks[K.check + c];
+    const int64_t v = X.get(ch.op);
+    if (v < ch.lo || v > ch.hi) {
+      first_fail = c;
+      break;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) first_fail = min(first_fail, __shfl_xor_sync(0xffffffffu, first_fail, d));
+  if (first_fail != 0x7FFFFFFF) return first_fail < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
   // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags, extents
   bool act_r = false, act_w = false, opq_r = false, opq_w = false;
   int nact = 0;
+  Ext e[2];
+  e[0].kind = e[1].kind = 2;
+  e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
   for (int d = lane; d < K.ndesc; d += 32) {
     const DDesc D = T.descs[K.desc + d];
-    if (!desc_active(T, K, D, X)) continue;
+    int64_t lb = 0, ub = 0;
+    if (!desc_active_extent(T, K, D, X, lb, ub)) continue;
     (D.kind == KIND_R ? act_r : act_w) = true;
-    if (D.opaque) (D.kind == KIND_R ? opq_r : opq_w) = true;
-    else ++nact;
+    if (D.opaque) {
+      (D.kind == KIND_R ? opq_r : opq_w) = true;
+      continue;
+    }
+    if (nact < 2) e[nact].lb = lb, e[nact].ub = ub, e[nact].kind = D.kind == KIND_R ? 0 : 1;
+    ++nact;
   }
   act_r = __any_sync(0xffffffffu, act_r);
   act_w = __any_sync(0xffffffffu, act_w);
@@ -207,18 +250,7 @@ static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r,
   opq_w = __any_sync(0xffffffffu, opq_w);
   if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
   if (!__any_sync(0xffffffffu, nact > 2)) {
-    // <= 64 active extents in total (<= 2 per lane): sort + sweep
-    Ext e[2];
-    int c = 0;
-    e[0].kind = e[1].kind = 2;
-    e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
-    for (int d = lane; d < K.ndesc; d += 32) {
-      const DDesc D = T.descs[K.desc + d];
-      if (D.opaque || !desc_active(T, K, D, X)) continue;
-      desc_extent(T, K, D, X, e[c].lb, e[c].ub);
-      e[c].kind = D.kind == KIND_R ? 0 : 1;
-      ++c;
-    }
+    // <= 64 active extents in total (<= 2 per lane, kept above): sort + sweep;
     // element index of e[0] is lane, of e[1] is 32 + lane
     warp_sort64(e[0], e[1], lane);
     return sweep64(e[0], e[1], lane) ? V_NI_OVERLAP : V_IDEM_CHECKED;
