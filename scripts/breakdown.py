@@ -94,6 +94,20 @@ def main():
     parity = {"full": int((res["full"]["codes"] != want_f).sum()),
               "base_r": int((res["base_r"]["codes"] != want_u).sum()),
               "base_sample256": int((res["base"]["codes"][idx] != want_e).sum())}
+    # range-overestimation conservatism, measured by the
+    # exact verifier: interval NI (10) where the exact byte sets are disjoint (0);
+    # and how many of those the stride-aware variant (row f4) recovers
+    full_c, base_c = res["full"]["codes"], res["base"]["codes"]
+    st = pk.Picker(0)
+    st.set_option("stride", 1)
+    st.load(s)
+    stride_c, _, _ = st.validate(rec, args)
+    stride_c = stride_c.cpu().numpy()
+    ro = (full_c == 10) & (base_c == 0)
+    out["ro_conservatism"] = {"records": int(len(rec)), "interval_ni": int((full_c == 10).sum()),
+                              "exact_ni": int((base_c == 10).sum()), "interval_ni_exact_i": int(ro.sum()),
+                              "recovered_by_stride": int((ro & (stride_c == 0)).sum()),
+                              "stride_unsound": int(((base_c == 10) & (stride_c == 0)).sum())}
     for v in res.values():
         c = v.pop("codes")
         v["verdicts"] = {int(k): int(x) for k, x in zip(*np.unique(c, return_counts=True))}
