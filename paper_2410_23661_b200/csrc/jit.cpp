@@ -47,7 +47,6 @@ struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   size_t smem = 0;
-  JitMeta* d_meta = nullptr;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
   uint32_t kb_unknown = 0;
@@ -559,7 +558,6 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->ctas = opt.ctas;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, lowered.c_str());
-  if (e == cudaSuccess) e = cudaMalloc(&m->d_meta, plan.meta.size() * sizeof(JitMeta));
   if (e == cudaSuccess) e = cudaMalloc(&m->d_consts, plan.consts.size() * sizeof(int64_t));
   // kernel id -> (bin | shape << 16); bins are positions in `ks`
   uint32_t maxid = 0;
@@ -579,8 +577,6 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   if (e == cudaSuccess) e = cudaMalloc(&m->d_kb, kb.size() * sizeof(KbEntry));
   if (e == cudaSuccess)
     e = cudaMemcpy(m->d_kb, kb.data(), kb.size() * sizeof(KbEntry), cudaMemcpyHostToDevice);
-  if (e == cudaSuccess)
-    e = cudaMemcpy(m->d_meta, plan.meta.data(), plan.meta.size() * sizeof(JitMeta), cudaMemcpyHostToDevice);
   if (e == cudaSuccess)
     e = cudaMemcpy(m->d_consts, plan.consts.data(), plan.consts.size() * sizeof(int64_t),
                    cudaMemcpyHostToDevice);
@@ -621,7 +617,6 @@ bool jit_is_stride(const JitModule* m) { return m && m->stride; }
 void jit_destroy(JitModule* m) {
   if (!m) return;
   if (m->lib) cudaLibraryUnload(m->lib);
-  if (m->d_meta) cudaFree(m->d_meta);
   if (m->d_consts) cudaFree(m->d_consts);
   if (m->d_kb) cudaFree(m->d_kb);
   delete m;
@@ -631,7 +626,6 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
                        uint8_t* flags, uint32_t* bits, unsigned long long* counts, int num_sms,
                        cudaStream_t s) {
   BucketParams P = P0;
-  P.jit_meta = m->d_meta;
   P.jit_consts = m->d_consts;
   P.kb_of = m->d_kb;
   P.kb_unknown = m->kb_unknown;

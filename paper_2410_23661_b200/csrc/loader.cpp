@@ -308,6 +308,8 @@ std::vector<IrKernel> parse_summaries(const char* text, size_t len) {
     for (auto& kj : root.at("kernels").arr()) {
       out.push_back(parse_kernel(kj));
       if (!ids.insert(out.back().id).second) ferr("duplicate kernel id");
+      // bins are 16-bit (KbEntry.kb = bin | key << 16); bin 65535 is reserved
+      if (out.size() >= 0xFFFF) ferr("more than 65534 kernels in one summary");
     }
   } catch (const JsonError& e) {
     ferr(e.what());
@@ -468,8 +470,6 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
   unknown.shortcut = V_ERR_KERNEL;
   unknown.path = PATH_SHORTCUT;
   t.kernels.assign(ks.empty() ? 1 : maxid + 1, unknown);
-  t.bin_of.assign(t.kernels.size(), kNone16);
-  for (size_t i = 0; i < ks.size() && i < kNone16; ++i) t.bin_of[ks[i].id] = (uint16_t)i;
   const uint32_t nb = (uint32_t)ks.size();
   t.kb_unknown = nb | (nb << 16);
   t.kb.assign(t.kernels.size(), KbEntry{t.kb_unknown, 0});

@@ -97,7 +97,6 @@ struct HostTables {
   std::vector<uint16_t> varlist;
   std::vector<DVarDef> vardef;
   std::vector<uint8_t> term_lvar;
-  std::vector<uint16_t> bin_of;  // kernel id -> index in the summary (kNone16: not loaded)
   std::vector<KbEntry> kb;       // kernel id -> {bin | bin << 16, 0} (table-driven grouping key)
   uint32_t kb_unknown = 0;
 };

@@ -161,7 +161,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
          o_p = append_bytes(blob, ht.prods), o_b = append_bytes(blob, ht.bexprs),
          o_v = append_bytes(blob, ht.vars), o_t = append_bytes(blob, ht.terms),
          o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
-         o_l = append_bytes(blob, ht.varlist), o_m = append_bytes(blob, ht.bin_of),
+         o_l = append_bytes(blob, ht.varlist),
          o_kb = append_bytes(blob, ht.kb), o_vd = append_bytes(blob, ht.vardef),
          o_tl = append_bytes(blob, ht.term_lvar);
   blob.resize(blob.size() + 256);
@@ -198,7 +198,6 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.T.guards = (const DGuard*)(b + o_g);
   c->P.T.descs = (const DDesc*)(b + o_d);
   c->P.T.varlist = (const uint16_t*)(b + o_l);
-  c->P.bin_of = (const uint16_t*)(b + o_m);
   c->P.kb_of = (const KbEntry*)(b + o_kb);
   c->P.T.vardef = (const DVarDef*)(b + o_vd);
   c->P.T.term_lvar = (const uint8_t*)(b + o_tl);

@@ -133,8 +133,8 @@ struct DevBatch {
   uint64_t args_lo, args_hi;
 };
 
-// Per-bin entry of the specialised module (jit.cpp): which generated function
-// evaluates the bin and where its constants start.
+// Per-bin entry of the specialised module's plan (jit.cpp, host side): the
+// bin's grouping key (shape), where its constants start, its arity.
 struct JitMeta {
   uint32_t shape, koff, nparams, pad;
 };
@@ -149,12 +149,10 @@ struct KbEntry {
 // Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
 struct BucketParams {
   Tables T;
-  const uint16_t* bin_of;  // [T.nkernel_slots]: dense bin of each loaded kernel id, kNone16 if none
   uint32_t nbins;          // bins 0..nbins-1 are kernels; bin nbins collects unknown ids
   uint32_t nkeys;          // grouping keys 0..nkeys-1
   const struct KbEntry* kb_of;  // [T.nkernel_slots]: per kernel id, see KbEntry
   uint32_t kb_unknown;          // kb of an id that is not loaded
-  const JitMeta* jit_meta;     // [nbins + 1] (specialised module only)
   const int64_t* jit_consts;   // per-kernel constants (specialised module only)
   uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
 };

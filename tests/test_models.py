@@ -139,3 +139,21 @@ def test_gpu_models_c2():
     got = p.consumer_models(rec, args, flags, ctx)
     want = O.oracle_models(s, rec, args, flags.cpu().numpy(), ctx)
     assert got == want
+
+
+@pytest.mark.gpu
+def test_gpu_models_errors():
+    """Call errors are statuses, not crashes: save bandwidth 0 -> EINVAL."""
+    import paper_2410_23661_b200 as pk
+    s = golden.golden_summary()
+    b = RecordBuilder()
+    b.add(0, [4096, 8192, 12288], (4, 1, 1), (128, 1, 1))
+    rec, args = b.build()
+    p = pk.Picker(0)
+    p.load(s)
+    flags, _, _ = p.validate(rec, args)
+    with pytest.raises(pk.PickerError) as e:
+        p.consumer_models(rec, args, flags, None, save_bytes_per_us=0)
+    assert e.value.status == -1
+    m = p.consumer_models(rec, args, flags, None)
+    assert m["n"] == 1 and m["preempt_ns_without"] == 0 and m["ckpt_bytes_all"] == 2 * 4 * 4 * 128
