@@ -337,7 +337,6 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + 2 * kArgBufBytes);
   uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);
   __shared__ uint32_t s_cnt[2][kPipeKeys];
-  __shared__ uint32_t s_grp[kTile / 32 + kPipeKeys];  // group -> start | rem << 13 | key << 19
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   __shared__ uint32_t s_next[2];
   __shared__ __align__(8) uint64_t s_bar[2];
@@ -404,7 +403,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       if (valid && lane == leader) b = atomicAdd(&s_cnt[buf][key], (uint32_t)__popc(peers));
       b = __shfl_sync(0xffffffffu, b, leader);
       kr[q] = valid ? key | (b + __popc(peers & lt_mask)) << 8 : 0xFFu;
-      rb[q] = (uint32_t)i | (kb & 0xFFFFu) << 16;
+      rb[q] = (uint32_t)i | key << 16;
       kn[q] = e;
     }
   };
@@ -437,33 +436,23 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // t-1, next used after B_b of t
     if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
     if (tid == 0) s_next[buf ^ 1] = kWarps;
-    // scan (every warp, registers): lane l holds keys l and 32 + l as
-    // count | groups << 16, inclusive
+    // scan (every warp, registers): lane l holds the counts of keys l and
+    // 32 + l; inclusive, then exclusive offsets of each key's sorted records
     const uint32_t c0 = s_cnt[buf][lane], c1 = s_cnt[buf][lane + 32];
-    uint32_t v0 = c0 | ((c0 + 31) >> 5) << 16, v1 = c1 | ((c1 + 31) >> 5) << 16;
+    uint32_t v0 = c0, v1 = c1;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t a0 = __shfl_up_sync(0xffffffffu, v0, d), a1 = __shfl_up_sync(0xffffffffu, v1, d);
       if (lane >= d) v0 += a0, v1 += a1;
     }
     v1 += __shfl_sync(0xffffffffu, v0, 31);
-    const uint32_t off0 = (v0 & 0xFFFFu) - c0, off1 = (v1 & 0xFFFFu) - c1;
-    const uint32_t ginc0 = v0 >> 16, ginc1 = v1 >> 16;
-    const uint32_t ngrp = __shfl_sync(0xffffffffu, ginc1, 31);
+    const uint32_t off0 = v0 - c0, off1 = v1 - c1;
     // scatter
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const uint32_t key = kr[q] & 0xFFu;
       const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31), o1 = __shfl_sync(0xffffffffu, off1, key & 31);
       if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
-    }
-    // group table: warp w writes groups j = w, w + kWarps, ... of every key
-    {
-      const uint32_t gs0 = ginc0 - ((c0 + 31) >> 5), gs1 = ginc1 - ((c1 + 31) >> 5);
-      for (uint32_t j = warp; 32 * j < c0; j += kWarps)
-        s_grp[gs0 + j] = (off0 + 32 * j) | min(32u, c0 - 32 * j) << 13 | (uint32_t)lane << 19;
-      for (uint32_t j = warp; 32 * j < c1; j += kWarps)
-        s_grp[gs1 + j] = (off1 + 32 * j) | min(32u, c1 - 32 * j) << 13 | (uint32_t)(lane + 32) << 19;
     }
     __syncthreads();  // B_b
     // the previous tile's buffers are free: start the copy of the next tile
@@ -477,40 +466,52 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const unsigned char* hdr = smem + buf * kHdrBytes;
     const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
     const StageInfo si = s_info[buf];
-    // (claiming one group ahead was measured slower: a warp holding a claimed
-    // group lengthens the tail, C4 1.04 -> 0.32 G inst/s)
-    for (uint32_t g = (uint32_t)warp; g < ngrp; g = warp_claim(&s_next[buf])) {
-      const uint32_t e = s_grp[g];
-      const uint32_t key = e >> 19, start = e & 0x1FFFu, rem = (e >> 13) & 63u;
-      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
-        for (uint32_t q = 0; q < min(rem, 32u); ++q) {
-          const uint32_t wi = s_perm[start + q].x & 0xFFFFu;
-          const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
-          const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
-                             (uint64_t)r.nargs <= si.hi - r.arg_off;
+    // Evaluation by 32-slot slices of the key-sorted order (warp w takes slice
+    // w, then claims): a slice holds one or a few keys (the sort makes each
+    // key's records contiguous); the warp runs each key's code once with that
+    // key's lanes active.  One claim per 32 records instead of one per
+    // (key, 32-record) group, and no group table.  (Claiming ahead was measured
+    // slower: a warp holding a claim lengthens the tail, C4 1.04 -> 0.32.)
+    const uint32_t nsl = (uint32_t)(m + 31) / 32;
+    for (uint32_t sl = (uint32_t)warp; sl < nsl; sl = warp_claim(&s_next[buf])) {
+      const uint32_t slot = sl * 32 + lane;
+      const bool valid = slot < (uint32_t)m;
+      const uint2 pe = valid ? s_perm[slot] : make_uint2(0xFFFFFFFFu, 0u);
+      const uint32_t mykey = pe.x >> 16;
+      uint32_t pending = __ballot_sync(0xffffffffu, valid);
+      while (pending) {
+        const uint32_t key = __shfl_sync(0xffffffffu, mykey, __ffs(pending) - 1);
+        const bool mine = valid && mykey == key;
+        const uint32_t mask = __ballot_sync(0xffffffffu, mine);
+        pending &= ~mask;
+        if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+          for (uint32_t wm = mask; wm; wm &= wm - 1) {
+            const uint32_t wi = __shfl_sync(0xffffffffu, pe.x & 0xFFFFu, __ffs(wm) - 1);
+            const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
+            const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                               (uint64_t)r.nargs <= si.hi - r.arg_off;
+            const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                     : B.args + r.arg_off;
+            const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+            if (lane == 0) s_code[wi] = cw;
+          }
+          continue;
+        }
+        if (mine) {
+          const uint32_t li = pe.x & 0xFFFFu;
+          const picker_rec_t r = rec_from_smem(hdr + 32 * li);
+          // args inside the staged span [lo, hi) (span < 2^32 slots): one 64-bit
+          // subtraction, then 32-bit compares
+          const uint64_t rel = r.arg_off - si.lo;
+          const bool local = si.staged && (rel >> 32) == 0 && (uint32_t)rel <= (uint32_t)(si.hi - si.lo) &&
+                             r.nargs <= (uint32_t)(si.hi - si.lo) - (uint32_t)rel;
+          // one call site: a second inlined copy of every shape function (shared
+          // vs global pointer) doubles the code and thrashes the instruction
+          // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
           const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
                                    : B.args + r.arg_off;
-          const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
-          if (lane == 0) s_code[wi] = cw;
+          s_code[li] = Dispatch::eval(key, key, pe.y, local, P, r, a, B);
         }
-        continue;
-      }
-      if ((uint32_t)lane < rem) {
-        const uint2 pe = s_perm[start + lane];
-        const uint32_t li = pe.x & 0xFFFFu;
-        const picker_rec_t r = rec_from_smem(hdr + 32 * li);
-        // args inside the staged span [lo, hi) (span < 2^32 slots): one 64-bit
-        // subtraction, then 32-bit compares
-        const uint64_t rel = r.arg_off - si.lo;
-        const bool local = si.staged && (rel >> 32) == 0 && (uint32_t)rel <= (uint32_t)(si.hi - si.lo) &&
-                           r.nargs <= (uint32_t)(si.hi - si.lo) - (uint32_t)rel;
-        // one call site: a second inlined copy of every shape function (shared
-        // vs global pointer) doubles the code and thrashes the instruction
-        // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
-        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
-                                 : B.args + r.arg_off;
-        const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
-        s_code[li] = code;
       }
     }
     if (tile + G < ntiles) keys(tile + G, it + 1);
@@ -530,8 +531,7 @@ struct GenericDispatch {
   static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local,
                                                  const BucketParams& P, const picker_rec_t& r,
                                                  const int64_t* a, const DevBatch& B) {
-    (void)key, (void)kn, (void)local;
-    if (bin >= P.nbins) return V_ERR_KERNEL;
+    (void)key, (void)bin, (void)kn, (void)local;  // the evaluator checks the kernel id itself
     return eval_generic(P.T, r, a, B.args_lo, B.args_hi);
   }
 };
