@@ -63,6 +63,15 @@ __device__ __forceinline__ bool args_in_range(const picker_rec_t& r, uint32_t np
          (uint64_t)r.nargs <= hi - r.arg_off;
 }
 
+// Code of a record whose kernel needs no evaluation (KbEntry.kn direct code):
+// unknown ids, kernel-level classes after the arity / pool check.
+__device__ __forceinline__ uint32_t direct_code(uint32_t kn, uint32_t nargs, uint64_t arg_off, uint64_t lo,
+                                                uint64_t hi) {
+  if (!(kn & kDirectArity)) return kn & 0xFFu;
+  const bool ok = nargs == (kn >> 24) && arg_off >= lo && arg_off <= hi && (uint64_t)nargs <= hi - arg_off;
+  return ok ? (kn & 0xFFu) : (uint32_t)V_ERR_ARITY;
+}
+
 // Operand values of one record.  `a` points at the record's own argument
 // slots: global memory, or the CTA's shared-memory copy (generic pointer).
 struct RecVals {

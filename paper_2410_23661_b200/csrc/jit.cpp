@@ -50,6 +50,7 @@ struct JitModule {
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
   uint32_t kb_unknown = 0;
+  uint32_t shortcut_key = 0;  // grouping key of the shortcut kernels and unknown ids
   uint32_t nkeys = 0;
   int nshapes = 0;
   int tile = 0, threads = 0, ctas = 0;
@@ -207,7 +208,10 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
   // emits the extent of descriptor di as `const int64_t lb<di>, ub<di>` at indent `ind`
   auto extent = [&](size_t di, const char* ind) {
     const IrDesc& d = k.desc[di];
-    std::string lb = d.base == OPD_NONE ? "0LL" : opnd(d.base), ub = lb;
+    // the term sums first and the base last: descriptors with the same terms
+    // (e.g. every buffer of one tensor shape) share one offset expression,
+    // which the compiler then computes once
+    std::string lb = "0LL", ub = lb;
     for (size_t ti = 0; ti < d.terms.size(); ++ti) {
       const IrTerm& t = d.terms[ti];
       std::string c = g.prod(t.c);
@@ -237,6 +241,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
       }
     }
     if (d.width > 1) ub = "add64(" + ub + ", " + g.k((int64_t)d.width - 1) + ")";
+    if (d.base != OPD_NONE) lb = "add64(" + opnd(d.base) + ", " + lb + ")", ub = "add64(" + opnd(d.base) + ", " + ub + ")";
     s << ind << "const int64_t lb" << di << " = " << lb << ", ub" << di << " = " << ub << ";\n";
     if (stride) {  // g = gcd of |sum of coefficients| of the varying (variable, divisor) groups
       std::vector<std::pair<std::pair<int, uint32_t>, std::string>> groups;
@@ -289,6 +294,8 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
       if (stride) t = "(" + t + " && may_collide(lb" + I + ", G" + I + "(), W" + I + ", lb" + J + ", G" + J + "(), W" + J + "))";
       hit += " | " + t;
     }
+    // (a hull pre-filter over the kept extents was measured slower on C4:
+    // the branch per streamed extent grows the code, which is what bounds it)
     s << "    ov |= on" << di << " & (" << hit << ");\n  }\n";
   }
   auto any = [&](const std::vector<int>& a) {
@@ -432,8 +439,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
     if (k.path == PATH_WIDE) {
       m.shape = SHAPE_WIDE;  // evaluated warp-cooperatively by the bucket kernel itself
     } else if (k.path == PATH_SHORTCUT) {
-      m.shape = shape_shortcut;
-      P.consts.push_back(k.shortcut);
+      m.shape = shape_shortcut;  // direct code in the KbEntry (jit_build), no constants
     } else if (k.path == PATH_JIT) {
       const int s = shape_of[i];
       m.shape = SHAPE_FIRST + (uint32_t)s;
@@ -458,12 +464,12 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
          "    if (key == 0) return V_ERR_KERNEL;\n"
       << (stride ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
                  : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
-      <<
+      << "    if (key == " << shape_shortcut
+      << ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, B.args_hi);\n"
          "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
          "      return V_ERR_ARITY;\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
-         "    switch (key) {\n"
-         "      case " << shape_shortcut << ": return (uint8_t)__ldg(K);\n";
+         "    switch (key) {\n";
   for (size_t s = 0; s < shapes.size(); ++s)
     src << "      case " << SHAPE_FIRST + s << ": return ks" << s << "(r, a, K);\n";
   src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
@@ -563,8 +569,10 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   uint32_t maxid = 0;
   for (auto& k : ks) maxid = std::max(maxid, k.id);
   const uint32_t nbins = (uint32_t)ks.size();
-  m->kb_unknown = nbins | ((uint32_t)SHAPE_UNKNOWN << 16);
-  std::vector<KbEntry> kb(ks.empty() ? 1 : (size_t)maxid + 1, KbEntry{m->kb_unknown, 0});
+  // unknown ids take the shortcut key with the direct code 0xFF (no arity check)
+  m->shortcut_key = SHAPE_FIRST + (uint32_t)plan.nshapes;
+  m->kb_unknown = nbins | (m->shortcut_key << 16);
+  std::vector<KbEntry> kb(ks.empty() ? 1 : (size_t)maxid + 1, KbEntry{m->kb_unknown, V_ERR_KERNEL});
   for (uint32_t i = 0; i < nbins; ++i) {
     const JitMeta& jm = plan.meta[i];
     if (jm.koff >= (1u << 24) || jm.nparams > 255) {
@@ -572,7 +580,9 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
       jit_destroy(m);
       return nullptr;
     }
-    kb[ks[i].id] = KbEntry{i | ((uint32_t)plan.key_of[i] << 16), jm.koff | (jm.nparams << 24)};
+    const uint32_t kn = ks[i].path == PATH_SHORTCUT ? (uint32_t)ks[i].shortcut | kDirectArity | (jm.nparams << 24)
+                                                    : jm.koff | (jm.nparams << 24);
+    kb[ks[i].id] = KbEntry{i | ((uint32_t)plan.key_of[i] << 16), kn};
   }
   if (e == cudaSuccess) e = cudaMalloc(&m->d_kb, kb.size() * sizeof(KbEntry));
   if (e == cudaSuccess)
@@ -631,6 +641,7 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
   P.kb_unknown = m->kb_unknown;
   P.nkeys = m->nkeys;
   P.wide_key = m->stride ? 0xFFFFFFFFu : SHAPE_WIDE;  // stride mode: wide kernels through eval_stride
+  P.direct_key = m->shortcut_key;
   const uint64_t ntiles = (n + m->tile - 1) / m->tile;
   const uint64_t cap = (uint64_t)num_sms * m->ctas;
   const uint64_t grid = ntiles < cap ? ntiles : cap;

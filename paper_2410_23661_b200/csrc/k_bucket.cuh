@@ -65,6 +65,30 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       : "memory");
 }
 
+// Thread 0: fetch the argument-span bounds of a tile (its first record's
+// arg_off, its last record's arg_off and nargs) into shared memory with
+// cp.async, so the load latency (the headers of a tile two steps ahead are not
+// in any cache) is not waited for where it is issued; read back by
+// bounds_read after cp.async.wait_all.  bnd[2] receives the 4-byte nargs.
+__device__ __forceinline__ void bounds_async(const DevBatch& B, uint64_t n, uint64_t tile, uint64_t* bnd) {
+  const uint64_t base = tile * kTile;
+  if (base >= n) return;
+  const uint64_t m = min((uint64_t)kTile, n - base);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(bnd)), "l"(&B.rec[base].arg_off)
+               : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(bnd + 1)),
+               "l"(&B.rec[base + m - 1].arg_off)
+               : "memory");
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(bnd + 2)), "l"(&B.rec[base + m - 1].nargs)
+               : "memory");
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bounds_read(const uint64_t* bnd, uint64_t& lo, uint64_t& lo_last,
+                                            uint64_t& n_last) {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+  lo = bnd[0], lo_last = bnd[1], n_last = *reinterpret_cast<const uint32_t*>(bnd + 2);
+}
+
 struct StageInfo {
   uint64_t lo, hi;  // staged argument slots [lo, hi)
   uint32_t shift;   // byte offset of slot lo inside the staged buffer
@@ -151,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __shared__ uint32_t s_ngrp, s_next;
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ StageInfo s_info[2];
+  __shared__ __align__(16) uint64_t s_bnd[3];  // thread 0: bounds of the next tile to stage
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint64_t ntiles = (n + kTile - 1) / kTile;
@@ -186,8 +211,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const uint32_t buf = it & 1, parity = (it >> 1) & 1;
     const uint64_t base = tile * kTile;
     const int m = (int)min((uint64_t)kTile, n - base);
-    uint64_t nlo = 0, nll = 0, nnl = 0;
-    if (tid == 0) bounds(tile + 2 * G, nlo, nll, nnl);  // consumed after this tile
+    if (tid == 0) bounds_async(B, n, tile + 2 * G, s_bnd);  // consumed after this tile
     for (uint32_t b = tid; b < nk; b += kThreads) s_cnt[b] = 0;
     mbar_wait(&s_bar[buf], parity);
     const unsigned char* hdr = smem + buf * kHdrBytes;
@@ -285,9 +309,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     __syncthreads();
     // this tile's buffers are free: start the copy of the tile after next
-    if (tid == 0)
+    if (tid == 0) {
+      uint64_t nlo, nll, nnl;
+      bounds_read(s_bnd, nlo, nll, nnl);
       stage_tile(B, n, tile + 2 * G, smem + buf * kHdrBytes, smem + kArgOff + buf * kArgBufBytes,
                  &s_bar[buf], &s_info[buf], nlo, nll, nnl);
+    }
 
     // 5. emit in record order: u8 codes (coalesced), idempotent bit words
     //    (one ballot per 32 records), histogram (match_any-aggregated)
@@ -335,12 +362,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   constexpr uint32_t kHdrBytes = kTile * 32;
   constexpr uint32_t kArgOff = 2 * kHdrBytes;
   uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + 2 * kArgBufBytes);
-  uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);
+  // codes per tile parity: keys(t+1) writes direct codes while emit(t-1) is done
+  uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);  // [2][kTile]
   __shared__ uint32_t s_cnt[2][kPipeKeys];
+  __shared__ uint32_t s_grp[kTile / 32 + kPipeKeys];  // group -> start | rem << 13 | key << 19
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   __shared__ uint32_t s_next[2];
   __shared__ __align__(8) uint64_t s_bar[2];
   __shared__ StageInfo s_info[2];
+  __shared__ __align__(16) uint64_t s_bnd[3];  // thread 0: bounds of the next tile to stage
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
@@ -390,29 +420,36 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       uint32_t key = 0xFFu, kb = 0, e = 0;
       if (valid) {
         const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
-        kb = P.kb_unknown;
+        kb = P.kb_unknown, e = V_ERR_KERNEL;
         if (kid < P.T.nkernel_slots) {
           const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
           kb = v.x, e = v.y;
         }
         key = kb >> 16;
+        if (key == P.direct_key) {  // shortcut / unknown: final here, not sorted
+          const uint2 h = *reinterpret_cast<const uint2*>(hdr + 32 * i + 24);
+          s_code[buf * kTile + i] = (uint8_t)direct_code(
+              e, *reinterpret_cast<const uint32_t*>(hdr + 32 * i + 4), (uint64_t)h.y << 32 | h.x, B.args_lo,
+              B.args_hi);
+          key = 0xFFu;
+        }
       }
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int leader = __ffs(peers) - 1;
       uint32_t b = 0;
-      if (valid && lane == leader) b = atomicAdd(&s_cnt[buf][key], (uint32_t)__popc(peers));
+      if (key != 0xFFu && lane == leader) b = atomicAdd(&s_cnt[buf][key], (uint32_t)__popc(peers));
       b = __shfl_sync(0xffffffffu, b, leader);
-      kr[q] = valid ? key | (b + __popc(peers & lt_mask)) << 8 : 0xFFu;
-      rb[q] = (uint32_t)i | key << 16;
+      kr[q] = key != 0xFFu ? key | (b + __popc(peers & lt_mask)) << 8 : 0xFFu;
+      rb[q] = (uint32_t)i | (kb & 0xFFFFu) << 16;
       kn[q] = e;
     }
   };
   // codes of one tile in record order: u8 flags, idempotent bit words, histogram
-  auto emit = [&](uint64_t base, int m) {
+  auto emit = [&](uint64_t base, int m, uint32_t buf) {
     for (int i0 = warp * 32; i0 < m; i0 += kThreads) {
       const int i = i0 + lane;
       const bool valid = i < m;
-      const uint32_t c = valid ? s_code[i] : 0u;
+      const uint32_t c = valid ? s_code[buf * kTile + i] : 0u;
       const unsigned idem = __ballot_sync(0xffffffffu, valid && c <= V_IDEM_KERNEL);
       if (valid) flags[base + i] = (uint8_t)c;
       if (bits != nullptr && lane == 0) bits[(base + i0) >> 5] = idem;
@@ -423,30 +460,31 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   };
 
   if ((uint64_t)blockIdx.x < ntiles) keys(blockIdx.x, 0);
-  uint64_t nlo = 0, nll = 0, nnl = 0;  // thread 0: arg bounds of the next tile to stage
-  if (tid == 0) bounds(blockIdx.x + 2 * G, nlo, nll, nnl);
+  if (tid == 0) bounds_async(B, n, blockIdx.x + 2 * G, s_bnd);  // the next tile to stage
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
     const uint32_t buf = it & 1;
     const uint64_t base = tile * kTile;
     const int m = (int)min((uint64_t)kTile, n - base);
     __syncthreads();  // B_a: eval(t-1) and keys(t) done
-    if (it > 0) emit(base - G * kTile, kTile);  // tiles before the last are full
+    if (it > 0) emit(base - G * kTile, kTile, buf ^ 1);  // tiles before the last are full
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
     if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
     if (tid == 0) s_next[buf ^ 1] = kWarps;
-    // scan (every warp, registers): lane l holds the counts of keys l and
-    // 32 + l; inclusive, then exclusive offsets of each key's sorted records
+    // scan (every warp, registers): lane l holds keys l and 32 + l as
+    // count | groups << 16, inclusive
     const uint32_t c0 = s_cnt[buf][lane], c1 = s_cnt[buf][lane + 32];
-    uint32_t v0 = c0, v1 = c1;
+    uint32_t v0 = c0 | ((c0 + 31) >> 5) << 16, v1 = c1 | ((c1 + 31) >> 5) << 16;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t a0 = __shfl_up_sync(0xffffffffu, v0, d), a1 = __shfl_up_sync(0xffffffffu, v1, d);
       if (lane >= d) v0 += a0, v1 += a1;
     }
     v1 += __shfl_sync(0xffffffffu, v0, 31);
-    const uint32_t off0 = v0 - c0, off1 = v1 - c1;
+    const uint32_t off0 = (v0 & 0xFFFFu) - c0, off1 = (v1 & 0xFFFFu) - c1;
+    const uint32_t ginc0 = v0 >> 16, ginc1 = v1 >> 16;
+    const uint32_t ngrp = __shfl_sync(0xffffffffu, ginc1, 31);
     // scatter
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
@@ -454,70 +492,68 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31), o1 = __shfl_sync(0xffffffffu, off1, key & 31);
       if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
     }
+    // group table: warp w writes groups j = w, w + kWarps, ... of every key
+    {
+      const uint32_t gs0 = ginc0 - ((c0 + 31) >> 5), gs1 = ginc1 - ((c1 + 31) >> 5);
+      for (uint32_t j = warp; 32 * j < c0; j += kWarps)
+        s_grp[gs0 + j] = (off0 + 32 * j) | min(32u, c0 - 32 * j) << 13 | (uint32_t)lane << 19;
+      for (uint32_t j = warp; 32 * j < c1; j += kWarps)
+        s_grp[gs1 + j] = (off1 + 32 * j) | min(32u, c1 - 32 * j) << 13 | (uint32_t)(lane + 32) << 19;
+    }
     __syncthreads();  // B_b
     // the previous tile's buffers are free: start the copy of the next tile
     // (after B_b, so this serial thread-0 work is not waited for at a barrier)
     if (it > 0 && tid == 0) {
+      uint64_t nlo, nll, nnl;
+      bounds_read(s_bnd, nlo, nll, nnl);
       stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
                  &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
-      bounds(tile + 2 * G, nlo, nll, nnl);
+      bounds_async(B, n, tile + 2 * G, s_bnd);
     }
 
     const unsigned char* hdr = smem + buf * kHdrBytes;
     const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
     const StageInfo si = s_info[buf];
-    // Evaluation by 32-slot slices of the key-sorted order (warp w takes slice
-    // w, then claims): a slice holds one or a few keys (the sort makes each
-    // key's records contiguous); the warp runs each key's code once with that
-    // key's lanes active.  One claim per 32 records instead of one per
-    // (key, 32-record) group, and no group table.  (Claiming ahead was measured
-    // slower: a warp holding a claim lengthens the tail, C4 1.04 -> 0.32.)
-    const uint32_t nsl = (uint32_t)(m + 31) / 32;
-    for (uint32_t sl = (uint32_t)warp; sl < nsl; sl = warp_claim(&s_next[buf])) {
-      const uint32_t slot = sl * 32 + lane;
-      const bool valid = slot < (uint32_t)m;
-      const uint2 pe = valid ? s_perm[slot] : make_uint2(0xFFFFFFFFu, 0u);
-      const uint32_t mykey = pe.x >> 16;
-      uint32_t pending = __ballot_sync(0xffffffffu, valid);
-      while (pending) {
-        const uint32_t key = __shfl_sync(0xffffffffu, mykey, __ffs(pending) - 1);
-        const bool mine = valid && mykey == key;
-        const uint32_t mask = __ballot_sync(0xffffffffu, mine);
-        pending &= ~mask;
-        if (key == P.wide_key) {  // K2: the whole warp on one record at a time
-          for (uint32_t wm = mask; wm; wm &= wm - 1) {
-            const uint32_t wi = __shfl_sync(0xffffffffu, pe.x & 0xFFFFu, __ffs(wm) - 1);
-            const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
-            const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
-                               (uint64_t)r.nargs <= si.hi - r.arg_off;
-            const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
-                                     : B.args + r.arg_off;
-            const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
-            if (lane == 0) s_code[wi] = cw;
-          }
-          continue;
-        }
-        if (mine) {
-          const uint32_t li = pe.x & 0xFFFFu;
-          const picker_rec_t r = rec_from_smem(hdr + 32 * li);
-          // args inside the staged span [lo, hi) (span < 2^32 slots): one 64-bit
-          // subtraction, then 32-bit compares
-          const uint64_t rel = r.arg_off - si.lo;
-          const bool local = si.staged && (rel >> 32) == 0 && (uint32_t)rel <= (uint32_t)(si.hi - si.lo) &&
-                             r.nargs <= (uint32_t)(si.hi - si.lo) - (uint32_t)rel;
-          // one call site: a second inlined copy of every shape function (shared
-          // vs global pointer) doubles the code and thrashes the instruction
-          // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
+    // (claiming one group ahead was measured slower: a warp holding a claimed
+    // group lengthens the tail, C4 1.04 -> 0.32 G inst/s)
+    for (uint32_t g = (uint32_t)warp; g < ngrp; g = warp_claim(&s_next[buf])) {
+      const uint32_t e = s_grp[g];
+      const uint32_t key = e >> 19, start = e & 0x1FFFu, rem = (e >> 13) & 63u;
+      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+        for (uint32_t q = 0; q < min(rem, 32u); ++q) {
+          const uint32_t wi = s_perm[start + q].x & 0xFFFFu;
+          const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
+          const bool local = si.staged && r.arg_off >= si.lo && r.arg_off <= si.hi &&
+                             (uint64_t)r.nargs <= si.hi - r.arg_off;
           const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
                                    : B.args + r.arg_off;
-          s_code[li] = Dispatch::eval(key, key, pe.y, local, P, r, a, B);
+          const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+          if (lane == 0) s_code[buf * kTile + wi] = cw;
         }
+        continue;
+      }
+      if ((uint32_t)lane < rem) {
+        const uint2 pe = s_perm[start + lane];
+        const uint32_t li = pe.x & 0xFFFFu;
+        const picker_rec_t r = rec_from_smem(hdr + 32 * li);
+        // args inside the staged span [lo, hi) (span < 2^32 slots): one 64-bit
+        // subtraction, then 32-bit compares
+        const uint64_t rel = r.arg_off - si.lo;
+        const bool local = si.staged && (rel >> 32) == 0 && (uint32_t)rel <= (uint32_t)(si.hi - si.lo) &&
+                           r.nargs <= (uint32_t)(si.hi - si.lo) - (uint32_t)rel;
+        // one call site: a second inlined copy of every shape function (shared
+        // vs global pointer) doubles the code and thrashes the instruction
+        // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
+        const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
+                                 : B.args + r.arg_off;
+        const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
+        s_code[buf * kTile + li] = code;
       }
     }
     if (tile + G < ntiles) keys(tile + G, it + 1);
     if (tile + G >= ntiles) {  // last tile of this CTA
       __syncthreads();
-      emit(base, m);
+      emit(base, m, buf);
     }
   }
   __syncthreads();
@@ -531,7 +567,8 @@ struct GenericDispatch {
   static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local,
                                                  const BucketParams& P, const picker_rec_t& r,
                                                  const int64_t* a, const DevBatch& B) {
-    (void)key, (void)bin, (void)kn, (void)local;  // the evaluator checks the kernel id itself
+    (void)key, (void)kn, (void)local;
+    if (bin >= P.nbins) return V_ERR_KERNEL;
     return eval_generic(P.T, r, a, B.args_lo, B.args_hi);
   }
 };

@@ -17,7 +17,8 @@ struct StrideDispatch {
   static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local,
                                                  const BucketParams& P, const picker_rec_t& r, const int64_t* a,
                                                  const DevBatch& B) {
-    (void)key, (void)bin, (void)kn, (void)local;  // the evaluator checks the kernel id itself
+    (void)key, (void)kn, (void)local;
+    if (bin >= P.nbins) return V_ERR_KERNEL;
     return eval_stride(P.T, r, a, B.args_lo, B.args_hi);
   }
 };

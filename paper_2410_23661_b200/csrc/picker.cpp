@@ -204,6 +204,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
   c->P.wide_key = c->P.nbins + 1;  // table-driven grouping (the JIT module uses its own)
+  c->P.direct_key = 0xFFFFFFFFu;   // the table path evaluates shortcuts in eval_generic
   {
     size_t nd = 0, nc = 0;
     for (auto& k : ks)

@@ -141,10 +141,14 @@ struct JitMeta {
 
 // Per kernel id, read once per record when a tile is grouped (k_bucket.cuh):
 // kb = bin | key << 16 (key: the grouping key), kn = offset of the kernel's
-// constants | nparams << 24 (specialised module; 0 on the table path).
+// constants | nparams << 24 (specialised module; 0 on the table path).  For
+// the key BucketParams.direct_key (kernel-level shortcuts and unknown ids of
+// the specialised module) kn is a direct code: code | kDirectArity (the arity
+// and pool checks apply) | nparams << 24.
 struct KbEntry {
   uint32_t kb, kn;
 };
+constexpr uint32_t kDirectArity = 0x100u;
 
 // Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
 struct BucketParams {
@@ -155,6 +159,8 @@ struct BucketParams {
   uint32_t kb_unknown;          // kb of an id that is not loaded
   const int64_t* jit_consts;   // per-kernel constants (specialised module only)
   uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
+  uint32_t direct_key;         // key whose code is final in the key pass (KbEntry.kn = direct
+                               // code, see direct_code); 0xFFFFFFFF: none
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads
@@ -190,11 +196,11 @@ constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
   return bucket_smem_bytes_for(nkeys, kTile, PICKER_ARGS_PER_REC);
 }
 // Pipelined variant for at most kPipeKeys grouping keys (k_validate_pipe):
-// staging buffers, s_perm (u32 x 2) and s_code (u8) per record; the per-key
+// staging buffers, s_perm (u32 x 2) and two s_code (u8) per record; the per-key
 // counters are static shared memory.
 constexpr uint32_t kPipeKeys = 64;
 constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec) {
-  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 9 + 128;
+  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 + 128;
 }
 
 // Generic-path limits (a kernel beyond them uses the wide path).
