@@ -384,8 +384,13 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
   JitPlan P;
   std::ostringstream src;
+  // paths no kernel of this summary takes are left out of the module (code size)
+  bool any_wide = false, any_generic = false;
+  for (auto& k : ks) any_wide |= k.path == PATH_WIDE, any_generic |= k.path == PATH_GENERIC;
+  const bool table_path = any_generic || (stride && any_wide);  // key 1 (and 2 in stride mode)
   src << "// generated by picker jit.cpp\n"
-         "typedef signed char int8_t; typedef short int16_t; typedef int int32_t; typedef long long int64_t;\n"
+      << (stride || !any_wide ? "#define PICKER_NO_WIDE 1\n" : "")
+      << "typedef signed char int8_t; typedef short int16_t; typedef int int32_t; typedef long long int64_t;\n"
          "typedef unsigned char uint8_t; typedef unsigned short uint16_t; typedef unsigned int uint32_t;\n"
          "typedef unsigned long long uint64_t; typedef unsigned long size_t; typedef unsigned long uintptr_t;\n"
          "#include \"eval_generic.cuh\"\n#include \"eval_stride.cuh\"\n#include \"k_bucket.cuh\"\n"
@@ -462,8 +467,9 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
          "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
          "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
-      << (stride ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
-                 : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
+      << (!table_path ? ""
+          : stride    ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
+                      : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
       << "    if (key == " << shape_shortcut
       << ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, B.args_hi);\n"
          "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"

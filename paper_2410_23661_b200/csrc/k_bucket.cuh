@@ -33,6 +33,15 @@
 
 namespace picker {
 
+// A specialised module without wide (K2) kernels is compiled with
+// PICKER_NO_WIDE: the warp-cooperative path is then dead code that would sit
+// between the hot loop's blocks (instruction-cache locality).
+#ifdef PICKER_NO_WIDE
+constexpr bool kWidePath = false;
+#else
+constexpr bool kWidePath = true;
+#endif
+
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
@@ -284,7 +293,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const uint32_t e = s_grp[g];
       const uint32_t key = e >> 8, j = e & 255u;
       const uint32_t start = s_off[key] + 32u * j, rem = s_cnt[key] - 32u * j;
-      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+      if (kWidePath && key == P.wide_key) {  // K2: the whole warp on one record at a time
         for (uint32_t q = 0; q < min(rem, 32u); ++q) {
           const uint32_t wi = s_perm[start + q];
           const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
@@ -413,35 +422,46 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     const int m = (int)min((uint64_t)kTile, n - base);
     mbar_wait(&s_bar[buf], (it >> 1) & 1);
     const unsigned char* hdr = smem + buf * kHdrBytes;
+    // phases over all of the thread's records, so the table loads and the
+    // match_any latencies of its records overlap
+    uint32_t key[kPer], e[kPer];
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int i = q * kThreads + warp * 32 + lane;
-      const bool valid = i < m;
-      uint32_t key = 0xFFu, kb = 0, e = 0;
-      if (valid) {
+      uint32_t kb = 0xFFu << 16;
+      e[q] = V_ERR_KERNEL;
+      if (i < m) {
         const uint32_t kid = *reinterpret_cast<const uint32_t*>(hdr + 32 * i);
-        kb = P.kb_unknown, e = V_ERR_KERNEL;
+        kb = P.kb_unknown;
         if (kid < P.T.nkernel_slots) {
           const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + kid);
-          kb = v.x, e = v.y;
-        }
-        key = kb >> 16;
-        if (key == P.direct_key) {  // shortcut / unknown: final here, not sorted
-          const uint2 h = *reinterpret_cast<const uint2*>(hdr + 32 * i + 24);
-          s_code[buf * kTile + i] = (uint8_t)direct_code(
-              e, *reinterpret_cast<const uint32_t*>(hdr + 32 * i + 4), (uint64_t)h.y << 32 | h.x, B.args_lo,
-              B.args_hi);
-          key = 0xFFu;
+          kb = v.x, e[q] = v.y;
         }
       }
-      const unsigned peers = __match_any_sync(0xffffffffu, key);
-      const int leader = __ffs(peers) - 1;
-      uint32_t b = 0;
-      if (key != 0xFFu && lane == leader) b = atomicAdd(&s_cnt[buf][key], (uint32_t)__popc(peers));
-      b = __shfl_sync(0xffffffffu, b, leader);
-      kr[q] = key != 0xFFu ? key | (b + __popc(peers & lt_mask)) << 8 : 0xFFu;
+      key[q] = kb >> 16;
       rb[q] = (uint32_t)i | (kb & 0xFFFFu) << 16;
-      kn[q] = e;
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int i = q * kThreads + warp * 32 + lane;
+      if (key[q] == P.direct_key) {  // shortcut / unknown: final here, not sorted
+        const uint2 h = *reinterpret_cast<const uint2*>(hdr + 32 * i + 24);
+        s_code[buf * kTile + i] = (uint8_t)direct_code(e[q], *reinterpret_cast<const uint32_t*>(hdr + 32 * i + 4),
+                                                       (uint64_t)h.y << 32 | h.x, B.args_lo, B.args_hi);
+        key[q] = 0xFFu;
+      }
+    }
+    unsigned peers[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) peers[q] = __match_any_sync(0xffffffffu, key[q]);
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int leader = 31 - __clz(peers[q]);  // any lane of the peers does the add
+      uint32_t b = 0;
+      if (key[q] != 0xFFu && lane == leader) b = atomicAdd(&s_cnt[buf][key[q]], (uint32_t)__popc(peers[q]));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      kr[q] = key[q] != 0xFFu ? key[q] | (b + __popc(peers[q] & lt_mask)) << 8 : 0xFFu;
+      kn[q] = e[q];
     }
   };
   // codes of one tile in record order: u8 flags, idempotent bit words, histogram
@@ -519,7 +539,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     for (uint32_t g = (uint32_t)warp; g < ngrp; g = warp_claim(&s_next[buf])) {
       const uint32_t e = s_grp[g];
       const uint32_t key = e >> 19, start = e & 0x1FFFu, rem = (e >> 13) & 63u;
-      if (key == P.wide_key) {  // K2: the whole warp on one record at a time
+      if (kWidePath && key == P.wide_key) {  // K2: the whole warp on one record at a time
         for (uint32_t q = 0; q < min(rem, 32u); ++q) {
           const uint32_t wi = s_perm[start + q].x & 0xFFFFu;
           const picker_rec_t r = rec_from_smem(hdr + 32 * wi);
