@@ -17,6 +17,11 @@ namespace picker {
 __device__ __forceinline__ int64_t mul64(int64_t a, int64_t b) {
   return (int64_t)((uint64_t)a * (uint64_t)b);
 }
+// Product of two values the loader proved to fit int32 (IrTerm.narrow): one
+// 32x32->64 multiply, exact.
+__device__ __forceinline__ int64_t mulw(int64_t a, int64_t b) {
+  return (int64_t)(int32_t)a * (int64_t)(int32_t)b;
+}
 __device__ __forceinline__ int64_t add64(int64_t a, int64_t b) {
   return (int64_t)((uint64_t)a + (uint64_t)b);
 }

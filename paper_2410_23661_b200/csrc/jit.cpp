@@ -119,7 +119,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
   s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K) {\n";
   s << "  const int64_t d0 = r.grid_x, d1 = r.grid_y, d2 = r.grid_z, d3 = r.block_x, d4 = r.block_y,"
        " d5 = r.block_z;\n";
-  s << "  if (!launch_limits_rec(r)) return V_NI_PRECOND;\n";
+  // (the CUDA launch limits are checked once in the dispatch, before the switch)
   std::vector<bool> used(np, false);
   for (auto* lst : {&k.pre, &k.glob})
     for (auto& c : *lst) uses(c.op, used);
@@ -140,12 +140,16 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
       else
         s << "  const int64_t x" << i << " = a[" << i << "];\n";
     }
-  for (auto& c : k.pre)
-    s << "  if (" << opnd(c.op) << " < " << g.k(c.lo) << " || " << opnd(c.op) << " > " << g.k(c.hi)
-      << ") return V_NI_PRECOND;\n";
-  for (auto& c : k.glob)
-    s << "  if (" << opnd(c.op) << " < " << g.k(c.lo) << " || " << opnd(c.op) << " > " << g.k(c.hi)
-      << ") return V_NI_GLOBAL;\n";
+  // lo <= x <= hi; with lo = 0 <= hi (every pointer bound) one unsigned compare
+  auto check = [&](const IrCheck& c, const char* code) {
+    if (c.lo == 0 && c.hi >= 0)
+      s << "  if ((uint64_t)" << opnd(c.op) << " > (uint64_t)" << g.k(c.hi) << ") return " << code << ";\n";
+    else
+      s << "  if (" << opnd(c.op) << " < " << g.k(c.lo) << " || " << opnd(c.op) << " > " << g.k(c.hi) << ") return "
+        << code << ";\n";
+  };
+  for (auto& c : k.pre) check(c, "V_NI_PRECOND");
+  for (auto& c : k.glob) check(c, "V_NI_GLOBAL");
   // variable slots, deduplicated by content (as in flatten())
   struct SlotKey {
     uint8_t skind, axis;
@@ -226,16 +230,17 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
       };
       const std::string L = "vl" + std::to_string(x), H = "vh" + std::to_string(x);
       const int sign = k.var_sign[di][t.var];
+      const std::string mul = t.narrow ? "mulw" : "mul64";
       if (sign > 0) {  // non-decreasing: min at lo, max at hi
-        if (!lo0[x]) lb = "add64(" + lb + ", mul64(" + c + ", " + phi(L) + "))";
-        ub = "add64(" + ub + ", mul64(" + c + ", " + phi(H) + "))";
+        if (!lo0[x]) lb = "add64(" + lb + ", " + mul + "(" + c + ", " + phi(L) + "))";
+        ub = "add64(" + ub + ", " + mul + "(" + c + ", " + phi(H) + "))";
       } else if (sign < 0) {
-        lb = "add64(" + lb + ", mul64(" + c + ", " + phi(H) + "))";
-        if (!lo0[x]) ub = "add64(" + ub + ", mul64(" + c + ", " + phi(L) + "))";
+        lb = "add64(" + lb + ", " + mul + "(" + c + ", " + phi(H) + "))";
+        if (!lo0[x]) ub = "add64(" + ub + ", " + mul + "(" + c + ", " + phi(L) + "))";
       } else {  // one term of unknown sign: both ends
         const std::string cv = "c" + std::to_string(di) + "_" + std::to_string(ti);
         s << ind << "const int64_t " << cv << " = " << c << ";\n";
-        std::string A = "mul64(" + cv + ", " + phi(L) + ")", Bv = "mul64(" + cv + ", " + phi(H) + ")";
+        std::string A = mul + "(" + cv + ", " + phi(L) + ")", Bv = mul + "(" + cv + ", " + phi(H) + ")";
         lb = "add64(" + lb + ", min64(" + A + ", " + Bv + "))";
         ub = "add64(" + ub + ", max64(" + A + ", " + Bv + "))";
       }
@@ -474,6 +479,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
       << ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, B.args_hi);\n"
          "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
          "      return V_ERR_ARITY;\n"
+         "    if (!launch_limits_rec(r)) return V_NI_PRECOND;  // every shape's first check\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n";
   for (size_t s = 0; s < shapes.size(); ++s)

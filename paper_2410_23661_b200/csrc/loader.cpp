@@ -440,6 +440,10 @@ void verify_kernel(IrKernel& k) {
       }
       Iv tv = ivmul(c, x);
       if (!fits(tv)) uerr(who + "term may overflow int64");
+      // both factors within int32 on every record that reaches the extents:
+      // the specialised code multiplies them with one 32x32->64 instruction
+      const i128 m31 = ((i128)1) << 31;
+      t.narrow = t.var >= 0 && c.lo >= -m31 && c.hi < m31 && x.lo >= -m31 && x.hi < m31;
       mag += std::max(-tv.lo, tv.hi);
     }
     mag += d.width;

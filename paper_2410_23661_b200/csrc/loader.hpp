@@ -41,6 +41,7 @@ struct IrTerm {
   IrProd c;
   int var;              // index into the descriptor's vars, -1: constant
   int64_t div;          // >= 1
+  bool narrow = false;  // verify_kernel: coefficient and floor(x / div) both fit int32
 };
 
 struct IrGuard {
