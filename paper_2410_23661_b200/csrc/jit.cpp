@@ -142,6 +142,20 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     }
   // lo <= x <= hi; with lo = 0 <= hi (every pointer bound) one unsigned compare
   auto check = [&](const IrCheck& c, const char* code) {
+    if (c.op < 6 || (c.op >= OPD_ARG0 && k.param_i32[c.op - OPD_ARG0])) {
+      // a launch dimension (in [1, kDimMax], launch limits checked first) or
+      // an i32 argument: clamp the bounds to the operand's type range, then one
+      // 32-bit compare of x - lo against the span (the range holds <= 2^32
+      // values; lo > hi after clamping never reaches a shape: the loader
+      // routes such kernels to the table path)
+      const int64_t tlo = c.op < 6 ? 1 : -2147483648LL, thi = c.op < 6 ? kDimMax[c.op] : 2147483647LL;
+      const int64_t lo = std::max(c.lo, tlo), hi = std::min(c.hi, thi);
+      if (lo <= hi) {
+        s << "  if ((uint32_t)" << opnd(c.op) << " - (uint32_t)" << g.k(lo) << " > (uint32_t)" << g.k(hi - lo)
+          << ") return " << code << ";\n";
+        return;
+      }
+    }
     if (c.lo == 0 && c.hi >= 0)
       s << "  if ((uint64_t)" << opnd(c.op) << " > (uint64_t)" << g.k(c.hi) << ") return " << code << ";\n";
     else
@@ -169,7 +183,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     return kk;
   };
   std::vector<SlotKey> keys;
-  std::vector<bool> lo0;
+  std::vector<bool> lo0, nonempty;
   auto slot_of = [&](const IrVar& v) -> int {
     SlotKey kk = key_of(v);
     for (size_t i = 0; i < keys.size(); ++i)
@@ -186,6 +200,8 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     for (auto& e : v.hi) add_hi(g.bexpr(e));
     keys.push_back(kk);
     lo0.push_back(v.skind != SK_NONE && v.lo.empty());
+    // [0, dim - 1] with dims >= 1 (launch limits): never empty
+    nonempty.push_back(v.skind != SK_NONE && v.lo.empty() && v.hi.empty());
     const size_t i = keys.size() - 1;
     s << "  const int64_t vl" << i << " = " << lo << ", vh" << i << " = " << hi << ";\n";
     return (int)i;
@@ -206,7 +222,8 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     std::string on = "true";
     for (auto& gd : d.guard)
       on += " && (" + opnd(gd.a) + " " + kCmp[gd.cmp] + " " + (gd.b == OPD_NONE ? g.k(gd.bconst) : opnd(gd.b)) + ")";
-    for (int x : sids[di]) on += " && (vl" + std::to_string(x) + " <= vh" + std::to_string(x) + ")";
+    for (int x : sids[di])
+      if (!nonempty[x]) on += " && (vl" + std::to_string(x) + " <= vh" + std::to_string(x) + ")";
     return on;
   };
   // emits the extent of descriptor di as `const int64_t lb<di>, ub<di>` at indent `ind`
