@@ -492,9 +492,12 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
       << (!table_path ? ""
           : stride    ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
                       : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
-      << "    if (key == " << shape_shortcut
-      << ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, B.args_hi);\n"
-         "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
+      // the pipelined kernel finishes shortcut / unknown records in its key pass
+      << (shape_shortcut + 1 <= kPipeKeys ? std::string()
+                                          : "    if (key == " + std::to_string(shape_shortcut) +
+                                                ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, "
+                                                "B.args_hi);\n")
+      << "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
          "      return V_ERR_ARITY;\n"
          "    if (!launch_limits_rec(r)) return V_NI_PRECOND;  // every shape's first check\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
