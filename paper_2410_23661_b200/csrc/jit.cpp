@@ -528,7 +528,8 @@ void order_by_shape(std::vector<IrKernel>& ks) {
 std::vector<std::string> geometry_defines(const Options& opt) {
   return {"-DPICKER_TILE=" + std::to_string(opt.tile), "-DPICKER_THREADS=" + std::to_string(opt.threads),
           "-DPICKER_CTAS=" + std::to_string(opt.ctas),
-          "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec)};
+          "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
+          "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs)};
 }
 
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
@@ -553,8 +554,8 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 
 // tile = 0 (auto, the default): geometry from the loaded COND kernels' mean
 // parameter count.  Few arguments (C2: 3.7, C3: 3.4): 448-record tiles, 224
-// threads, 3 CTAs/SM, 5 staged argument slots per record -- 21 warps/SM instead
-// of 16 (measured C2 35.0 -> 37.0 G inst/s, profiles/r01_sweep_geometry.txt).
+// threads, 5 staged argument slots per record, one argument buffer, 4 CTAs/SM
+// (28 warps; profiles/r01_sweep_geometry.txt has the sweep).
 // Many arguments (C4: 33): the argument spans do not fit a staging buffer
 // anyway, so the shared memory goes to 2048-record tiles of headers (512
 // threads, 1 CTA/SM, 1 staged slot per record): 4x more records per shape per
@@ -567,7 +568,11 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
     if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC) sum += k.param_names.size(), ++cnt;
   const double mean = cnt ? sum / cnt : 4.0;
   if (mean <= 6.0) {
-    opt.tile = 448, opt.threads = 224, opt.ctas = 3, opt.args_per_rec = 5;
+    // one argument buffer (the arguments of a tile are fetched while the
+    // previous tile is emitted and this one scattered) frees the shared memory
+    // for a 4th CTA: 28 warps/SM at 72 registers, no spills (C2 43.8 -> 47.4 G
+    // inst/s, C3 25.4 -> 27.4)
+    opt.tile = 448, opt.threads = 224, opt.ctas = 4, opt.args_per_rec = 5, opt.arg_bufs = 1;
   } else {
     opt.tile = 2048, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1;
   }
@@ -577,7 +582,8 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
 JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std::string& err) {
   const Options opt = resolve_geometry(ks, opt_in);
   if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
-      opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1) {
+      opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1 || opt.arg_bufs < 1 ||
+      opt.arg_bufs > 2) {
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
@@ -628,7 +634,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     return nullptr;
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes + 1;
-  m->smem = m->nkeys <= kPipeKeys ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec)
+  m->smem = m->nkeys <= kPipeKeys ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
+                                                        (uint32_t)opt.arg_bufs)
                                   : bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {
     err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";

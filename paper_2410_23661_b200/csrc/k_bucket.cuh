@@ -135,6 +135,43 @@ __device__ __forceinline__ void stage_tile(const DevBatch& B, uint64_t n, uint64
   if (abytes) tma_load_1d(arg, src, abytes, bar);
 }
 
+// Split staging for the single argument buffer (kArgBufs == 1): the headers
+// of a tile go ahead (double-buffered, sizes known without reading them); its
+// arguments are fetched once the previous tile's evaluation has released the
+// buffer, with the span read from the headers already in shared memory.
+__device__ __forceinline__ void stage_hdr(const DevBatch& B, uint64_t n, uint64_t tile, unsigned char* hdr,
+                                          uint64_t* bar) {
+  const uint64_t base = tile * kTile;
+  if (base >= n) return;
+  const uint32_t hbytes = (uint32_t)(min((uint64_t)kTile, n - base) * sizeof(picker_rec_t));
+  mbar_arrive_expect_tx(bar, hbytes);
+  tma_load_1d(hdr, B.rec + base, hbytes, bar);
+}
+__device__ __forceinline__ void stage_args(const DevBatch& B, int m, const unsigned char* hdr, unsigned char* arg,
+                                           uint64_t* bar, StageInfo* info) {
+  const uint64_t lo = *reinterpret_cast<const uint64_t*>(hdr + 24);
+  const uint64_t last_off = *reinterpret_cast<const uint64_t*>(hdr + 32 * (m - 1) + 24);
+  const uint64_t last_n = *reinterpret_cast<const uint32_t*>(hdr + 32 * (m - 1) + 4);
+  const uint64_t hi = last_off + last_n;
+  StageInfo si{lo, hi, 0, 0};
+  uint32_t abytes = 0;
+  const char* src = nullptr;
+  if (hi > lo && hi - lo <= (uint64_t)kArgCap && lo >= B.args_lo && hi <= B.args_hi) {
+    const uintptr_t a0 = (uintptr_t)(B.args + lo), a1 = (uintptr_t)(B.args + hi);
+    const uintptr_t s0 = a0 & ~(uintptr_t)15, s1 = (a1 + 15) & ~(uintptr_t)15;
+    const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
+    if (s0 >= p0 && s1 <= p1) {
+      si.staged = 1;
+      si.shift = (uint32_t)(a0 - s0);
+      abytes = (uint32_t)(s1 - s0);
+      src = (const char*)s0;
+    }
+  }
+  *info = si;
+  mbar_arrive_expect_tx(bar, abytes);  // 0 bytes: the phase completes at once
+  if (abytes) tma_load_1d(arg, src, abytes, bar);
+}
+
 __device__ __forceinline__ picker_rec_t rec_from_smem(const unsigned char* p) {
   const uint4 a = *reinterpret_cast<const uint4*>(p), b = *reinterpret_cast<const uint4*>(p + 16);
   picker_rec_t r;
@@ -370,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   extern __shared__ __align__(128) unsigned char smem[];
   constexpr uint32_t kHdrBytes = kTile * 32;
   constexpr uint32_t kArgOff = 2 * kHdrBytes;
-  uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + 2 * kArgBufBytes);
+  uint2* s_perm = reinterpret_cast<uint2*>(smem + kArgOff + kArgBufs * kArgBufBytes);
   // codes per tile parity: keys(t+1) writes direct codes while emit(t-1) is done
   uint8_t* s_code = reinterpret_cast<uint8_t*>(s_perm + kTile);  // [2][kTile]
   __shared__ uint32_t s_cnt[2][kPipeKeys];
@@ -378,6 +415,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   __shared__ uint32_t s_next[2];
   __shared__ __align__(8) uint64_t s_bar[2];
+  __shared__ __align__(8) uint64_t s_abar;  // kArgBufs == 1: the argument buffer
   __shared__ StageInfo s_info[2];
   __shared__ __align__(16) uint64_t s_bnd[3];  // thread 0: bounds of the next tile to stage
 
@@ -403,13 +441,18 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   if (tid == 0) {
     mbar_init(&s_bar[0], 1);
     mbar_init(&s_bar[1], 1);
+    mbar_init(&s_abar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     for (int b = 0; b < 2; ++b) {
-      uint64_t lo, ll, nl;
-      bounds(blockIdx.x + b * G, lo, ll, nl);
-      stage_tile(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, smem + kArgOff + b * kArgBufBytes,
-                 &s_bar[b], &s_info[b], lo, ll, nl);
+      if constexpr (kArgBufs == 1) {
+        stage_hdr(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, &s_bar[b]);
+      } else {
+        uint64_t lo, ll, nl;
+        bounds(blockIdx.x + b * G, lo, ll, nl);
+        stage_tile(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, smem + kArgOff + b * kArgBufBytes,
+                   &s_bar[b], &s_info[b], lo, ll, nl);
+      }
     }
   }
   __syncthreads();
@@ -480,13 +523,16 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   };
 
   if ((uint64_t)blockIdx.x < ntiles) keys(blockIdx.x, 0);
-  if (tid == 0) bounds_async(B, n, blockIdx.x + 2 * G, s_bnd);  // the next tile to stage
+  if (kArgBufs == 2 && tid == 0) bounds_async(B, n, blockIdx.x + 2 * G, s_bnd);  // the next tile to stage
   uint32_t it = 0;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += G, ++it) {
     const uint32_t buf = it & 1;
     const uint64_t base = tile * kTile;
     const int m = (int)min((uint64_t)kTile, n - base);
     __syncthreads();  // B_a: eval(t-1) and keys(t) done
+    // single argument buffer: free now; fetch this tile's arguments, which
+    // the scan / scatter / emit below overlap
+    if (kArgBufs == 1 && tid == 0) stage_args(B, m, smem + buf * kHdrBytes, smem + kArgOff, &s_abar, &s_info[buf]);
     if (it > 0) emit(base - G * kTile, kTile, buf ^ 1);  // tiles before the last are full
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
@@ -524,15 +570,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // the previous tile's buffers are free: start the copy of the next tile
     // (after B_b, so this serial thread-0 work is not waited for at a barrier)
     if (it > 0 && tid == 0) {
-      uint64_t nlo, nll, nnl;
-      bounds_read(s_bnd, nlo, nll, nnl);
-      stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
-                 &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
-      bounds_async(B, n, tile + 2 * G, s_bnd);
+      if constexpr (kArgBufs == 1) {
+        stage_hdr(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, &s_bar[buf ^ 1]);
+      } else {
+        uint64_t nlo, nll, nnl;
+        bounds_read(s_bnd, nlo, nll, nnl);
+        stage_tile(B, n, tile + G, smem + (buf ^ 1) * kHdrBytes, smem + kArgOff + (buf ^ 1) * kArgBufBytes,
+                   &s_bar[buf ^ 1], &s_info[buf ^ 1], nlo, nll, nnl);
+        bounds_async(B, n, tile + 2 * G, s_bnd);
+      }
     }
 
     const unsigned char* hdr = smem + buf * kHdrBytes;
-    const unsigned char* sarg = smem + kArgOff + buf * kArgBufBytes;
+    const unsigned char* sarg = smem + kArgOff + (kArgBufs == 1 ? 0u : buf * kArgBufBytes);
+    if (kArgBufs == 1) mbar_wait(&s_abar, it & 1);
     const StageInfo si = s_info[buf];
     // (claiming one group ahead was measured slower: a warp holding a claimed
     // group lengthens the tail, C4 1.04 -> 0.32 G inst/s)

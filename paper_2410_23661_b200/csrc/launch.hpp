@@ -25,6 +25,7 @@ struct Options {
   int64_t wide_pairs = 1 << 20;  // read x write pairs above which a kernel takes the wide path
   // geometry of the specialised kernel (tuning; k_bucket.cuh)
   int tile = 0, threads = 256, ctas = 2, args_per_rec = 8;  // tile 0: chosen at load (jit.cpp)
+  int arg_bufs = 2;  // argument staging buffers of the pipelined kernel (1: more CTAs per SM)
   bool stride = false;  // stride-aware ranges (row f4): validate through eval_stride (k_stride.cu)
 };
 

@@ -132,6 +132,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "threads") c->opt.threads = (int)v;
   else if (k == "ctas") c->opt.ctas = (int)v;
   else if (k == "args_per_rec") c->opt.args_per_rec = (int)v;
+  else if (k == "arg_bufs") c->opt.arg_bufs = (int)v;
   else if (k == "stride") c->opt.stride = v != 0;
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;

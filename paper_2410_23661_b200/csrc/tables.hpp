@@ -199,8 +199,13 @@ constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
 // staging buffers, s_perm (u32 x 2) and two s_code (u8) per record; the per-key
 // counters are static shared memory.
 constexpr uint32_t kPipeKeys = 64;
-constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec) {
-  return (size_t)2 * tile * 32 + (size_t)2 * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 + 128;
+#ifndef PICKER_ARG_BUFS
+#define PICKER_ARG_BUFS 2
+#endif
+constexpr int kArgBufs = PICKER_ARG_BUFS;  // 1 or 2 argument staging buffers (pipelined kernel)
+constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint32_t arg_bufs = 2) {
+  return (size_t)2 * tile * 32 + (size_t)arg_bufs * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 +
+         128;
 }
 
 // Generic-path limits (a kernel beyond them uses the wide path).
