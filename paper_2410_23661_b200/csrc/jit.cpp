@@ -27,6 +27,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -437,27 +438,48 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
   }
   const uint32_t shape_shortcut = SHAPE_FIRST + (uint32_t)shapes.size();
   // pass 2: a constant position with one value across all kernels of the shape
-  // becomes an immediate again; only the varying positions stay in the table
-  std::vector<std::vector<int>> slot(shapes.size());  // position -> compacted index, -1: immediate
+  // becomes an immediate again; only the varying positions stay in the table.
+  // A kernel's varying constants are packed as int32 words (two for a value
+  // outside int32, low word first) in 16-byte blocks: the shape reads them
+  // with one 128-bit load per 4 words at its start (kv[], registers).
+  std::vector<std::vector<int>> slot(shapes.size());  // position -> int32 word, -1: immediate
+  std::vector<std::vector<char>> wide(shapes.size());  // position needs two words
+  std::vector<int> nwords(shapes.size(), 0);          // per shape, a multiple of 4
   for (size_t s = 0; s < shapes.size(); ++s) {
     const std::vector<int64_t>& k0 = kconst[members[s][0]];
     slot[s].assign(k0.size(), -1);
+    wide[s].assign(k0.size(), 0);
     int q = 0;
     for (size_t p = 0; p < k0.size(); ++p) {
-      bool uniform = true;
-      for (size_t i : members[s]) uniform &= kconst[i][p] == k0[p];
-      if (!uniform) slot[s][p] = q++;
+      bool uniform = true, fits = true;
+      for (size_t i : members[s]) {
+        uniform &= kconst[i][p] == k0[p];
+        fits &= kconst[i][p] >= INT32_MIN && kconst[i][p] <= INT32_MAX;
+      }
+      if (uniform) continue;
+      wide[s][p] = !fits;
+      slot[s][p] = q;
+      q += fits ? 1 : 2;
     }
+    nwords[s] = (q + 3) & ~3;
     std::string& b = shapes[s];
     for (size_t p = k0.size(); p-- > 0;) {
       const std::string tok = "__ldg(K + " + std::to_string(p) + ")";
-      // kept loads are renamed through a marker so later passes cannot match them
-      const std::string rep = slot[s][p] < 0 ? "(" + lit(k0[p]) + ")"
-                                             : "__ldg(K@ + " + std::to_string(slot[s][p]) + ")";
+      const int w = slot[s][p];
+      const std::string rep =
+          w < 0 ? "(" + lit(k0[p]) + ")"
+          : wide[s][p] ? "((int64_t)kv[" + std::to_string(w + 1) + "] << 32 | (uint32_t)kv[" + std::to_string(w) + "])"
+                       : "((int64_t)kv[" + std::to_string(w) + "])";
       for (size_t at = b.find(tok); at != std::string::npos; at = b.find(tok, at + rep.size()))
         b.replace(at, tok.size(), rep);
     }
-    for (size_t at = b.find("K@"); at != std::string::npos; at = b.find("K@", at)) b.erase(at + 1, 1);
+    if (nwords[s]) {  // the loads go first in the body
+      const size_t at = b.find("{\n") + 2;
+      b.insert(at, "  int32_t kv[" + std::to_string(nwords[s]) + "];\n#pragma unroll\n  for (int i = 0; i < " +
+                       std::to_string(nwords[s] / 4) +
+                       "; ++i) {\n    const int4 t = __ldg(reinterpret_cast<const int4*>(K) + i);\n"
+                       "    kv[4 * i] = t.x, kv[4 * i + 1] = t.y, kv[4 * i + 2] = t.z, kv[4 * i + 3] = t.w;\n  }\n");
+    }
   }
   P.meta.resize(ks.size() + 1);
   for (size_t i = 0; i < ks.size(); ++i) {
@@ -470,8 +492,15 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
     } else if (k.path == PATH_JIT) {
       const int s = shape_of[i];
       m.shape = SHAPE_FIRST + (uint32_t)s;
-      for (size_t p = 0; p < kconst[i].size(); ++p)
-        if (slot[s][p] >= 0) P.consts.push_back(kconst[i][p]);
+      if (P.consts.size() & 1) P.consts.push_back(0);  // 16-byte aligned block
+      m.koff = (uint32_t)P.consts.size();
+      std::vector<uint32_t> w(nwords[s], 0);
+      for (size_t p = 0; p < kconst[i].size(); ++p) {
+        if (slot[s][p] < 0) continue;
+        w[slot[s][p]] = (uint32_t)(uint64_t)kconst[i][p];
+        if (wide[s][p]) w[slot[s][p] + 1] = (uint32_t)((uint64_t)kconst[i][p] >> 32);
+      }
+      for (size_t j = 0; j < w.size(); j += 2) P.consts.push_back((int64_t)((uint64_t)w[j + 1] << 32 | w[j]));
     }
     P.meta[i] = m;
   }
