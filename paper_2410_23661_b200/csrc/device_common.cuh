@@ -113,12 +113,14 @@ __device__ __forceinline__ bool launch_limits_ok(const RecVals& X) {
 
 // The same limits on the header fields in 32-bit arithmetic (unsigned
 // wrap-around turns each two-sided range test into one compare).
+// Branch-free (one predicate chain, no early exits); the product can wrap only
+// when a factor is already out of range, which sets `bad` on its own.
 __device__ __forceinline__ bool launch_limits_rec(const picker_rec_t& r) {
   const uint32_t gx = r.grid_x, gy = r.grid_y, gz = r.grid_z;
   const uint32_t bx = r.block_x, by = r.block_y, bz = r.block_z;
-  if (gx - 1u > 2147483646u || gy == 0u || gz == 0u) return false;
-  if (bx - 1u > 1023u || by - 1u > 1023u || bz - 1u > 63u) return false;
-  return bx * by * bz <= (uint32_t)kBlockMaxThreads;  // <= 2^26: no wrap
+  const bool bad = (gx - 1u > 2147483646u) | (gy == 0u) | (gz == 0u) | (bx - 1u > 1023u) | (by - 1u > 1023u) |
+                   (bz - 1u > 63u) | (bx * by * bz > (uint32_t)kBlockMaxThreads);
+  return !bad;
 }
 
 __device__ __forceinline__ int count_bin(uint8_t code) { return code <= 11 ? code : 15; }

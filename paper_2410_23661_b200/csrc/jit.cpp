@@ -526,8 +526,10 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
                                           : "    if (key == " + std::to_string(shape_shortcut) +
                                                 ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, "
                                                 "B.args_hi);\n")
-      << "    if (local ? r.nargs != (kn >> 24) : !args_in_range(r, kn >> 24, B.args_lo, B.args_hi))\n"
-         "      return V_ERR_ARITY;\n"
+      // branch-free: a staged record's arguments lie inside the pool
+      << "    const bool in_pool = local | ((r.arg_off >= B.args_lo) & (r.arg_off <= B.args_hi) &\n"
+         "                                  ((uint64_t)r.nargs <= B.args_hi - r.arg_off));\n"
+         "    if ((r.nargs != (kn >> 24)) | !in_pool) return V_ERR_ARITY;\n"
          "    if (!launch_limits_rec(r)) return V_NI_PRECOND;  // every shape's first check\n"
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n";
