@@ -53,6 +53,11 @@ bool any_jit(const std::vector<IrKernel>& ks) {
   return false;
 }
 
+bool validate_writes_counts(JitModule* jit, const Options& opt, uint64_t n) {
+  if (n == 0 || opt.stride != jit_is_stride(jit)) return false;  // as launch_validate chooses below
+  return jit_small_path(jit, n);
+}
+
 cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options& opt,
                             const DevBatch& b, uint64_t n, uint8_t* flags, uint32_t* bits,
                             unsigned long long* counts, int num_sms, cudaStream_t s,

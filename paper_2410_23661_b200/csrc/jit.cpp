@@ -47,6 +47,7 @@ namespace picker {
 struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
+  cudaKernel_t small_kernel = nullptr;  // k_validate_small: n <= kSmallMax
   size_t smem = 0;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
@@ -377,7 +378,9 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   const char* name_expr = src.find("k_validate_pipe<JitDispatch>") != std::string::npos
                               ? "picker::k_validate_pipe<picker::JitDispatch>"
                               : "picker::k_validate_bucket<picker::JitDispatch>";
+  const char* small_expr = "picker::k_validate_small<picker::JitDispatch>";
   nvrtcAddNameExpression(prog, name_expr);
+  nvrtcAddNameExpression(prog, small_expr);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
                                    "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
   for (auto& d : defines) opts.push_back(d.c_str());
@@ -394,6 +397,9 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   const char* low = nullptr;
   nvrtcGetLoweredName(prog, name_expr, &low);
   lowered = low ? low : "";
+  low = nullptr;
+  nvrtcGetLoweredName(prog, small_expr, &low);
+  lowered += std::string("\n") + (low ? low : "");  // main kernel, small-batch kernel
   size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);
   cubin.assign(n, '\0');
@@ -539,7 +545,10 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
          "template __global__ void " << (shape_shortcut + 1 <= kPipeKeys ? "k_validate_pipe" : "k_validate_bucket")
       << "<JitDispatch>(const __grid_constant__ BucketParams, "
          "const __grid_constant__ DevBatch, uint64_t, "
-         "uint8_t*, uint32_t*, unsigned long long*);\n}  // namespace picker\n";
+         "uint8_t*, uint32_t*, unsigned long long*);\n"
+         "template __global__ void k_validate_small<JitDispatch>(const __grid_constant__ BucketParams, "
+         "const __grid_constant__ DevBatch, uint32_t, uint8_t*, uint32_t*, unsigned long long*);\n"
+         "}  // namespace picker\n";
   P.src = src.str();
   P.nshapes = (int)shapes.size();
   return P;
@@ -566,7 +575,7 @@ std::vector<std::string> geometry_defines(const Options& opt) {
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
                  bool use_cache, std::string& err) {
   const std::vector<std::string> defs = geometry_defines(opt);
-  std::string key = plan.src + "|sm_100a|v3";
+  std::string key = plan.src + "|sm_100a|v4";
   for (auto& d : defs) key += "|" + d;
   const uint64_t h = fnv1a(key);
   char name[64];
@@ -632,7 +641,10 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->threads = opt.threads;
   m->ctas = opt.ctas;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, lowered.c_str());
+  const size_t nl = lowered.find('\n');
+  const std::string main_name = lowered.substr(0, nl), small_name = nl == std::string::npos ? "" : lowered.substr(nl + 1);
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, main_name.c_str());
+  if (e == cudaSuccess && !small_name.empty()) e = cudaLibraryGetKernel(&m->small_kernel, m->lib, small_name.c_str());
   if (e == cudaSuccess) e = cudaMalloc(&m->d_consts, plan.consts.size() * sizeof(int64_t));
   // kernel id -> (bin | shape << 16); bins are positions in `ks`
   uint32_t maxid = 0;
@@ -694,6 +706,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
 
 bool jit_is_stride(const JitModule* m) { return m && m->stride; }
 
+bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
+
 void jit_destroy(JitModule* m) {
   if (!m) return;
   if (m->lib) cudaLibraryUnload(m->lib);
@@ -712,6 +726,11 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
   P.nkeys = m->nkeys;
   P.wide_key = m->stride ? 0xFFFFFFFFu : SHAPE_WIDE;  // stride mode: wide kernels through eval_stride
   P.direct_key = m->shortcut_key;
+  if (jit_small_path(m, n)) {  // one CTA, counts written (no memset needed)
+    uint32_t n32 = (uint32_t)n;
+    void* argv[] = {(void*)&P, (void*)&B, (void*)&n32, (void*)&flags, (void*)&bits, (void*)&counts};
+    return cudaLaunchKernel((const void*)m->small_kernel, dim3(1), dim3(kSmallThreads), argv, 0, s);
+  }
   const uint64_t ntiles = (n + m->tile - 1) / m->tile;
   const uint64_t cap = (uint64_t)num_sms * m->ctas;
   const uint64_t grid = ntiles < cap ? ntiles : cap;

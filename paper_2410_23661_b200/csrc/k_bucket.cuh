@@ -632,6 +632,57 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
 }
 
+// Small batches (n <= kSmallMax, one CTA): one thread per record straight from
+// global memory -- no staging, no sort, no grid-wide atomics.  This is the
+// latency path of a launcher that validates a few launches and waits for the
+// verdicts (the paper's per-launch use); the counts are written,
+// not accumulated, so the caller needs no memset before it.
+template <class Dispatch>
+__global__ void __launch_bounds__(kSmallThreads)
+    k_validate_small(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B, uint32_t n,
+                     uint8_t* __restrict__ flags, uint32_t* __restrict__ bits,
+                     unsigned long long* __restrict__ counts) {
+  __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
+  __syncthreads();
+  for (uint32_t i0 = (uint32_t)tid & ~31u; i0 < n; i0 += kSmallThreads) {
+    const uint32_t i = i0 + lane;
+    const bool valid = i < n;
+    uint32_t code = 0, key = 0xFFFFFFFFu, kb = P.kb_unknown, kn = V_ERR_KERNEL;
+    picker_rec_t r{};
+    if (valid) {
+      r = load_rec(B.rec + i);
+      if (r.kernel_id < P.T.nkernel_slots) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2*>(P.kb_of) + r.kernel_id);
+        kb = v.x, kn = v.y;
+      }
+      key = kb >> 16;
+    }
+    const bool wide = kWidePath && valid && key == P.wide_key;
+    if (kWidePath) {  // K2 records: the whole warp on one record at a time
+      for (unsigned wm = __ballot_sync(0xffffffffu, wide); wm; wm &= wm - 1) {
+        const uint32_t src = (uint32_t)__ffs(wm) - 1;
+        const picker_rec_t rr = load_rec(B.rec + i0 + src);
+        const uint8_t cw = eval_wide_warp(P.T, rr, B.args + rr.arg_off, B.args_lo, B.args_hi, lane);
+        if ((uint32_t)lane == src) code = cw;
+      }
+    }
+    if (valid && key == P.direct_key)  // shortcut / unknown id (not in the pipelined dispatch)
+      code = direct_code(kn, r.nargs, r.arg_off, B.args_lo, B.args_hi);
+    else if (valid && !wide)
+      code = Dispatch::eval(key, kb & 0xFFFFu, kn, false, P, r, B.args + r.arg_off, B);
+    const unsigned idem = __ballot_sync(0xffffffffu, valid && code <= V_IDEM_KERNEL);
+    if (valid) flags[i] = (uint8_t)code;
+    if (bits != nullptr && lane == 0) bits[i0 >> 5] = idem;
+    const int hb = valid ? count_bin((uint8_t)code) : 16;
+    const unsigned same = __match_any_sync(0xffffffffu, hb);
+    if (valid && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
+  }
+  __syncthreads();
+  if (counts && tid < PICKER_NUM_COUNTS) counts[tid] = s_hist[tid];
+}
+
 // Dispatch used by the static library: every bin through the table-driven
 // evaluator (grouping by kernel makes its table reads warp-uniform).
 struct GenericDispatch {

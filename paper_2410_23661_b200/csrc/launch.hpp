@@ -46,6 +46,10 @@ struct JitPlan {
 };
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride);
 bool jit_is_stride(const JitModule* m);
+// The module has the small-batch kernel and n <= kSmallMax (one CTA, counts written).
+bool jit_small_path(const JitModule* m, uint64_t n);
+// launch_validate will take the small-batch kernel (it writes the counts: no memset).
+bool validate_writes_counts(JitModule* jit, const Options& opt, uint64_t n);
 // Fills in the automatic geometry (tile = 0) from the summaries.
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
 // Stable-sort kernels by generated shape so neighbouring bins share code.

@@ -310,13 +310,13 @@ int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, 
   DevGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   c->last_launches = 0;
-  if (counts) {
+  Options o = c->opt;
+  if (o.bucket < 0) o.bucket = c->bucket_auto;
+  if (counts && !validate_writes_counts(c->jit, o, n)) {  // the kernels accumulate
     cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
-  Options o = c->opt;
-  if (o.bucket < 0) o.bucket = c->bucket_auto;
   cudaError_t e = launch_validate(c->P, c->jit, o, db, n, flags, bits,
                                   (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
   if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");

@@ -199,6 +199,8 @@ constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
 // staging buffers, s_perm (u32 x 2) and two s_code (u8) per record; the per-key
 // counters are static shared memory.
 constexpr uint32_t kPipeKeys = 64;
+// Small-batch kernel of the specialised module (k_validate_small): one CTA.
+constexpr uint32_t kSmallMax = 1024, kSmallThreads = 256;
 #ifndef PICKER_ARG_BUFS
 #define PICKER_ARG_BUFS 2
 #endif

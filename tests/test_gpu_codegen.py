@@ -153,3 +153,27 @@ def test_geometries(pk, opt):
     _assert_same(_codes(pk, s, rec, args, **opt), want)
     perm = np.random.default_rng(3).permutation(len(rec))  # arguments out of record order
     _assert_same(_codes(pk, s, rec[perm], args, packed=False, **opt), want[perm])
+
+
+@pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, wide_pairs=4), dict(jit=1, stride=1)], ids=str)
+def test_small_batch_kernel(pk, opt):
+    """n <= 1024 takes the one-CTA small-batch kernel (no staging, counts
+    written instead of accumulated); around its limit the tiled kernel."""
+    s = random_summary(41, n_kernels=30)
+    rec, args = random_records(42, s, 1100, max_threads=256, max_grid=32)
+    want_all = np.array(O.oracle_batch_mp(s, rec, args, O.oracle_interval, stride=bool(opt.get("stride"))),
+                        dtype=np.uint8)
+    p = pk.Picker(0, **opt)
+    p.load(s)
+    for n in (1, 31, 32, 33, 1000, 1024, 1025, 1100):
+        flags, bits, counts = p.validate(rec[:n], args)
+        want = want_all[:n]
+        _assert_same(flags.cpu().numpy(), want)
+        exp_c = np.zeros(16, np.int64)
+        for c in want:
+            exp_c[c if c <= 11 else 15] += 1
+        assert np.array_equal(counts.cpu().numpy(), exp_c), n
+        idem = np.pad((want <= 1).astype(np.uint8), (0, (-n) % 32)).reshape(-1, 32)[:, ::-1]
+        assert np.array_equal(bits.cpu().numpy().view(np.uint32),
+                              np.packbits(idem, axis=1).view(">u4").reshape(-1).astype(np.uint32)), n
+    p.close()
