@@ -147,11 +147,8 @@ __device__ __forceinline__ void stage_hdr(const DevBatch& B, uint64_t n, uint64_
   mbar_arrive_expect_tx(bar, hbytes);
   tma_load_1d(hdr, B.rec + base, hbytes, bar);
 }
-__device__ __forceinline__ void stage_args(const DevBatch& B, int m, const unsigned char* hdr, unsigned char* arg,
-                                           uint64_t* bar, StageInfo* info) {
-  const uint64_t lo = *reinterpret_cast<const uint64_t*>(hdr + 24);
-  const uint64_t last_off = *reinterpret_cast<const uint64_t*>(hdr + 32 * (m - 1) + 24);
-  const uint64_t last_n = *reinterpret_cast<const uint32_t*>(hdr + 32 * (m - 1) + 4);
+__device__ __forceinline__ void stage_args_span(const DevBatch& B, uint64_t lo, uint64_t last_off, uint64_t last_n,
+                                                unsigned char* arg, uint64_t* bar, StageInfo* info) {
   const uint64_t hi = last_off + last_n;
   StageInfo si{lo, hi, 0, 0};
   uint32_t abytes = 0;
@@ -170,6 +167,12 @@ __device__ __forceinline__ void stage_args(const DevBatch& B, int m, const unsig
   *info = si;
   mbar_arrive_expect_tx(bar, abytes);  // 0 bytes: the phase completes at once
   if (abytes) tma_load_1d(arg, src, abytes, bar);
+}
+__device__ __forceinline__ void stage_args(const DevBatch& B, int m, const unsigned char* hdr, unsigned char* arg,
+                                           uint64_t* bar, StageInfo* info) {
+  stage_args_span(B, *reinterpret_cast<const uint64_t*>(hdr + 24),
+                  *reinterpret_cast<const uint64_t*>(hdr + 32 * (m - 1) + 24),
+                  *reinterpret_cast<const uint32_t*>(hdr + 32 * (m - 1) + 4), arg, bar, info);
 }
 
 __device__ __forceinline__ picker_rec_t rec_from_smem(const unsigned char* p) {
@@ -447,6 +450,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     for (int b = 0; b < 2; ++b) {
       if constexpr (kArgBufs == 1) {
         stage_hdr(B, n, blockIdx.x + b * G, smem + b * kHdrBytes, &s_bar[b]);
+        if (b == 0 && (uint64_t)blockIdx.x < ntiles) {
+          // the first tile's arguments: bounds read from global memory, so the
+          // copy overlaps the header copy instead of following it
+          uint64_t lo, ll, nl;
+          bounds(blockIdx.x, lo, ll, nl);
+          stage_args_span(B, lo, ll, nl, smem + kArgOff, &s_abar, &s_info[0]);
+        }
       } else {
         uint64_t lo, ll, nl;
         bounds(blockIdx.x + b * G, lo, ll, nl);
@@ -532,7 +542,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     __syncthreads();  // B_a: eval(t-1) and keys(t) done
     // single argument buffer: free now; fetch this tile's arguments, which
     // the scan / scatter / emit below overlap
-    if (kArgBufs == 1 && tid == 0) stage_args(B, m, smem + buf * kHdrBytes, smem + kArgOff, &s_abar, &s_info[buf]);
+    if (kArgBufs == 1 && tid == 0 && it > 0)
+      stage_args(B, m, smem + buf * kHdrBytes, smem + kArgOff, &s_abar, &s_info[buf]);
     if (it > 0) emit(base - G * kTile, kTile, buf ^ 1);  // tiles before the last are full
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
