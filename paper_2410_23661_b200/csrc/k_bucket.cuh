@@ -1,11 +1,12 @@
 // K1 staged + bucketed validation kernel.
 //
-// One persistent CTA per SM walks tiles of kTile launch records.  Each tile's
-// 32-byte headers and its contiguous argument span are copied global->shared
-// by the TMA engine (cp.async.bulk, completion on an mbarrier), double-
-// buffered so the copy of the next tile overlaps the evaluation of this one:
-// every input byte crosses HBM once, in bulk, and all per-record gathers hit
-// shared memory.
+// Persistent CTAs (kCtasPerSm per SM) walk tiles of kTile launch records.
+// Each tile's 32-byte headers and its contiguous argument span are copied
+// global->shared by the TMA engine (cp.async.bulk, completion on an mbarrier);
+// the headers are double-buffered a tile ahead, the arguments double-buffered
+// or (kArgBufs == 1, the specialised module's default) fetched into one buffer
+// while the previous tile is emitted: every input byte crosses HBM once, in
+// bulk, and all per-record gathers hit shared memory.
 //
 // Inside a tile the records are grouped by `key` before evaluation, so that a
 // warp evaluates up to 32 instances that run the SAME code:
@@ -395,10 +396,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 //   - every warp scans the <= 64 key counters itself (lane l holds keys l and
 //     32 + l) and maps a claimed group index to its key with two ballots;
 //   - the scatter writes {record | bin << 16, kn} per sorted slot, so an
-//     evaluating lane needs one shared load to find its record and kernel.
+//     evaluating lane needs one shared load to find its record and kernel;
+//   - shortcut kernels and unknown ids get their final code in the key pass
+//     (direct_code) and never enter the sort.
 // Per tile t (B = __syncthreads):
-//   B_a | emit(t-1), scan + scatter(t) | B_b | restage (t-1)'s buffer with t+1,
-//   eval(t), keys(t+1)
+//   B_a | [kArgBufs == 1: fetch args(t)] emit(t-1), scan + scatter(t) | B_b |
+//   restage (t-1)'s header buffer with t+1, [wait args(t)] eval(t), keys(t+1)
 template <class Dispatch>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     k_validate_pipe(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B, uint64_t n,
