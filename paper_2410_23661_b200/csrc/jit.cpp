@@ -575,8 +575,12 @@ std::vector<std::string> geometry_defines(const Options& opt) {
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
                  bool use_cache, std::string& err) {
   const std::vector<std::string> defs = geometry_defines(opt);
-  std::string key = plan.src + "|sm_100a|v4";
+  // the key covers the generated source, the geometry AND the embedded
+  // headers (k_bucket.cuh, ...): a library built from changed kernels must not
+  // reuse a module compiled from the old ones
+  std::string key = plan.src + "|sm_100a|v5";
   for (auto& d : defs) key += "|" + d;
+  for (int i = 0; i < kEmbedCount; ++i) key += "|" + std::string(kEmbedNames[i]) + "|" + kEmbedSrc[i];
   const uint64_t h = fnv1a(key);
   char name[64];
   snprintf(name, sizeof(name), "%016llx.cubin", (unsigned long long)h);

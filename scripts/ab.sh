@@ -15,7 +15,7 @@ for spec in "$@"; do
   patch=""
   [[ "$spec" == *:* ]] && patch=${spec#*:}
   dir=/tmp/ab_$name
-  rm -rf "$dir"
+  rm -rf "$dir" /tmp/ab_cache_$name
   mkdir -p "$dir"
   (cd "$ROOT" && tar --exclude=./gpurun_out --exclude=./.git -cf - .) | (cd "$dir" && tar xf -)
   if [ -n "$patch" ]; then
@@ -24,7 +24,8 @@ for spec in "$@"; do
   (cd "$dir" && python -c "import __graft_entry__ as g; g.build()") > "$OUT/ab_build_$name.log" 2>&1 ||
     { echo "$name: build failed" >> "$OUT/ab.txt"; continue; }
   for w in $WL; do
-    (cd "$dir" && timeout 300 python bench.py --workload "$w" --steps 20 --warmup 5 --no-cpu-baseline \
+    # a JIT module cache of its own per variant (variants can share generated source)
+    (cd "$dir" && PICKER_JIT_CACHE=/tmp/ab_cache_$name timeout 300 python bench.py --workload "$w" --steps 20 --warmup 5 --no-cpu-baseline \
        --no-latency --e2e-steps 1 ${AB_OPTS:-}) > "$OUT/ab_${name}_$w.json" 2> "$OUT/ab_${name}_$w.err"
     python - "$OUT/ab_${name}_$w.json" "$name" "$w" >> "$OUT/ab.txt" <<'EOF'
 import json, sys
