@@ -601,9 +601,10 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 // threads, 5 staged argument slots per record, one argument buffer, 4 CTAs/SM
 // (28 warps; profiles/r01_sweep_geometry.txt has the sweep).
 // Many arguments (C4: 33): the argument spans do not fit a staging buffer
-// anyway, so the shared memory goes to 2048-record tiles of headers (512
-// threads, 1 CTA/SM, 1 staged slot per record): 4x more records per shape per
-// tile fill the warps (C4 1.09 -> 1.60 G inst/s, profiles/r01_sweep_geometry.txt).
+// anyway, so the shared memory goes to 2560-record tiles of headers (512
+// threads, 1 CTA/SM, 1 staged slot per record, one argument buffer): more
+// records per shape per tile fill the warps (C4 1.09 -> 2.01 G inst/s,
+// profiles/r01_sweep_geometry.txt).
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   if (opt.tile != 0) return opt;
   double sum = 0;
@@ -618,7 +619,8 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
     // inst/s, C3 25.4 -> 27.4)
     opt.tile = 448, opt.threads = 224, opt.ctas = 4, opt.args_per_rec = 5, opt.arg_bufs = 1;
   } else {
-    opt.tile = 2048, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1;
+    // one argument buffer: its 16 KB go to 2560-record tiles (C4 1.96 -> 2.01 G inst/s)
+    opt.tile = 2560, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1, opt.arg_bufs = 1;
   }
   return opt;
 }
