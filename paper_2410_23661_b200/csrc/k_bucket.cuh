@@ -115,11 +115,15 @@ __device__ __forceinline__ void stage_tile(const DevBatch& B, uint64_t n, uint64
   if (base >= n) return;
   const uint64_t m = min((uint64_t)kTile, n - base);
   const uint32_t hbytes = (uint32_t)(m * sizeof(picker_rec_t));
-  const uint64_t hi = last_off + last_n;
+  // a span longer than the buffer (or running past the pool) is staged up to
+  // the buffer's capacity: the records whose arguments lie in the staged
+  // prefix read shared memory, the rest global memory (their `local` test)
+  const uint64_t hi_all = last_off + last_n;
+  const uint64_t hi = min(min(hi_all, lo + (uint64_t)kArgCap), B.args_hi);
   StageInfo si{lo, hi, 0, 0};
   uint32_t abytes = 0;
   const char* src = nullptr;
-  if (hi > lo && hi - lo <= (uint64_t)kArgCap && lo >= B.args_lo && hi <= B.args_hi) {
+  if (hi_all >= lo && hi > lo && lo >= B.args_lo) {
     const uintptr_t a0 = (uintptr_t)(B.args + lo), a1 = (uintptr_t)(B.args + hi);
     const uintptr_t s0 = a0 & ~(uintptr_t)15, s1 = (a1 + 15) & ~(uintptr_t)15;
     const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
@@ -153,11 +157,15 @@ __device__ __forceinline__ void stage_args(const DevBatch& B, int m, const unsig
   const uint64_t lo = *reinterpret_cast<const uint64_t*>(hdr + 24);
   const uint64_t last_off = *reinterpret_cast<const uint64_t*>(hdr + 32 * (m - 1) + 24);
   const uint64_t last_n = *reinterpret_cast<const uint32_t*>(hdr + 32 * (m - 1) + 4);
-  const uint64_t hi = last_off + last_n;
+  // a span longer than the buffer (or running past the pool) is staged up to
+  // the buffer's capacity: the records whose arguments lie in the staged
+  // prefix read shared memory, the rest global memory (their `local` test)
+  const uint64_t hi_all = last_off + last_n;
+  const uint64_t hi = min(min(hi_all, lo + (uint64_t)kArgCap), B.args_hi);
   StageInfo si{lo, hi, 0, 0};
   uint32_t abytes = 0;
   const char* src = nullptr;
-  if (hi > lo && hi - lo <= (uint64_t)kArgCap && lo >= B.args_lo && hi <= B.args_hi) {
+  if (hi_all >= lo && hi > lo && lo >= B.args_lo) {
     const uintptr_t a0 = (uintptr_t)(B.args + lo), a1 = (uintptr_t)(B.args + hi);
     const uintptr_t s0 = a0 & ~(uintptr_t)15, s1 = (a1 + 15) & ~(uintptr_t)15;
     const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
