@@ -597,8 +597,8 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 }
 
 // tile = 0 (auto, the default): geometry from the loaded COND kernels' mean
-// parameter count.  Few arguments (C2: 3.7, C3: 3.4): 448-record tiles, 224
-// threads, 5 staged argument slots per record, one argument buffer, 4 CTAs/SM
+// parameter count.  Few arguments (C2: 3.7, C3: 3.4): 896-record tiles, 448
+// threads, 5 staged argument slots per record, one argument buffer, 2 CTAs/SM
 // (28 warps; profiles/r01_sweep_geometry.txt has the sweep).
 // Many arguments (C4: 33): the argument spans do not fit a staging buffer
 // anyway, so the shared memory goes to 2560-record tiles of headers (512
@@ -614,10 +614,11 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   const double mean = cnt ? sum / cnt : 4.0;
   if (mean <= 6.0) {
     // one argument buffer (the arguments of a tile are fetched while the
-    // previous tile is emitted and this one scattered) frees the shared memory
-    // for a 4th CTA: 28 warps/SM at 72 registers, no spills (C2 43.8 -> 47.4 G
-    // inst/s, C3 25.4 -> 27.4)
-    opt.tile = 448, opt.threads = 224, opt.ctas = 4, opt.args_per_rec = 5, opt.arg_bufs = 1;
+    // previous tile is emitted and this one scattered) leaves room for 28
+    // warps/SM at 72 registers, no spills: 2 CTAs x 448 threads on 896-record
+    // tiles (fuller groups: C2 49.9-50.4 G inst/s) rather than 4 x 224 on 448
+    // (C2 47.9-48.1, C3 +1.7 %); profiles/r01_sweep_geometry.txt
+    opt.tile = 896, opt.threads = 448, opt.ctas = 2, opt.args_per_rec = 5, opt.arg_bufs = 1;
   } else {
     // one argument buffer: its 16 KB go to 2560-record tiles (C4 1.96 -> 2.01 G inst/s)
     opt.tile = 2560, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1, opt.arg_bufs = 1;
