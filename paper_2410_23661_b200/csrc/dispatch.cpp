@@ -27,6 +27,12 @@ void select_paths(std::vector<IrKernel>& ks, const Options& opt) {
       k.path = PATH_SHORTCUT;
       continue;
     }
+    if (k.never_evaluates) {
+      // empty pre/glob box: every record stops at a check before any address,
+      // which the table-driven evaluator decides (no specialised code is emitted)
+      k.path = PATH_GENERIC;
+      continue;
+    }
     size_t nr = 0, nw = 0, nvars = 0;
     for (auto& d : k.desc) {
       (d.kind == KIND_R ? nr : nw)++;

@@ -360,6 +360,7 @@ void verify_kernel(IrKernel& k) {
     if (box.op[o].lo > box.op[o].hi) {
       k.never_evaluates = true;  // every record fails a check before any address
       k.path = PATH_GENERIC;
+      for (size_t di = 0; di < k.desc.size(); ++di) k.var_sign[di].assign(k.desc[di].vars.size(), 0);
       return;
     }
   auto need = [&](uint8_t o) {

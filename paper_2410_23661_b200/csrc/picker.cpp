@@ -350,7 +350,11 @@ int picker_validate_batch_host(picker_ctx_t* c, const picker_batch_t* b, uint64_
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync");
 
   const bool packed = b->args_packed != 0;
-  const uint64_t CH = 1ULL << 22;  // records per chunk (multiple of 32)
+  // Records per chunk: at most 2^22, balanced over the chunks and a multiple of
+  // 32, so that with more than one chunk none is small enough for the
+  // small-batch kernel, which writes the counts instead of adding to them.
+  const uint64_t nch = (n + (1ULL << 22) - 1) >> 22;
+  const uint64_t CH = nch ? (((n + nch - 1) / nch + 31) & ~31ULL) : 32;
   const int64_t* whole_args = nullptr;
   if (!packed && b->args_len) {
     // no contiguity promise: copy the whole pool once into pipeline 1's buffer

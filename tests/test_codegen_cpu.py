@@ -68,3 +68,19 @@ def test_launch_limits_once_and_packed_constants(pk):
     assert "__ldg(K +" not in src  # no scalar 64-bit constant loads left
     varying = [b for b in bodies.values() if "kv[" in b]
     assert varying and all("reinterpret_cast<const int4*>(K)" in b for b in varying)
+
+
+def test_contradictory_preconditions_compile(pk):
+    """a kernel whose pre/glob box is empty (N in [5, 3])
+    verifies (every record fails a check -> code 7/8 before any address); the
+    generator must route it to the table path instead of emitting specialised
+    code from variable signs it never computed."""
+    k = golden.relu(0)
+    k["pre"] = [p for p in k["pre"] if p["op"] != "N"] + [{"op": "N", "lo": 5, "hi": 3}]
+    s = {"version": 1, "kernels": [k, golden.vector_add(1)]}
+    assert pk.verify_summaries(s)[0] == 2
+    r, msg, src = pk.compile_summaries(s, want_source=True)
+    assert r == 1, msg  # one specialised shape (vectorAdd); relu takes the table path
+    # the same kernel alone (no specialised kernel in the module at all)
+    r, msg, _ = pk.compile_summaries({"version": 1, "kernels": [k]}, want_source=True)
+    assert r == 0, msg
