@@ -172,11 +172,15 @@ int picker_validate_batch_host(picker_ctx_t* ctx, const picker_batch_t* batch, u
  * point (thread, induction and fresh variable) of every active symbolic
  * address and intersects the touched BYTES, so it has no range
  * overestimation (l.1170-1185).  Records with more than
- * max_points_per_instance points, or whose possibly-shared bytes (the hull of
- * the pairwise read/write extent intersections) span more than 2^31 bytes, get
- * code 11.  exact_out[n] and counts_out[16] are device pointers (counts_out
- * nullable).  Intended for small grids.  Unlike the other calls this one is
- * SYNCHRONOUS: it returns after the outputs are written.                     */
+ * max_points_per_instance points (summed over the active symbolic addresses)
+ * get code 11; there is no limit on the address span.  exact_out[n] and
+ * counts_out[16] are device pointers (counts_out nullable); n < 2^32.
+ * Intended for small grids.  Asynchronous on `stream`, like
+ * picker_validate_batch.  The context keeps a device arena for the byte-set
+ * tables (>= 512 MB, 16 B per table entry, up to 2 entries per 64-byte block
+ * a point can write); it grows when max_points needs more (PICKER_ECUDA if
+ * that allocation fails).  PICKER_EINVAL when max_points x (blocks per point
+ * of the widest descriptor) exceeds 2^40.                                    */
 int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                        uint8_t* exact_out, uint64_t* counts_out,
                        uint64_t max_points_per_instance, void* stream);

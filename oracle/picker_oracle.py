@@ -404,15 +404,11 @@ def exact_points(kernels, rec):
     return total
 
 
-EXACT_WINDOW_CAP = 1 << 31  # bytes; the verifier's bitmap limit (reading Q22)
-
-
-def oracle_exact(kernels, rec, cap=1 << 20, window_cap=EXACT_WINDOW_CAP):
+def oracle_exact(kernels, rec, cap=1 << 20):
     """Strawman verdict: per-thread address enumeration and set intersection
-    (Fig. 3).  Code 11 when more than ``cap`` points, or when
-    the bytes a read and a write could share (the hull of the pairwise
-    intersections of their range extents) span more than ``window_cap`` bytes
-    (reading Q22: the verifier's resource limits; the paper's strawman has none)."""
+    (Fig. 3).  Code 11 when the active non-opaque symbolic
+    addresses have more than ``cap`` points in total ("the point
+    count exceeds the cap"; reading Q22)."""
     code, st = _prefix(kernels, rec)
     if code is not None:
         return code
@@ -420,11 +416,6 @@ def oracle_exact(kernels, rec, cap=1 << 20, window_cap=EXACT_WINDOW_CAP):
     if _opaque_rule(active):
         return NI_OPAQUE
     if exact_points(kernels, rec) > cap:
-        return EXACT_SKIPPED
-    ext = [(d["kind"], interval_extent(d, vals, box)) for d, box in active]
-    inter = [(max(r[0], w[0]), min(r[1], w[1])) for kr, r in ext if kr == "R"
-             for kw, w in ext if kw == "W" and r[0] <= w[1] and w[0] <= r[1]]
-    if inter and max(b for _, b in inter) - min(a for a, _ in inter) + 1 > window_cap:
         return EXACT_SKIPPED
     rbytes, wbytes = set(), set()
     for d, box in active:

@@ -547,7 +547,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (it > 0) emit(base - G * kTile, kTile, buf ^ 1);  // tiles before the last are full
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
-    if (tid < (int)kPipeKeys) s_cnt[buf ^ 1][tid] = 0;
+    for (int b = tid; b < (int)kPipeKeys; b += kThreads) s_cnt[buf ^ 1][b] = 0;  // CTAs of < 64 threads too
     if (tid == 0) s_next[buf ^ 1] = kWarps;
     // scan (every warp, registers): lane l holds keys l and 32 + l as
     // count | groups << 16, inclusive

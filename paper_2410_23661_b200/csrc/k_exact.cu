@@ -9,16 +9,23 @@
 // l.1170-1185): comparing it with the range-based verdict measures that
 // conservatism, and checks that the range model never misses an overlap.
 //
-// Two kernels:
+// Kernels (all on `stream`, no host round trip):
 //   X1 (one thread per record): the shared prefix (kernel class, launch limits,
 //      preconditions, global condition, opaque rule), the point count (cap ->
 //      code 11), the range extents.  No pairwise extent intersection => exact 0
-//      (exact sets are subsets of the extents).  Otherwise the record is pending
-//      with the hull of the pairwise intersections as its window (> 2^31 bytes
-//      -> code 11, reading Q22).
-//   X2 (one CTA per pending record): a bitmap over the window in a global
-//      arena; every point of every active write descriptor sets the bits of its
-//      bytes (atomicOr); every point of every active read descriptor tests them.
+//      (exact sets are subsets of the extents).  Otherwise the record is pending:
+//      its window is the hull of the pairwise intersections (only bytes there
+//      can be shared), and it is appended to one of two device lists by the
+//      size of its byte-set table (an atomic counter: on-device compaction).
+//   X2 (persistent; a CTA claims pending records): the written bytes of the
+//      window go into an open-addressing hash table in the CTA's slice of a
+//      global arena -- one entry per touched 64-byte block (key = block index,
+//      value = 64-bit byte mask; atomicCAS on the key, atomicOr on the mask) --
+//      then every read point tests its blocks' masks.  The table is sized from
+//      the write points (<= 2 entries per block), so its size is bounded by the
+//      point cap, not by the window: no window limit (reading Q22).  Records
+//      whose table exceeds a slice of the small pass go to the big pass, whose
+//      slices hold the largest table the point cap allows.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -32,17 +39,21 @@
 namespace picker {
 
 constexpr uint32_t kPending = 0x100;
-constexpr uint64_t kExactWindowCap = 1ULL << 31;  // bytes (oracle: EXACT_WINDOW_CAP)
 constexpr int kExactThreads = 256;
+constexpr unsigned long long kEmptyKey = ~0ULL;
 
 __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t lim) {
   if (a == 0 || b == 0) return 0;
   return a > lim / b ? lim : min(a * b, lim);
 }
 
-// X1: final code, or kPending with the window [wlo, whi] to enumerate.
+// 64-byte blocks one point of `width` bytes can touch
+__device__ __forceinline__ uint64_t blocks_per_point(uint32_t width) { return (width + 63) / 64 + 1; }
+
+// X1: final code, or kPending with the window [wlo, whi] and the number of
+// hash-table blocks the window's written bytes can occupy.
 __device__ uint32_t exact_prefix(const Tables& T, const picker_rec_t r, const int64_t* a, uint64_t alo,
-                                 uint64_t ahi, uint64_t cap, int64_t& wlo, int64_t& whi) {
+                                 uint64_t ahi, uint64_t cap, int64_t& wlo, int64_t& whi, uint64_t& wblocks) {
   const uint32_t kid = r.kernel_id;
   if (kid >= T.nkernel_slots) return V_ERR_KERNEL;
   const DKernel K = T.kernels[kid];
@@ -57,7 +68,7 @@ __device__ uint32_t exact_prefix(const Tables& T, const picker_rec_t r, const in
     if (v < ch.lo || v > ch.hi) return c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
   }
   bool opq_r = false, opq_w = false, act_r = false, act_w = false;
-  uint64_t points = 0;
+  uint64_t points = 0, wpb = 0;  // wpb: write points x blocks per point
   const uint64_t lim = cap + 1;
   for (int di = 0; di < K.ndesc; ++di) {
     const DDesc D = T.descs[K.desc + di];
@@ -75,6 +86,7 @@ __device__ uint32_t exact_prefix(const Tables& T, const picker_rec_t r, const in
       p = sat_mul(p, (uint64_t)(hi - lo) + 1, lim);
     }
     points = min(points + p, lim);
+    if (D.kind == KIND_W) wpb += p * blocks_per_point(D.width);  // p <= cap + 1 (cap checked below)
   }
   if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
   if (points > cap) return V_EXACT_SKIPPED;
@@ -98,117 +110,173 @@ __device__ uint32_t exact_prefix(const Tables& T, const picker_rec_t r, const in
     }
   }
   if (!any) return V_IDEM_CHECKED;
-  if ((uint64_t)(whi - wlo) + 1 > kExactWindowCap) return V_EXACT_SKIPPED;
+  const uint64_t wspan = ((uint64_t)(whi - wlo) >> 6) + 2;  // blocks of the window
+  wblocks = min(wpb, wspan);
   return kPending;
 }
 
-__global__ void k_exact_prefix(Tables T, DevBatch B, uint64_t n, uint64_t cap, uint8_t* __restrict__ out,
-                               uint32_t* __restrict__ status, int64_t* __restrict__ win) {
+// log2 of the table entries for b blocks: load factor <= 1/2, >= 64 entries
+__host__ __device__ __forceinline__ uint32_t table_log2(uint64_t b) {
+  uint32_t l = 6;
+  while ((1ULL << l) < 2 * b) ++l;
+  return l;
+}
+
+struct ExactLists {
+  uint32_t* pend[2];    // pending record indices: small pass, big pass
+  uint32_t* count;      // [0], [1]: list lengths; [2], [3]: claim counters
+};
+
+__global__ void k_exact_prefix(Tables T, DevBatch B, uint64_t n, uint64_t cap, uint32_t small_log2,
+                               uint8_t* __restrict__ out, int64_t* __restrict__ win, uint8_t* __restrict__ tlog,
+                               ExactLists L) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (uint64_t)gridDim.x * blockDim.x) {
     const picker_rec_t r = load_rec(B.rec + i);
     int64_t wlo = 0, whi = -1;
-    const uint32_t st = exact_prefix(T, r, B.args + r.arg_off, B.args_lo, B.args_hi, cap, wlo, whi);
-    status[i] = st;
+    uint64_t wb = 0;
+    const uint32_t st = exact_prefix(T, r, B.args + r.arg_off, B.args_lo, B.args_hi, cap, wlo, whi, wb);
+    out[i] = st == kPending ? 0 : (uint8_t)st;
+    if (st != kPending) continue;
     win[2 * i] = wlo;
     win[2 * i + 1] = whi;
-    out[i] = st == kPending ? 0 : (uint8_t)st;
+    const uint32_t tl = table_log2(wb);
+    tlog[i] = (uint8_t)tl;
+    const int big = tl > small_log2;
+    L.pend[big][atomicAdd(L.count + big, 1u)] = (uint32_t)i;
   }
 }
 
-// X2: one CTA per pending record.  Pass 0 marks the window bytes written,
-// pass 1 tests the bytes read.
-__global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch B, const uint32_t* __restrict__ pend,
+// X2: CTAs claim records of list `which`; each has a slice of 2^slice_log2
+// table entries (keys, then masks).
+__global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch B, ExactLists L, int which,
                                                               const int64_t* __restrict__ win,
-                                                              const uint64_t* __restrict__ woff,
-                                                              uint32_t* __restrict__ arena, uint8_t* __restrict__ out) {
+                                                              const uint8_t* __restrict__ tlog,
+                                                              unsigned long long* __restrict__ arena,
+                                                              uint32_t slice_log2, uint8_t* __restrict__ out) {
   __shared__ int64_t s_lo[16], s_sz[16], s_coef[64], s_base;
   __shared__ uint32_t s_div[64];
   __shared__ uint8_t s_lvar[64], s_op[16], s_src[16];
   __shared__ int64_t s_arg[16];
   __shared__ uint64_t s_npts;
   __shared__ int s_on, s_found, s_nv, s_nt;
-  const uint64_t i = pend[blockIdx.x];
-  const picker_rec_t r = load_rec(B.rec + i);
-  const DKernel K = T.kernels[r.kernel_id];
-  const RecVals X(r, B.args + r.arg_off, K.i32mask);
-  const int64_t wlo = win[2 * i], whi = win[2 * i + 1];
-  const uint64_t L = (uint64_t)(whi - wlo) + 1, nwords = (L + 31) / 32;
-  uint32_t* bm = arena + woff[blockIdx.x];
-  for (uint64_t w = threadIdx.x; w < nwords; w += blockDim.x) bm[w] = 0;
-  if (threadIdx.x == 0) s_found = 0;
-  __syncthreads();
-  for (int pass = 0; pass < 2; ++pass) {
-    const uint8_t kind = pass == 0 ? KIND_W : KIND_R;
-    for (int di = 0; di < K.ndesc; ++di) {
-      const DDesc D = T.descs[K.desc + di];
-      if (D.kind != kind || D.opaque) continue;
-      if (threadIdx.x == 0) {
-        s_on = desc_active(T, K, D, X);
-        uint64_t np = 1;
-        for (int v = 0; v < D.nvar; ++v) {
-          int64_t lo, hi;
-          slot_bounds(T, K, X, T.varlist[D.var + v], lo, hi);
-          const DVarDef vd = T.vardef[D.var + v];
-          s_lo[v] = lo;
-          s_sz[v] = hi - lo + 1;
-          s_op[v] = vd.op;
-          s_src[v] = vd.src;
-          s_arg[v] = vd.arg;
-          if (vd.op == 0) np *= (uint64_t)(hi - lo + 1);  // bounded by the point cap (X1)
+  __shared__ uint32_t s_claim;
+  unsigned long long* keys = arena + ((uint64_t)blockIdx.x << (slice_log2 + 1));
+  unsigned long long* masks = keys + (1ULL << slice_log2);
+  const uint32_t npend = L.count[which];
+  for (;;) {
+    if (threadIdx.x == 0) s_claim = atomicAdd(L.count + 2 + which, 1u);
+    __syncthreads();
+    const uint32_t c = s_claim;
+    if (c >= npend) return;
+    const uint64_t i = L.pend[which][c];
+    const picker_rec_t r = load_rec(B.rec + i);
+    const DKernel K = T.kernels[r.kernel_id];
+    const RecVals X(r, B.args + r.arg_off, K.i32mask);
+    const int64_t wlo = win[2 * i], whi = win[2 * i + 1];
+    const uint32_t tl = tlog[i];
+    const uint64_t tmask = (1ULL << tl) - 1;
+    for (uint64_t e = threadIdx.x; e <= tmask; e += blockDim.x) keys[e] = kEmptyKey, masks[e] = 0;
+    if (threadIdx.x == 0) s_found = 0;
+    __syncthreads();
+    for (int pass = 0; pass < 2; ++pass) {
+      const uint8_t kind = pass == 0 ? KIND_W : KIND_R;
+      for (int di = 0; di < K.ndesc; ++di) {
+        const DDesc D = T.descs[K.desc + di];
+        if (D.kind != kind || D.opaque) continue;
+        if (threadIdx.x == 0) {
+          s_on = desc_active(T, K, D, X);
+          uint64_t np = 1;
+          for (int v = 0; v < D.nvar; ++v) {
+            int64_t lo, hi;
+            slot_bounds(T, K, X, T.varlist[D.var + v], lo, hi);
+            const DVarDef vd = T.vardef[D.var + v];
+            s_lo[v] = lo;
+            s_sz[v] = hi - lo + 1;
+            s_op[v] = vd.op;
+            s_src[v] = vd.src;
+            s_arg[v] = vd.arg;
+            if (vd.op == 0) np *= (uint64_t)(hi - lo + 1);  // bounded by the point cap (X1)
+          }
+          s_npts = np;
+          s_nv = D.nvar;
+          s_nt = D.nterm;
+          s_base = D.base == OPD_NONE ? 0 : X.get(D.base);
+          for (int t = 0; t < D.nterm; ++t) {
+            const DTerm tm = T.terms[D.term + t];
+            s_coef[t] = prod_val(T, K, X, tm.prod);
+            s_div[t] = tm.div;
+            s_lvar[t] = T.term_lvar[D.term + t];
+          }
         }
-        s_npts = np;
-        s_nv = D.nvar;
-        s_nt = D.nterm;
-        s_base = D.base == OPD_NONE ? 0 : X.get(D.base);
-        for (int t = 0; t < D.nterm; ++t) {
-          const DTerm tm = T.terms[D.term + t];
-          s_coef[t] = prod_val(T, K, X, tm.prod);
-          s_div[t] = tm.div;
-          s_lvar[t] = T.term_lvar[D.term + t];
-        }
-      }
-      __syncthreads();
-      if (s_on) {
-        const volatile int* found = &s_found;
-        for (uint64_t p = threadIdx.x; p < s_npts && !(pass == 1 && *found); p += blockDim.x) {
-          int64_t x[16];
-          uint64_t q = p;
-          for (int v = 0; v < s_nv; ++v)
-            if (s_op[v] == 0) {
-              const uint64_t sz = (uint64_t)s_sz[v];
-              x[v] = s_lo[v] + (int64_t)(q % sz);
-              q /= sz;
-            }
-          for (int v = 0; v < s_nv; ++v)
-            if (s_op[v] != 0) {
-              const int64_t src = x[s_src[v]], m = s_arg[v];
-              if (s_op[v] == DEF_OP_MOD) {
-                int64_t md = src % m;
-                x[v] = md < 0 ? md + m : md;  // floor modulo (Python %)
-              } else {
-                x[v] = src & m;
+        __syncthreads();
+        if (s_on) {
+          const volatile int* found = &s_found;
+          for (uint64_t p = threadIdx.x; p < s_npts && !(pass == 1 && *found); p += blockDim.x) {
+            int64_t x[16];
+            uint64_t q = p;
+            for (int v = 0; v < s_nv; ++v)
+              if (s_op[v] == 0) {
+                const uint64_t sz = (uint64_t)s_sz[v];
+                x[v] = s_lo[v] + (int64_t)(q % sz);
+                q /= sz;
               }
-            }
-          int64_t addr = s_base;
-          for (int t = 0; t < s_nt; ++t)
-            addr = add64(addr, s_lvar[t] == 0xFF ? s_coef[t] : mul64(s_coef[t], floordiv64(x[s_lvar[t]], s_div[t])));
-          const int64_t b0 = max64(addr, wlo), b1 = min64(add64(addr, (int64_t)D.width - 1), whi);
-          for (int64_t b = b0; b <= b1; ++b) {
-            const uint64_t off = (uint64_t)(b - wlo);
-            if (pass == 0) {
-              atomicOr(bm + (off >> 5), 1u << (off & 31));
-            } else if ((bm[off >> 5] >> (off & 31)) & 1u) {
-              s_found = 1;
-              break;
+            for (int v = 0; v < s_nv; ++v)
+              if (s_op[v] != 0) {
+                const int64_t src = x[s_src[v]], m = s_arg[v];
+                if (s_op[v] == DEF_OP_MOD) {
+                  int64_t md = src % m;
+                  x[v] = md < 0 ? md + m : md;  // floor modulo (Python %)
+                } else {
+                  x[v] = src & m;
+                }
+              }
+            int64_t addr = s_base;
+            for (int t = 0; t < s_nt; ++t)
+              addr = add64(addr, s_lvar[t] == 0xFF ? s_coef[t] : mul64(s_coef[t], floordiv64(x[s_lvar[t]], s_div[t])));
+            // bytes [b0, b1] of the window, as offsets from wlo
+            const int64_t b0 = max64(addr, wlo), b1 = min64(add64(addr, (int64_t)D.width - 1), whi);
+            if (b0 > b1) continue;
+            const uint64_t o0 = (uint64_t)(b0 - wlo), o1 = (uint64_t)(b1 - wlo);
+            for (uint64_t blk = o0 >> 6; blk <= (o1 >> 6); ++blk) {
+              const uint32_t s0 = blk == (o0 >> 6) ? (uint32_t)(o0 & 63) : 0;
+              const uint32_t s1 = blk == (o1 >> 6) ? (uint32_t)(o1 & 63) : 63;
+              const unsigned long long m = (~0ULL >> (63 - s1)) & (~0ULL << s0);
+              uint64_t h = (blk * 0x9E3779B97F4A7C15ULL) >> (64 - tl);
+              if (pass == 0) {
+                for (;;) {
+                  const unsigned long long k = atomicCAS(keys + h, kEmptyKey, (unsigned long long)blk);
+                  if (k == kEmptyKey || k == blk) {
+                    atomicOr(masks + h, m);
+                    break;
+                  }
+                  h = (h + 1) & tmask;
+                }
+              } else {
+                bool hit = false;
+                for (;;) {
+                  const unsigned long long k = keys[h];
+                  if (k == kEmptyKey) break;
+                  if (k == blk) {
+                    hit = (masks[h] & m) != 0;
+                    break;
+                  }
+                  h = (h + 1) & tmask;
+                }
+                if (hit) {
+                  s_found = 1;
+                  break;
+                }
+              }
             }
           }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
+    if (threadIdx.x == 0) out[i] = s_found ? V_NI_OVERLAP : V_IDEM_CHECKED;
+    __syncthreads();  // s_claim, the slice and s_found are reused
   }
-  if (threadIdx.x == 0) out[i] = s_found ? V_NI_OVERLAP : V_IDEM_CHECKED;
 }
 
 __global__ void k_histogram(const uint8_t* __restrict__ codes, uint64_t n, unsigned long long* counts) {
@@ -222,78 +290,71 @@ __global__ void k_histogram(const uint8_t* __restrict__ codes, uint64_t n, unsig
 }
 
 cudaError_t launch_exact(const Tables& T, const DevBatch& b, uint64_t n, uint8_t* out,
-                         unsigned long long* counts, uint64_t cap, int num_sms, cudaStream_t s, int* launches,
-                         std::string& err) {
+                         unsigned long long* counts, uint64_t cap, uint32_t max_width, void** arena,
+                         size_t* arena_bytes, int num_sms, cudaStream_t s, int* launches, std::string& err) {
   *launches = 0;
   if (n == 0) return cudaSuccess;
-  uint32_t* status = nullptr;
+  if (n >= (1ULL << 32)) {
+    err = "more than 2^32 - 1 records";
+    return cudaErrorInvalidValue;
+  }
+  // the largest table a record can need: every write point within the cap,
+  // each touching blocks_per_point(max width) blocks
+  const uint64_t bpp = (max_width + 63) / 64 + 1;
+  if (cap > (1ULL << 40) / bpp) {
+    err = "max_points too large for the byte-set tables";
+    return cudaErrorInvalidValue;
+  }
+  const uint32_t big_log2 = table_log2(std::max<uint64_t>(cap * bpp, 1));
+  const size_t big_bytes = (size_t)16 << big_log2;
+  const size_t want = std::max<size_t>(big_bytes, (size_t)512 << 20);
+  if (*arena_bytes < want) {
+    if (*arena) cudaFree(*arena);
+    *arena = nullptr;
+    *arena_bytes = 0;
+    cudaError_t e = cudaMalloc(arena, want);
+    if (e != cudaSuccess) {
+      err = "byte-set arena (" + std::to_string(want >> 20) + " MB)";
+      return e;
+    }
+    *arena_bytes = want;
+  }
+  const uint64_t entries = *arena_bytes / 16;
+  const uint32_t grid_small = (uint32_t)num_sms * 2;
+  uint32_t small_log2 = 6;
+  while ((2ULL << small_log2) * grid_small <= entries) ++small_log2;
+  small_log2 = std::min(small_log2, big_log2);
+  const uint32_t grid_big = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(entries >> big_log2, num_sms));
+
+  // scratch: windows, table sizes, two pending lists, 4 counters
   int64_t* win = nullptr;
-  cudaError_t e = cudaMallocAsync(&status, n * sizeof(uint32_t), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&win, 2 * n * sizeof(int64_t), s);
+  uint8_t* tl = nullptr;
+  uint32_t* lists = nullptr;
+  cudaError_t e = cudaMallocAsync(&win, 2 * n * sizeof(int64_t), s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&tl, n, s);
+  if (e == cudaSuccess) e = cudaMallocAsync(&lists, (2 * n + 4) * sizeof(uint32_t), s);
+  if (e == cudaSuccess) e = cudaMemsetAsync(lists + 2 * n, 0, 4 * sizeof(uint32_t), s);
   if (e != cudaSuccess) {
     err = "scratch allocation";
     return e;
   }
+  ExactLists L{{lists, lists + n}, lists + 2 * n};
   const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 8);
-  k_exact_prefix<<<(unsigned)blocks, 256, 0, s>>>(T, b, n, cap, out, status, win);
-  ++*launches;
-  std::vector<uint32_t> st(n);
-  std::vector<int64_t> w(2 * n);
-  e = cudaMemcpyAsync(st.data(), status, n * sizeof(uint32_t), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaMemcpyAsync(w.data(), win, 2 * n * sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) {
-    err = "X1 / D2H";
-    return e;
-  }
-  // batches of pending records whose bitmaps fit the arena
-  const uint64_t arena_words = 1ULL << 26;  // 256 MB
-  uint32_t* arena = nullptr;
-  std::vector<uint32_t> pend;
-  std::vector<uint64_t> off;
-  uint64_t used = 0;
-  uint32_t* d_pend = nullptr;
-  uint64_t* d_off = nullptr;
-  auto flush = [&]() -> cudaError_t {
-    if (pend.empty()) return cudaSuccess;
-    cudaError_t ee = cudaSuccess;
-    if (!arena) ee = cudaMallocAsync(&arena, arena_words * 4, s);
-    if (!d_pend && ee == cudaSuccess) ee = cudaMallocAsync(&d_pend, n * sizeof(uint32_t), s);
-    if (!d_off && ee == cudaSuccess) ee = cudaMallocAsync(&d_off, n * sizeof(uint64_t), s);
-    if (ee == cudaSuccess)
-      ee = cudaMemcpyAsync(d_pend, pend.data(), pend.size() * 4, cudaMemcpyHostToDevice, s);
-    if (ee == cudaSuccess)
-      ee = cudaMemcpyAsync(d_off, off.data(), off.size() * 8, cudaMemcpyHostToDevice, s);
-    if (ee != cudaSuccess) return ee;
-    k_exact_enum<<<(unsigned)pend.size(), kExactThreads, 0, s>>>(T, b, d_pend, win, d_off, arena, out);
-    ++*launches;
-    ee = cudaStreamSynchronize(s);  // pend/off host vectors are reused
-    pend.clear();
-    off.clear();
-    used = 0;
-    return ee;
-  };
-  for (uint64_t i = 0; i < n && e == cudaSuccess; ++i) {
-    if (st[i] != kPending) continue;
-    const uint64_t words = ((uint64_t)(w[2 * i + 1] - w[2 * i]) + 1 + 31) / 32;
-    if (used + words > arena_words) e = flush();
-    pend.push_back((uint32_t)i);
-    off.push_back(used);
-    used += (words + 31) & ~31ULL;
-  }
-  if (e == cudaSuccess) e = flush();
-  if (e == cudaSuccess && counts) {
+  k_exact_prefix<<<(unsigned)blocks, 256, 0, s>>>(T, b, n, cap, small_log2, out, win, tl, L);
+  k_exact_enum<<<grid_small, kExactThreads, 0, s>>>(T, b, L, 0, win, tl, (unsigned long long*)*arena, small_log2,
+                                                    out);
+  k_exact_enum<<<grid_big, kExactThreads, 0, s>>>(T, b, L, 1, win, tl, (unsigned long long*)*arena, big_log2, out);
+  *launches = 3;
+  if (counts) {
     k_histogram<<<(unsigned)std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 4), 256, 0, s>>>(out, n, counts);
     ++*launches;
   }
-  cudaFreeAsync(status, s);
   cudaFreeAsync(win, s);
-  if (arena) cudaFreeAsync(arena, s);
-  if (d_pend) cudaFreeAsync(d_pend, s);
-  if (d_off) cudaFreeAsync(d_off, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess && err.empty()) err = "X2";
-  return e == cudaSuccess ? cudaGetLastError() : e;
+  cudaFreeAsync(tl, s);
+  cudaFreeAsync(lists, s);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) err = "exact kernels";
+  return e;
 }
 
 }  // namespace picker

@@ -69,8 +69,11 @@ cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const 
                           const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,
                           int num_sms, cudaStream_t s);
 
+// Exact verifier (k_exact.cu).  `arena` / `arena_bytes`: the byte-set table
+// arena, owned by the caller's context and grown here when max_points needs it.
 cudaError_t launch_exact(const Tables& T, const DevBatch& b, uint64_t n, uint8_t* out,
-                         unsigned long long* counts, uint64_t max_points, int num_sms,
-                         cudaStream_t s, int* launches, std::string& err);
+                         unsigned long long* counts, uint64_t max_points, uint32_t max_width,
+                         void** arena, size_t* arena_bytes, int num_sms, cudaStream_t s, int* launches,
+                         std::string& err);
 
 }  // namespace picker

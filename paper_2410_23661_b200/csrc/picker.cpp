@@ -30,6 +30,9 @@ struct picker_ctx {
   size_t stage_bytes[2] = {0, 0};
   unsigned long long* dev_counts = nullptr;
   cudaStream_t aux = nullptr;
+  void* exact_arena = nullptr;  // byte-set tables of the exact verifier
+  size_t exact_arena_bytes = 0;
+  uint32_t max_width = 1;       // widest descriptor of the loaded summaries
   int last_launches = 0;
   bool bucket_auto = false;  // table-driven grouping when opt.bucket = -1 (launch.hpp)
 };
@@ -112,6 +115,7 @@ void picker_destroy(picker_ctx_t* c) {
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->exact_arena) cudaFree(c->exact_arena);
     jit_destroy(c->jit);
   }
   delete c;
@@ -188,6 +192,9 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->jit = jm;
   c->dev_tables = dev;
   c->dev_tables_bytes = blob.size();
+  c->max_width = 1;
+  for (auto& k : ks)
+    for (auto& d : k.desc) c->max_width = std::max<uint32_t>(c->max_width, (uint32_t)d.width);
   uint8_t* b = (uint8_t*)dev;
   c->P.T.kernels = (const DKernel*)(b + o_k);
   c->P.T.nkernel_slots = (uint32_t)ht.kernels.size();
@@ -471,6 +478,9 @@ int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uin
                        uint64_t* counts, uint64_t max_points, void* stream) {
   int st = check_batch(c, b, n, out);
   if (st) return st;
+  if (n >= (1ULL << 32)) return fail(c, PICKER_EINVAL, "exact check: n must be < 2^32");
+  if (max_points > (1ULL << 40) / ((c->max_width + 63) / 64 + 1))
+    return fail(c, PICKER_EINVAL, "exact check: max_points too large for the byte-set tables");
   DevGuard g(c->device);
   cudaStream_t s = (cudaStream_t)stream;
   if (counts) {
@@ -479,8 +489,8 @@ int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uin
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
   std::string err;
-  cudaError_t e = launch_exact(c->P.T, db, n, out, (unsigned long long*)counts, max_points,
-                               c->num_sms, s, &c->last_launches, err);
+  cudaError_t e = launch_exact(c->P.T, db, n, out, (unsigned long long*)counts, max_points, c->max_width,
+                               &c->exact_arena, &c->exact_arena_bytes, c->num_sms, s, &c->last_launches, err);
   if (e != cudaSuccess) return cuda_fail(c, e, ("exact check: " + err).c_str());
   return PICKER_OK;
 }

@@ -33,7 +33,7 @@ def test_exports_every_declared_symbol(pk):
 
 def test_golden_verifies(pk):
     n, msg = pk.verify_summaries(golden.golden_summary())
-    assert n == 9, msg
+    assert n == 10, msg
 
 
 @pytest.mark.parametrize("seed", range(6))

@@ -178,6 +178,57 @@ def test_exact_random(pk, seed):
     assert not ((inter == 0) & (got == 10)).any()
 
 
+def test_exact_cap_boundary_and_far_windows(pk):
+    """Code 11 at the point-cap boundary (1,536 points: cap 1,535 -> 11, cap
+    1,536 -> verdict), and accesses 2^36 bytes apart whose shared window spans
+    ~3 x 2^36 bytes (the byte-set tables hold only touched 64-byte blocks)."""
+    from test_oracle_pins import far_stride_summary
+    s = golden.golden_summary()
+    b = RecordBuilder()
+    b.add(0, [0x1000, 0x2000, 0x3000], (4,), (128,))
+    b.add(0, [0x1000, 0x2000, 0x1000], (4,), (128,))
+    rec, args = b.build()
+    p = _make(pk, s)
+    for cap, want in [(1535, [11, 11]), (1536, [0, 10])]:
+        out, _ = p.exact_check(rec, args, max_points=cap)
+        assert out.cpu().numpy().tolist() == want
+        assert _oracle_codes(s, rec, args, O.oracle_exact, cap=cap).tolist() == want
+    s = far_stride_summary()
+    b = RecordBuilder()
+    for off in range(0, 9):
+        for S in (1 << 36, 1 << 40, 64, 8, 4):
+            b.add(0, [1 << 44, S, off], (1,), (4,))
+            b.add(0, [1 << 44, S, off], (1,), (1024,))
+    rec, args = b.build()
+    want = _oracle_codes(s, rec, args, O.oracle_exact)
+    p = _make(pk, s)
+    out, _ = p.exact_check(rec, args)
+    assert np.array_equal(out.cpu().numpy(), want)
+    assert (want == 0).sum() > 0 and (want == 10).sum() > 0
+
+
+def test_exact_big_tables(pk):
+    """Records whose written blocks exceed a CTA slice of the small pass
+    (65,536 threads writing every 64th byte: > 2^16 table entries) take the
+    big pass; with and without a shared byte."""
+    t = {"gidx.x": {"lo": [], "hi": []}}
+    k = golden.kernel(
+        0, "spread", [("A", "ptr"), ("S", "i64"), ("off", "i64")],
+        [golden.desc("R", 4, "A", [golden.term(1, ["S"], "gidx.x")], t),
+         golden.desc("W", 4, "A", [golden.term(1, ["S"], "gidx.x"), golden.term(1, ["off"])], t)],
+        pre=golden.ptr_pre("A") + [{"op": "S", "lo": 0, "hi": 1 << 20}, {"op": "off", "lo": 0, "hi": 1 << 30}])
+    s = {"version": 1, "kernels": [k]}
+    b = RecordBuilder()
+    for S, off in [(64, 4), (64, 3), (128, 64), (128, 128), (64, 64 * 65535 + 4), (64, 64 * 65535)]:
+        b.add(0, [1 << 40, S, off], (64,), (1024,))
+    rec, args = b.build()
+    want = _oracle_codes(s, rec, args, O.oracle_exact)
+    assert want.tolist() == [0, 10, 0, 10, 0, 10]
+    p = _make(pk, s)
+    out, _ = p.exact_check(rec, args)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
 # ---- C4: cuDNN-like kernels with 16-48 pointer arguments ------------------------
 
 @pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, force_path=3), dict(jit=0, force_path=3),

@@ -148,3 +148,26 @@ def test_host_call_many_chunks(pk, c2):
     flags, bits, counts = p.validate_host(rec_h, args_h)
     p.close()
     _check(flags.numpy(), bits, counts, np.tile(want, R)[:n])
+
+
+@pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=0, bucket=1)], ids=str)
+def test_contradictory_preconditions(pk, opt):
+    """a kernel whose precondition box is empty loads and
+    every one of its records is code 7, next to a kernel
+    on the specialised path."""
+    from tracegen import golden
+    from tracegen.records import RecordBuilder
+    k = golden.relu(0)
+    k["pre"] = [p for p in k["pre"] if p["op"] != "N"] + [{"op": "N", "lo": 5, "hi": 3}]
+    s = {"version": 1, "kernels": [k, golden.vector_add(1)]}
+    b = RecordBuilder()
+    for i in range(3000):
+        if i % 3:
+            b.add(0, (0x10000, 0x20000, 16 + i % 20), grid=(4,), block=(32,))
+        else:
+            b.add(1, (0x1000, 0x2000, 0x3000 if i % 2 else 0x1000), grid=(4,), block=(128,))
+    rec, args = b.build()
+    want = np.array(O.oracle_batch(s, rec, args), np.uint8)
+    assert set(want[1::3]) == {7}
+    flags, bits, counts = _run(pk, s, rec, args, **opt)
+    _check(flags, bits, counts, want)

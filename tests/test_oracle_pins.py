@@ -270,3 +270,45 @@ def test_i32_sign_extension(G):
     assert O.oracle_interval(G, r) == 0
     r = _rec(3, [65536, 131072, 0xFFFFFFFF], (4, 1, 1), (32, 1, 1))  # N = -1 < 0
     assert O.oracle_interval(G, r) == 7
+
+
+# ---- exact verifier: point cap (code 11) and far-apart accesses ------------------
+# Code 11 is "the point count exceeds the cap" (reading Q22); there is
+# no limit on the span of the addresses.
+
+def test_exact_point_cap_boundary(G):
+    """vectorAdd, gdim 4 x bdim 128: 3 symbolic addresses x 512 threads = 1,536
+    points (every thread of every symbolic address)."""
+    r = _rec(0, [0x1000, 0x2000, 0x3000], (4, 1, 1), (128, 1, 1))
+    assert O.exact_points(G, r) == 1536
+    assert O.oracle_exact(G, r, cap=1535) == O.EXACT_SKIPPED
+    assert O.oracle_exact(G, r, cap=1536) == O.IDEM_CHECKED
+    r = _rec(0, [0x1000, 0x2000, 0x1000], (4, 1, 1), (128, 1, 1))  # C aliases A
+    assert O.oracle_exact(G, r, cap=1535) == O.EXACT_SKIPPED
+    assert O.oracle_exact(G, r, cap=1536) == O.NI_OVERLAP
+    # the opaque rule is decided before any point is counted (§8C order)
+    r = _rec(9, [0x1000, 0x2000, 1, 1], (1, 1, 1), (32, 1, 1))
+    assert O.oracle_exact(G, r, cap=0) == O.NI_OPAQUE
+
+
+def far_stride_summary():
+    """k(int* A, long S, long off): v = A[S*tid/4]; A[(S*tid + off)/4] = v
+    (byte addresses A + S*tid and A + S*tid + off, 4 bytes each)."""
+    t = {"tid.x": {"lo": [], "hi": []}}
+    return {"version": 1, "kernels": [golden.kernel(
+        0, "far_stride", [("A", "ptr"), ("S", "i64"), ("off", "i64")],
+        [golden.desc("R", 4, "A", [golden.term(1, ["S"], "tid.x")], t),
+         golden.desc("W", 4, "A", [golden.term(1, ["S"], "tid.x"), golden.term(1, ["off"])], t)],
+        pre=golden.ptr_pre("A") + [{"op": "S", "lo": 0, "hi": 1 << 40}, {"op": "off", "lo": 0, "hi": 64}])]}
+
+
+@pytest.mark.parametrize("off,exact", [(4, O.IDEM_CHECKED), (2, O.NI_OVERLAP), (0, O.NI_OVERLAP)])
+def test_exact_far_apart_accesses(off, exact):
+    """S = 2^36, bdim 4: reads {A + k S .. + 3}, writes {A + k S + off .. + 3},
+    k = 0..3.  The range extents [A, A + 3 S + 3] and [A + off, A + 3 S + off + 3]
+    overlap (interval 10); the byte sets share bytes only
+    when off < 4 (l.717-730).  The shared window spans ~3 x 2^36 bytes."""
+    K = O.index_summary(far_stride_summary())
+    r = _rec(0, [1 << 44, 1 << 36, off], (1, 1, 1), (4, 1, 1))
+    assert O.oracle_interval(K, r) == O.NI_OVERLAP
+    assert O.oracle_exact(K, r) == exact

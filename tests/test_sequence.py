@@ -88,3 +88,74 @@ def test_gpu_sequence_parity(window, concurrent):
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
     assert len(set(want.tolist())) > 2
+
+
+# Opaque windows (reading Q23 with the opaque rule of PAPER.md l.761-765).
+# Kernel 9 (opaque_io): rflag 1 = plain read src+4*tid, 2 = opaque read;
+# wflag 1 = opaque write, 2 = plain write out+4*tid.  bdim 32: 128-byte extents.
+def _io(out, src, rflag, wflag):
+    return (9, [out, src, rflag, wflag], (1, 1, 1), (32, 1, 1))
+
+
+def test_opaque_write_after_a_read():
+    """Instance 0 reads src, instance 1 writes through an opaque address: the
+    write may clobber the earlier input (j=1 >= i=0) -> 9 in both modes."""
+    r = _recs([_io(0x10000, 0x20000, 1, 0), _io(0x30000, 0x40000, 0, 1)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.NI_OPAQUE
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OPAQUE
+
+
+def test_opaque_write_before_a_read():
+    """The opaque write comes first: a later read sees the written value (RAW),
+    no input of the list is clobbered -> 0 sequential; concurrent -> 9."""
+    r = _recs([_io(0x30000, 0x40000, 0, 1), _io(0x10000, 0x20000, 1, 0)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.IDEM_CHECKED
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OPAQUE
+
+
+def test_opaque_read_before_a_write():
+    """Instance 0 reads through an opaque address, instance 1 writes out: the
+    write may clobber what was read -> 9 in both modes."""
+    r = _recs([_io(0x10000, 0x20000, 2, 0), _io(0x30000, 0x40000, 0, 2)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.NI_OPAQUE
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OPAQUE
+
+
+def test_opaque_read_after_a_write():
+    """The plain write comes first, the opaque read after it -> 0 sequential
+    (RAW); concurrent -> 9."""
+    r = _recs([_io(0x30000, 0x40000, 0, 2), _io(0x10000, 0x20000, 2, 0)])
+    assert O.oracle_sequence(G, r, O.SEQ_SEQUENTIAL) == O.IDEM_CHECKED
+    assert O.oracle_sequence(G, r, O.SEQ_CONCURRENT) == O.NI_OPAQUE
+
+
+def test_opaque_inside_one_instance():
+    """One instance with an opaque write and a plain read is 9 as a window of
+    one, as it is alone (test golden 'opaque write with an active read')."""
+    r = _recs([_io(0x10000, 0x20000, 1, 1)])
+    for m in (O.SEQ_SEQUENTIAL, O.SEQ_CONCURRENT):
+        assert O.oracle_sequence(G, r, m) == O.NI_OPAQUE
+    r = _recs([_io(0x10000, 0x20000, 0, 1), _io(0x50000, 0x60000, 0, 1)])  # writes only
+    for m in (O.SEQ_SEQUENTIAL, O.SEQ_CONCURRENT):
+        assert O.oracle_sequence(G, r, m) == O.IDEM_CHECKED
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_gpu_sequence_golden_opaque(concurrent):
+    """The hand-derived opaque windows above, through picker_validate_sequence."""
+    import paper_2410_23661_b200 as pk
+    rows = [_io(0x10000, 0x20000, 1, 0), _io(0x30000, 0x40000, 0, 1),
+            _io(0x30000, 0x40000, 0, 1), _io(0x10000, 0x20000, 1, 0),
+            _io(0x10000, 0x20000, 2, 0), _io(0x30000, 0x40000, 0, 2),
+            _io(0x30000, 0x40000, 0, 2), _io(0x10000, 0x20000, 2, 0),
+            _io(0x10000, 0x20000, 0, 1), _io(0x50000, 0x60000, 0, 1)]
+    want = [9, 9, 9, 9, 0] if concurrent else [9, 0, 9, 0, 0]
+    b = RecordBuilder()
+    for kid, a, grid, block in rows:
+        b.add(kid, a, grid=grid, block=block)
+    rec, args = b.build()
+    p = pk.Picker(0)
+    p.load(golden.golden_summary())
+    got = p.validate_sequence(rec, args, 2, concurrent=concurrent).cpu().numpy()
+    assert got.tolist() == want

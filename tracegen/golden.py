@@ -15,6 +15,9 @@ Kernels (ids are fixed so golden record files can refer to them):
   6 modfresh   PAPER.md l.990-992: A+tid%10 -> A+v, v in [0,9]
   7 opaque_na  PAPER.md l.755-765, 1149-1159: an address read from memory
   8 atomic     PAPER.md l.771-773: contains an atomic -> NONIDEM (ATOMIC)
+  9 opaque_io  PAPER.md l.755-765, 1486-1491: opaque reads AND writes (an offset
+               from __constant__ memory, the NA type (3)), each under its own
+               runtime-checkable guard, next to plain reads and writes
 """
 from __future__ import annotations
 
@@ -144,6 +147,27 @@ def opaque_na(kid=7):
     )
 
 
+def opaque_io(kid=9):
+    # __constant__ int c_off;   (a non-parameter variable, PAPER.md l.1489-1491 type (3))
+    # k(int* out, const int* src, int rflag, int wflag) {
+    #   int v = 0;
+    #   if (rflag == 1) v = src[tid];            // R src + 4*tid
+    #   if (rflag == 2) v = src[c_off + tid];    // R opaque
+    #   if (wflag == 1) out[c_off + tid] = v;    // W opaque
+    #   if (wflag == 2) out[tid] = v;            // W out + 4*tid
+    # }
+    t = {"tid.x": {"lo": [], "hi": []}}
+    i32 = {"lo": -(1 << 31), "hi": (1 << 31) - 1}
+    return kernel(
+        kid, "opaque_io", [("out", "ptr"), ("src", "ptr"), ("rflag", "i32"), ("wflag", "i32")],
+        [desc("R", 4, "src", [term(4, (), "tid.x")], t, guard=[{"a": "rflag", "cmp": "==", "b": 1}]),
+         desc("R", 4, None, [], t, opaque=True, guard=[{"a": "rflag", "cmp": "==", "b": 2}]),
+         desc("W", 4, None, [], t, opaque=True, guard=[{"a": "wflag", "cmp": "==", "b": 1}]),
+         desc("W", 4, "out", [term(4, (), "tid.x")], t, guard=[{"a": "wflag", "cmp": "==", "b": 2}])],
+        pre=ptr_pre("out", "src") + [dict(op="rflag", **i32), dict(op="wflag", **i32)],
+    )
+
+
 def atomic_k(kid=8):
     return kernel(kid, "atomicHist", [("H", "ptr")],
                   [desc("W", 4, "H", [term(4, (), "gidx.x")], GIDX)],
@@ -154,7 +178,7 @@ def golden_summary():
     return {
         "version": 1,
         "kernels": [vector_add(), vector_set(), vector_inc(), relu(), stride_ro(),
-                    tighten(), modfresh(), opaque_na(), atomic_k()],
+                    tighten(), modfresh(), opaque_na(), atomic_k(), opaque_io()],
     }
 
 
