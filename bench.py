@@ -71,13 +71,16 @@ WORKLOADS = {
            "C3 TVM-style tiled GEMM/conv kernels with affine strided ranges (64 kernels, 16,384-record base)"),
     "c4": (dict(n=1 << 13, n_kernels=32), 512,
            "C4 cuDNN-like kernels with 16-48 pointer args (32 kernels, 8,192-record base)"),
+    "wide": (dict(n=1 << 12, n_kernels=16), 128,
+             "wide family: multi-tensor-apply kernels with 150-300 symbolic addresses, > 4096 read x write "
+             "pairs each, K2 sort + sweep path (16 kernels, 4,096-record base)"),
 }
 
 
 def make_base(workload):
     from tracegen import workloads as W
     kw = WORKLOADS[workload][0]
-    return {"c2": W.make_c2, "c3": W.make_c3, "c4": W.make_c4}[workload](**kw)
+    return {"c2": W.make_c2, "c3": W.make_c3, "c4": W.make_c4, "wide": W.make_wide}[workload](**kw)
 
 
 def workload_config(args, world, n_base=None, flush=False):
@@ -88,7 +91,7 @@ def workload_config(args, world, n_base=None, flush=False):
                     + (" (C5 stream)" if world > 1 and args.workload == "c2" else ""),
         "records_per_gpu": n_base * args.replicas,
         "records_total": n_base * args.replicas * world,
-        "seed": {"c2": 23661, "c3": 23662, "c4": 23663}[args.workload],
+        "seed": {"c2": 23661, "c3": 23662, "c4": 23663, "wide": 23665}[args.workload],
         "l2": "L2 flushed (512 MB write) before every timed step" if flush
               else "inputs > 6x the 126 MB L2 per GPU, no flush needed",
         "parallelism": f"dp{world} (instance shards, all-gather of flag bits)" if world > 1 else "single GPU",

@@ -72,20 +72,31 @@ static __device__ void desc_extent(const Tables& T, const DKernel& K, const DDes
 
 // ---------------------------------------------------------------------------
 // K2: one warp evaluates one instance with many read/write sites (SURVEY §2.5:
-// cuDNN-like kernels with 16+ pointer arguments).  Lanes compute descriptor
-// extents in parallel; the read/write test is a sweep-line over the extents
-// sorted by lower bound: an extent overlaps an extent of the other kind iff,
-// in lb order, the running maximum ub of the other kind seen so far reaches
-// its lb (closed byte intervals; equal lbs overlap in any order).  Up to
-// 2 x 32 extents are sorted in registers by a warp bitonic network; records
-// with more active extents fall back to lanes over all read x write pairs.
+// cuDNN-like / multi-tensor kernels with 16+ pointer arguments).  Lanes
+// compute descriptor extents in parallel; the read/write test is a sweep-line
+// over the extents sorted by lower bound: an extent overlaps an extent of the
+// other kind iff, in lb order, the running maximum ub of the other kind seen
+// so far reaches its lb (closed byte intervals; equal lbs overlap in any
+// order).  Kernels with <= 64 descriptors sort 2 x 32 extents in registers (a
+// warp bitonic network); larger ones (<= kWideMax) write one element per
+// descriptor into the warp's scratch (global memory, L1/L2-resident), sort it
+// there with the same network (lanes over compare-exchange pairs, __syncwarp
+// between stages) and sweep it 32 elements at a time with carried maxima.
 // The verdict equals the pairwise definition -- checked
-// against the oracle (tests, wide path forced).
+// against the oracle (tests: wide families, wide path forced).
 // ---------------------------------------------------------------------------
 struct Ext {
   int64_t lb, ub;
   uint32_t kind;  // 0 read, 1 write, 2 none (padding)
 };
+// scratch element: 32 bytes, two 16-byte halves
+struct __align__(16) WideElem {
+  int64_t lb, ub;
+  uint32_t kind, pad0;
+  uint64_t pad1;
+};
+static_assert(sizeof(WideElem) == kWideElemBytes, "scratch element layout");
+
 
 static __device__ __forceinline__ Ext shfl_ext(const Ext& e, int src) {
   Ext o;
@@ -201,9 +212,49 @@ static __device__ bool desc_active_extent(const Tables& T, const DKernel& K, con
   return true;
 }
 
+static __device__ __forceinline__ bool elem_less(const WideElem& a, const WideElem& b) {
+  return a.kind != 2 && (b.kind == 2 || a.lb < b.lb);
+}
+
+// Bitonic sort of the warp's scratch [0, np2) (np2 a power of two >= 64).
+static __device__ void scratch_sort(WideElem* e, uint32_t np2, int lane) {
+  for (uint32_t k = 2; k <= np2; k <<= 1) {
+    for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+      // pair p: i = p with bit j inserted as 0, partner i | j
+      for (uint32_t p = lane; p < np2 / 2; p += 32) {
+        const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1)), q = i | j;
+        const WideElem a = e[i], b = e[q];
+        const bool asc = (i & k) == 0;
+        if (asc ? elem_less(b, a) : elem_less(a, b)) e[i] = b, e[q] = a;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Sweep of the sorted scratch [0, np2): exclusive prefix max of ub per kind.
+static __device__ bool scratch_sweep(const WideElem* e, uint32_t np2, int lane) {
+  const int64_t NEG = (-9223372036854775807LL - 1);
+  int64_t carry_r = NEG, carry_w = NEG;
+  for (uint32_t h = 0; h < np2; h += 32) {
+    const WideElem x = e[h + lane];
+    if (__all_sync(0xffffffffu, x.kind == 2)) break;  // padding sorts last
+    const int64_t vr = x.kind == 0 ? x.ub : NEG, vw = x.kind == 1 ? x.ub : NEG;
+    const int64_t ir = max64(warp_incl_max(vr, lane), carry_r), iw = max64(warp_incl_max(vw, lane), carry_w);
+    int64_t xr = __shfl_up_sync(0xffffffffu, ir, 1), xw = __shfl_up_sync(0xffffffffu, iw, 1);
+    if (lane == 0) xr = carry_r, xw = carry_w;
+    const bool hit = (x.kind == 0 && xw >= x.lb) || (x.kind == 1 && xr >= x.lb);
+    if (__any_sync(0xffffffffu, hit)) return true;
+    carry_r = __shfl_sync(0xffffffffu, ir, 31);
+    carry_w = __shfl_sync(0xffffffffu, iw, 31);
+  }
+  return false;
+}
+
 // Verdict of one record, computed by the whole warp (all lanes return it).
+// `scratch`: this warp's kWideMax elements (nullptr: pairwise for > 64).
 static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r, const int64_t* a,
-                                         uint64_t alo, uint64_t ahi, int lane) {
+                                         uint64_t alo, uint64_t ahi, int lane, WideElem* scratch) {
   // prefix (Fig. 3 order); the preconditions / global condition are split over
   // the lanes: the first failing check in order decides (pre before glob)
   const uint32_t kid = r.kernel_id;
@@ -226,36 +277,52 @@ static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r,
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) first_fail = min(first_fail, __shfl_xor_sync(0xffffffffu, first_fail, d));
   if (first_fail != 0x7FFFFFFF) return first_fail < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
-  // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags, extents
+  // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags,
+  // extents (registers for <= 64 descriptors, else element d of the scratch)
+  const bool in_regs = K.ndesc <= 64;
+  const bool in_scratch = !in_regs && scratch != nullptr && K.ndesc <= kWideMax;
+  const uint32_t np2 = in_scratch ? max(64u, 1u << (32 - __clz((uint32_t)K.ndesc - 1))) : 0u;
   bool act_r = false, act_w = false, opq_r = false, opq_w = false;
-  int nact = 0;
   Ext e[2];
   e[0].kind = e[1].kind = 2;
   e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
-  for (int d = lane; d < K.ndesc; d += 32) {
-    const DDesc D = T.descs[K.desc + d];
-    int64_t lb = 0, ub = 0;
-    if (!desc_active_extent(T, K, D, X, lb, ub)) continue;
-    (D.kind == KIND_R ? act_r : act_w) = true;
-    if (D.opaque) {
-      (D.kind == KIND_R ? opq_r : opq_w) = true;
-      continue;
+  for (int d = lane, k = 0; d < (in_scratch ? (int)np2 : K.ndesc); d += 32, ++k) {
+    WideElem x{0, 0, 2, 0, 0};
+    if (d < K.ndesc) {
+      const DDesc D = T.descs[K.desc + d];
+      int64_t lb = 0, ub = 0;
+      if (desc_active_extent(T, K, D, X, lb, ub)) {
+        (D.kind == KIND_R ? act_r : act_w) = true;
+        if (D.opaque)
+          (D.kind == KIND_R ? opq_r : opq_w) = true;
+        else
+          x = WideElem{lb, ub, D.kind == KIND_R ? 0u : 1u, 0, 0};
+      }
     }
-    if (nact < 2) e[nact].lb = lb, e[nact].ub = ub, e[nact].kind = D.kind == KIND_R ? 0 : 1;
-    ++nact;
+    if (in_scratch) {
+      scratch[d] = x;
+    } else if (k < 2) {
+      e[k].lb = x.lb, e[k].ub = x.ub, e[k].kind = x.kind;
+    }
   }
   act_r = __any_sync(0xffffffffu, act_r);
   act_w = __any_sync(0xffffffffu, act_w);
   opq_r = __any_sync(0xffffffffu, opq_r);
   opq_w = __any_sync(0xffffffffu, opq_w);
   if ((opq_r && act_w) || (opq_w && act_r)) return V_NI_OPAQUE;
-  if (!__any_sync(0xffffffffu, nact > 2)) {
-    // <= 64 active extents in total (<= 2 per lane, kept above): sort + sweep;
+  if (in_regs) {
     // element index of e[0] is lane, of e[1] is 32 + lane
     warp_sort64(e[0], e[1], lane);
     return sweep64(e[0], e[1], lane) ? V_NI_OVERLAP : V_IDEM_CHECKED;
   }
-  // many active extents: lanes over all (read, write) descriptor pairs
+  if (in_scratch) {
+    __syncwarp();
+    scratch_sort(scratch, np2, lane);
+    const bool hit = scratch_sweep(scratch, np2, lane);
+    __syncwarp();  // the scratch is reused by the warp's next record
+    return hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
+  }
+  // beyond the scratch: lanes over all (read, write) descriptor pairs
   const int nd = K.ndesc;
   bool hit = false;
   for (int p = lane; p < nd * nd && !__any_sync(__activemask(), hit); p += 32) {

@@ -713,6 +713,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
 
 bool jit_is_stride(const JitModule* m) { return m && m->stride; }
 
+int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 : 0; }
+
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
 
 void jit_destroy(JitModule* m) {

@@ -197,6 +197,12 @@ __device__ __forceinline__ picker_rec_t rec_from_smem(const unsigned char* p) {
   return r;
 }
 
+// The K2 scratch of warp `warp` of this CTA (blockDim.x / 32 warps per CTA).
+__device__ __forceinline__ WideElem* wide_scratch(const BucketParams& P, int warp) {
+  if (P.wide_scratch == nullptr) return nullptr;
+  return reinterpret_cast<WideElem*>(P.wide_scratch) + ((uint64_t)blockIdx.x * (blockDim.x >> 5) + warp) * kWideMax;
+}
+
 // Lane 0 claims the next work item; the index is broadcast to the warp.
 __device__ __forceinline__ uint32_t warp_claim(uint32_t* counter) {
   uint32_t g = 0;
@@ -347,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                              (uint64_t)r.nargs <= si.hi - r.arg_off;
           const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
                                    : B.args + r.arg_off;
-          const uint8_t c = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+          const uint8_t c = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane, wide_scratch(P, warp));
           if (lane == 0) s_code[wi] = c;
         }
         continue;
@@ -609,7 +615,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                              (uint64_t)r.nargs <= si.hi - r.arg_off;
           const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
                                    : B.args + r.arg_off;
-          const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane);
+          const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane, wide_scratch(P, warp));
           if (lane == 0) s_code[buf * kTile + wi] = cw;
         }
         continue;
@@ -675,7 +681,8 @@ __global__ void __launch_bounds__(kSmallThreads)
       for (unsigned wm = __ballot_sync(0xffffffffu, wide); wm; wm &= wm - 1) {
         const uint32_t src = (uint32_t)__ffs(wm) - 1;
         const picker_rec_t rr = load_rec(B.rec + i0 + src);
-        const uint8_t cw = eval_wide_warp(P.T, rr, B.args + rr.arg_off, B.args_lo, B.args_hi, lane);
+        const uint8_t cw = eval_wide_warp(P.T, rr, B.args + rr.arg_off, B.args_lo, B.args_hi, lane,
+                                          wide_scratch(P, tid >> 5));
         if ((uint32_t)lane == src) code = cw;
       }
     }

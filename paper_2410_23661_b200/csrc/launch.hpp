@@ -46,6 +46,8 @@ struct JitPlan {
 };
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride);
 bool jit_is_stride(const JitModule* m);
+// Warps per SM of the specialised module's persistent kernel (CTAs x threads / 32).
+int jit_warps_per_sm(const JitModule* m);
 // The module has the small-batch kernel and n <= kSmallMax (one CTA, counts written).
 bool jit_small_path(const JitModule* m, uint64_t n);
 // launch_validate will take the small-batch kernel (it writes the counts: no memset).

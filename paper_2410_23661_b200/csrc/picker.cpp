@@ -30,6 +30,8 @@ struct picker_ctx {
   size_t stage_bytes[2] = {0, 0};
   unsigned long long* dev_counts = nullptr;
   cudaStream_t aux = nullptr;
+  void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
+  size_t wide_scratch_bytes = 0;
   void* exact_arena = nullptr;  // byte-set tables of the exact verifier
   size_t exact_arena_bytes = 0;
   uint32_t max_width = 1;       // widest descriptor of the loaded summaries
@@ -116,6 +118,7 @@ void picker_destroy(picker_ctx_t* c) {
     if (c->dev_counts) cudaFree(c->dev_counts);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->exact_arena) cudaFree(c->exact_arena);
+    if (c->wide_scratch) cudaFree(c->wide_scratch);
     jit_destroy(c->jit);
   }
   delete c;
@@ -187,6 +190,27 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
       return fail(c, PICKER_ECUDA, "JIT: " + jerr);
     }
   }
+  // K2 scratch for kernels with more than 64 descriptors on the wide path:
+  // one slice per warp of the largest persistent grid (or the small kernel)
+  size_t scratch_bytes = 0;
+  for (auto& k : ks)
+    if (k.path == PATH_WIDE && k.desc.size() > 64) {
+      const int wps = std::max({kCtasPerSm * kWarps, jit_warps_per_sm(jm), (int)(kSmallThreads / 32)});
+      scratch_bytes = (size_t)c->num_sms * wps * kWideMax * kWideElemBytes;
+      break;
+    }
+  if (scratch_bytes > c->wide_scratch_bytes) {
+    if (c->wide_scratch) cudaFree(c->wide_scratch);
+    c->wide_scratch = nullptr;
+    c->wide_scratch_bytes = 0;
+    if (cudaMalloc(&c->wide_scratch, scratch_bytes) != cudaSuccess) {
+      cudaFree(dev);
+      jit_destroy(jm);
+      return fail(c, PICKER_ENOMEM, "cudaMalloc(wide scratch) failed");
+    }
+    c->wide_scratch_bytes = scratch_bytes;
+  }
+  c->P.wide_scratch = scratch_bytes ? c->wide_scratch : nullptr;
   if (c->dev_tables) cudaFree(c->dev_tables);
   jit_destroy(c->jit);
   c->jit = jm;

@@ -158,6 +158,7 @@ struct BucketParams {
   const struct KbEntry* kb_of;  // [T.nkernel_slots]: per kernel id, see KbEntry
   uint32_t kb_unknown;          // kb of an id that is not loaded
   const int64_t* jit_consts;   // per-kernel constants (specialised module only)
+  void* wide_scratch;          // K2: kWideMax 32-byte elements per warp of the grid (desc_eval.cuh)
   uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
   uint32_t direct_key;         // key whose code is final in the key pass (KbEntry.kn = direct
                                // code, see direct_code); 0xFFFFFFFF: none
@@ -209,6 +210,11 @@ constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint3
   return (size_t)2 * tile * 32 + (size_t)arg_bufs * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 +
          128;
 }
+
+// K2 scratch (desc_eval.cuh): descriptors per kernel sorted in the warp's
+// scratch, and the bytes of one element.
+constexpr int kWideMax = 1024;
+constexpr int kWideElemBytes = 32;
 
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind

@@ -403,6 +403,56 @@ def t_cudnn_like(rng, *, nptr=None):
     return ("cudnn_like", params, descs, pre, []), sample
 
 
+def t_multi_tensor(rng, *, kind=None, ntensor=None):
+    """Multi-tensor-apply kernels (fused optimizers, foreach ops, multi-tensor
+    norms): one launch touches T tensors of a parameter list, each through its
+    own pointer argument (sizes shared by groups of 4 tensors), so the summary
+    has 150-300 symbolic addresses and |R| x |W| > 4096 -- the wide (K2) path
+    of SURVEY §8 row a8.  (<= 192 parameters per kernel, the loader's limit.)
+      foreach_binary: o_i = a_i op b_i        (R a_i, R b_i, W o_i; T 48-56)
+      adam_fused:     p, m, v updated in place (R p g m v, W p m v; T 24-44)
+      l2norm:         ws[i] = |x_i|            (R x_i, W ws + 8 i; T 80-150)"""
+    kind = kind or rng_pick(rng, ["foreach_binary"] * 6 + ["l2norm"] * 3 + ["adam_fused"] * 1)
+    T = ntensor or int({"foreach_binary": rng.integers(48, 57), "adam_fused": rng.integers(24, 45),
+                        "l2norm": rng.integers(80, 151)}[kind])
+    ins, outs = {"foreach_binary": (["a", "b"], ["o"]), "adam_fused": (["p", "g", "m", "v"], ["p", "m", "v"]),
+                 "l2norm": (["x"], [])}[kind]
+    names = sorted(set(ins + outs), key=(ins + outs).index)
+    ns = (T + 3) // 4
+    params = [(f"{l}{i}", "ptr") for l in names for i in range(T)] + [(f"n{j}", "i64") for j in range(ns)]
+    if kind == "l2norm":
+        params.append(("ws", "ptr"))
+    descs = []
+    for i in range(T):
+        v = {"ind0": {"lo": [bx(0)], "hi": [bx(-1, (1, [f"n{i // 4}"]))]}}
+        for l in ins:
+            descs.append(desc("R", 4, f"{l}{i}", [term(4, (), "ind0")], v))
+        for l in outs:
+            descs.append(desc("W", 4, f"{l}{i}", [term(4, (), "ind0")], v))
+        if kind == "l2norm":
+            descs.append(desc("W", 8, "ws", [term(8 * i)], {}))
+    ptrs = [p for p, k in params if k == "ptr"]
+    pre = ptr_pre(ptrs) + [{"op": f"n{j}", "lo": 0, "hi": 1 << 28} for j in range(ns)]
+    groups = []  # parameter groups the kernel is launched on (a training loop repeats them)
+
+    def sample(rng, st):
+        if len(groups) < 3 and (not groups or rng.random() < 0.3):
+            n = [int(2 ** rng.uniform(8, 20)) for _ in range(ns)]
+            bufs = {p: st.alloc.buf(8 * T if p == "ws" else 4 * n[int(p[1:]) // 4]) for p in ptrs}
+            groups.append((n, bufs))
+        n, bufs = groups[int(rng.integers(0, len(groups)))]
+        pv = dict(bufs)
+        if outs and st.alias(rng):
+            # an output tensor aliases an input tensor of the list (in-place use)
+            pv[f"{outs[0]}{int(rng.integers(0, T))}"] = pv[f"{ins[-1]}{int(rng.integers(0, T))}"]
+        if kind == "l2norm" and st.alias(rng):
+            pv["ws"] = pv[f"x{int(rng.integers(0, T))}"]  # workspace inside a read tensor
+        args = [pv[p] for p in ptrs if p != "ws"] + n + ([pv["ws"]] if kind == "l2norm" else [])
+        return args, (int(rng_pick(rng, [64, 148, 296, 592])), 1, 1), (512, 1, 1)
+
+    return (f"mt_{kind}", params, descs, pre, []), sample
+
+
 def t_shortcut(rng, cls, reason=None):
     """Kernel-level I / NI kernels: memset-like writes; the
     validator returns their class without computing."""
@@ -572,6 +622,30 @@ def make_c4(seed=23663, n=1 << 12, n_kernels=32):
         ks.append(_finish(kid, f"{nm}{kid}", p, d, pre, gl))
         smps.append(smp)
     st = ProgState(rng, alloc, dict(p_alias=0.01, ni_share=0, p_opaque_on=0), 512)
+    b = RecordBuilder()
+    ptr_mask = []
+    for i in range(n):
+        j = int(rng.integers(0, n_kernels))
+        args, grid, block = smps[j](rng, st)
+        b.add(j, args, grid=grid, block=block)
+        ptr_mask.extend(p["kind"] == "ptr" for p in ks[j]["params"])
+    rec, args = b.build()
+    return {"version": 1, "kernels": ks}, rec, args, {"ptr_mask": np.array(ptr_mask, bool)}
+
+
+def make_wide(seed=23665, n=1 << 12, n_kernels=16):
+    """Wide family ("instances with many pointer arguments"):
+    multi-tensor-apply kernels with 80-400 symbolic addresses, all beyond 4096
+    read x write pairs (auto-routed to the K2 sort + sweep path); ~5 % of the
+    launches alias an output (or the workspace) to an input tensor."""
+    rng = np.random.default_rng(seed)
+    alloc = Alloc(rng)
+    ks, smps = [], []
+    for kid in range(n_kernels):
+        (nm, p, d, pre, gl), smp = t_multi_tensor(rng)
+        ks.append(_finish(kid, f"{nm}{kid}", p, d, pre, gl))
+        smps.append(smp)
+    st = ProgState(rng, alloc, dict(p_alias=0.05, ni_share=0, p_opaque_on=0), 512)
     b = RecordBuilder()
     ptr_mask = []
     for i in range(n):
