@@ -69,7 +69,7 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches) {
   if (n == 0) return cudaSuccess;
-  *launches += 1;
+  *launches += jit && opt.stride == jit_is_stride(jit) ? jit_launch_count(jit, n) : 1;
   // stride mode: the specialised module if it was built stride-aware (option
   // set before picker_load_summaries), else the table-driven evaluator
   if (opt.stride && !jit_is_stride(jit)) return launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);

@@ -57,6 +57,13 @@ struct JitModule {
   int nshapes = 0;
   int tile = 0, threads = 0, ctas = 0;
   bool stride = false;  // built with stride-aware shapes (row f4)
+  // shape-sorted schedule (k_sorted.cuh): S1 keys, S2 scan, S3 scatter,
+  // S4 validate, S5 emit; its scratch grows with the largest batch seen
+  cudaKernel_t sk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  int sort_warps = 0;
+  size_t sort_smem = 0;
+  void* sort_buf = nullptr;
+  size_t sort_cap = 0;  // records the scratch holds
 };
 
 namespace {
@@ -381,6 +388,12 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   const char* small_expr = "picker::k_validate_small<picker::JitDispatch>";
   nvrtcAddNameExpression(prog, name_expr);
   nvrtcAddNameExpression(prog, small_expr);
+  // the shape-sorted schedule's kernels (k_sorted.cuh), when the module has them
+  const bool sorted = src.find("k_validate_sorted<JitDispatch>") != std::string::npos;
+  const char* sort_exprs[] = {"picker::k_sort_keys", "picker::k_sort_scan", "picker::k_sort_scatter",
+                              "picker::k_validate_sorted<picker::JitDispatch>", "picker::k_sort_emit"};
+  if (sorted)
+    for (const char* e : sort_exprs) nvrtcAddNameExpression(prog, e);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
                                    "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
   for (auto& d : defines) opts.push_back(d.c_str());
@@ -400,6 +413,12 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   low = nullptr;
   nvrtcGetLoweredName(prog, small_expr, &low);
   lowered += std::string("\n") + (low ? low : "");  // main kernel, small-batch kernel
+  if (sorted)
+    for (const char* e : sort_exprs) {  // then the sorted schedule's five kernels
+      low = nullptr;
+      nvrtcGetLoweredName(prog, e, &low);
+      lowered += std::string("\n") + (low ? low : "");
+    }
   size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);
   cubin.assign(n, '\0');
@@ -410,7 +429,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
   JitPlan P;
   std::ostringstream src;
   // paths no kernel of this summary takes are left out of the module (code size)
@@ -423,6 +442,8 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
          "typedef unsigned char uint8_t; typedef unsigned short uint16_t; typedef unsigned int uint32_t;\n"
          "typedef unsigned long long uint64_t; typedef unsigned long size_t; typedef unsigned long uintptr_t;\n"
          "#include \"eval_generic.cuh\"\n#include \"eval_stride.cuh\"\n#include \"k_bucket.cuh\"\n"
+      << (sorted ? "#include \"k_sorted.cuh\"\n" : "")
+      << ""
          "namespace picker {\n";
   // pass 1: body text with every constant as a load, grouped into shapes
   std::map<std::string, uint32_t> shape_id;
@@ -548,6 +569,11 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride) {
          "uint8_t*, uint32_t*, unsigned long long*);\n"
          "template __global__ void k_validate_small<JitDispatch>(const __grid_constant__ BucketParams, "
          "const __grid_constant__ DevBatch, uint32_t, uint8_t*, uint32_t*, unsigned long long*);\n"
+      << (sorted && shape_shortcut + 1 <= kPipeKeys
+              ? "template __global__ void k_validate_sorted<JitDispatch>(const __grid_constant__ BucketParams, "
+                "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
+              : "")
+      << ""
          "}  // namespace picker\n";
   P.src = src.str();
   P.nshapes = (int)shapes.size();
@@ -569,7 +595,9 @@ std::vector<std::string> geometry_defines(const Options& opt) {
   return {"-DPICKER_TILE=" + std::to_string(opt.tile), "-DPICKER_THREADS=" + std::to_string(opt.threads),
           "-DPICKER_CTAS=" + std::to_string(opt.ctas),
           "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
-          "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs)};
+          "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
+          "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
+          "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot))};
 }
 
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
@@ -606,12 +634,23 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
 // records per shape per tile fill the warps (C4 1.09 -> 2.01 G inst/s,
 // profiles/r01_sweep_geometry.txt).
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
-  if (opt.tile != 0) return opt;
   double sum = 0;
   int cnt = 0;
+  size_t maxargs = 0;
   for (auto& k : ks)
-    if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC) sum += k.param_names.size(), ++cnt;
+    if (k.path == PATH_JIT || k.path == PATH_WIDE || k.path == PATH_GENERIC)
+      sum += k.param_names.size(), ++cnt, maxargs = std::max(maxargs, k.param_names.size());
   const double mean = cnt ? sum / cnt : 4.0;
+  // shape-sorted schedule (k_sorted.cuh) for many-argument summaries: one
+  // argument slot per lane (the 16-byte-rounded span of up to 62 arguments;
+  // longer records read global memory), as many warps as ~200 KB of slots hold
+  if (opt.sorted < 0) opt.sorted = mean > 6.0 && !opt.stride;
+  if (opt.sorted) {
+    const int slot = (int)((std::min<size_t>(std::max<size_t>(maxargs, 1), 62) * 8 + 16 + 15) / 16 * 16);
+    opt.sort_slot = slot;
+    opt.sort_warps = std::max(1, std::min(16, (200 * 1024) / (32 * slot)));
+  }
+  if (opt.tile != 0) return opt;
   if (mean <= 6.0) {
     // one argument buffer (the arguments of a tile are fetched while the
     // previous tile is emitted and this one scattered) leaves room for 28
@@ -634,7 +673,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeys && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
     return nullptr;
@@ -648,10 +687,22 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->threads = opt.threads;
   m->ctas = opt.ctas;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
-  const size_t nl = lowered.find('\n');
-  const std::string main_name = lowered.substr(0, nl), small_name = nl == std::string::npos ? "" : lowered.substr(nl + 1);
-  if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, main_name.c_str());
-  if (e == cudaSuccess && !small_name.empty()) e = cudaLibraryGetKernel(&m->small_kernel, m->lib, small_name.c_str());
+  std::vector<std::string> names;  // main, small, [the sorted schedule's five]
+  for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
+    b = lowered.find('\n', a);
+    if (b == std::string::npos) b = lowered.size();
+    names.push_back(lowered.substr(a, b - a));
+  }
+  if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, names[0].c_str());
+  if (e == cudaSuccess && names.size() > 1 && !names[1].empty())
+    e = cudaLibraryGetKernel(&m->small_kernel, m->lib, names[1].c_str());
+  if (names.size() == 7)
+    for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaLibraryGetKernel(&m->sk[q], m->lib, names[2 + q].c_str());
+  if (e == cudaSuccess && m->sk[3]) {
+    m->sort_warps = opt.sort_warps;
+    m->sort_smem = (size_t)opt.sort_warps * 32 * opt.sort_slot;
+    e = cudaFuncSetAttribute((const void*)m->sk[3], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m->sort_smem);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&m->d_consts, plan.consts.size() * sizeof(int64_t));
   // kernel id -> (bin | shape << 16); bins are positions in `ks`
   uint32_t maxid = 0;
@@ -717,8 +768,13 @@ int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 
 
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
 
+int jit_launch_count(const JitModule* m, uint64_t n) {
+  return m && m->sk[3] && n > kSmallMax && n < (1ULL << 32) ? 5 : 1;
+}
+
 void jit_destroy(JitModule* m) {
   if (!m) return;
+  if (m->sort_buf) cudaFree(m->sort_buf);
   if (m->lib) cudaLibraryUnload(m->lib);
   if (m->d_consts) cudaFree(m->d_consts);
   if (m->d_kb) cudaFree(m->d_kb);
@@ -739,6 +795,42 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     uint32_t n32 = (uint32_t)n;
     void* argv[] = {(void*)&P, (void*)&B, (void*)&n32, (void*)&flags, (void*)&bits, (void*)&counts};
     return cudaLaunchKernel((const void*)m->small_kernel, dim3(1), dim3(kSmallThreads), argv, 0, s);
+  }
+  if (m->sk[3] && n < (1ULL << 32)) {  // shape-sorted schedule (k_sorted.cuh)
+    SortScratch S{};
+    S.nblk = (uint32_t)std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 8);
+    S.chunk = (uint32_t)(((n + S.nblk - 1) / S.nblk + 31) & ~31ULL);
+    const uint32_t max_blk = (uint32_t)num_sms * 8;
+    if (m->sort_cap < n) {  // keys, permutation, (key, block) counts, per-key tables
+      if (m->sort_buf) cudaFree(m->sort_buf);
+      m->sort_buf = nullptr;
+      m->sort_cap = 0;
+      const size_t bytes = ((n + 255) & ~255ULL) * 5 + (size_t)kSortKeys * max_blk * 4 + kMetaWords * 4 + 256;
+      cudaError_t e = cudaMalloc(&m->sort_buf, bytes);
+      if (e != cudaSuccess) return e;
+      m->sort_cap = n;
+    }
+    uint8_t* b = (uint8_t*)m->sort_buf;
+    const size_t cap = (m->sort_cap + 255) & ~255ULL;
+    S.perm = (uint32_t*)b;
+    S.keys = b + cap * 4;
+    S.hist = (uint32_t*)(b + cap * 5);
+    S.meta = S.hist + (size_t)kSortKeys * max_blk;
+    void* a1[] = {(void*)&P, (void*)&B, (void*)&n, (void*)&S, (void*)&flags};
+    cudaError_t e = cudaLaunchKernel((const void*)m->sk[0], dim3(S.nblk), dim3(256), a1, 0, s);
+    void* a2[] = {(void*)&S};
+    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[1], dim3(1), dim3(kSortScanThreads), a2, 0, s);
+    void* a3[] = {(void*)&n, (void*)&S};
+    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[2], dim3(S.nblk), dim3(256), a3, 0, s);
+    void* a4[] = {(void*)&P, (void*)&B, (void*)&S, (void*)&flags};
+    if (e == cudaSuccess)
+      e = cudaLaunchKernel((const void*)m->sk[3], dim3(num_sms), dim3(m->sort_warps * 32), a4, m->sort_smem, s);
+    const uint64_t words = (n + 31) / 32;
+    const unsigned eb = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)num_sms * 8);
+    const uint8_t* cf = flags;
+    void* a5[] = {(void*)&cf, (void*)&n, (void*)&bits, (void*)&counts};
+    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[4], dim3(eb), dim3(256), a5, 0, s);
+    return e;
   }
   const uint64_t ntiles = (n + m->tile - 1) / m->tile;
   const uint64_t cap = (uint64_t)num_sms * m->ctas;

@@ -27,6 +27,10 @@ struct Options {
   int tile = 0, threads = 256, ctas = 2, args_per_rec = 8;  // tile 0: chosen at load (jit.cpp)
   int arg_bufs = 2;  // argument staging buffers of the pipelined kernel (1: more CTAs per SM)
   bool stride = false;  // stride-aware ranges (row f4): validate through eval_stride (k_stride.cu)
+  // shape-sorted schedule (k_sorted.cuh): 1 on, 0 off, -1 by the summary (on
+  // for many-argument summaries, the geometry of C4); its warps per CTA and
+  // per-record argument slot bytes are resolved with the geometry
+  int sorted = -1, sort_warps = 0, sort_slot = 0;
 };
 
 struct JitModule;
@@ -44,8 +48,10 @@ struct JitPlan {
   std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
   int nshapes = 0;
 };
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride);
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false);
 bool jit_is_stride(const JitModule* m);
+// Kernel launches one picker_validate_batch of n records makes on the module.
+int jit_launch_count(const JitModule* m, uint64_t n);
 // Warps per SM of the specialised module's persistent kernel (CTAs x threads / 32).
 int jit_warps_per_sm(const JitModule* m);
 // The module has the small-batch kernel and n <= kSmallMax (one CTA, counts written).

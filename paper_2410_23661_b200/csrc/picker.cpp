@@ -141,6 +141,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "args_per_rec") c->opt.args_per_rec = (int)v;
   else if (k == "arg_bufs") c->opt.arg_bufs = (int)v;
   else if (k == "stride") c->opt.stride = v != 0;
+  else if (k == "sorted") c->opt.sorted = v < 0 ? -1 : (int)(v != 0);
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
@@ -291,9 +292,10 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     Options opt;
     select_paths(ks, opt);
     order_by_shape(ks);
-    JitPlan plan = jit_plan(ks, false);
+    const Options geo = resolve_geometry(ks, opt);
+    JitPlan plan = jit_plan(ks, false, geo.sorted > 0);
     std::string cubin, lowered, err;
-    if (!jit_compile(plan, resolve_geometry(ks, opt), cubin, lowered, false, err)) {
+    if (!jit_compile(plan, geo, cubin, lowered, false, err)) {
       put(msg, msg_len, err);
       put(src_out, src_len, plan.src);
       return PICKER_ECUDA;

@@ -216,6 +216,23 @@ constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint3
 constexpr int kWideMax = 1024;
 constexpr int kWideElemBytes = 32;
 
+// Shape-sorted schedule (k_sorted.cuh): host-visible layout of its scratch.
+constexpr uint32_t kSortKeys = kPipeKeys;  // grouping keys of the module (<= 64)
+constexpr uint32_t kSortNoKey = 0xFF;      // final code in S1, not sorted
+constexpr int kSortScanThreads = 1024;
+
+// Device scratch of the sorted schedule (owned by the module, jit.cpp).
+struct SortScratch {
+  uint8_t* keys;   // [n]
+  uint32_t* perm;  // [n]: key-sorted position -> record
+  uint32_t* hist;  // [kSortKeys * nblk]: (key, block) counts, scanned in place by S2
+  uint32_t* meta;  // key_off[kSortKeys + 1] | key_cnt[kSortKeys] | gstart[kSortKeys + 1] | claim
+  uint32_t nblk;   // blocks of S1 / S3
+  uint32_t chunk;  // records per block (a multiple of 32)
+};
+constexpr uint32_t kMetaOff = 0, kMetaCnt = kSortKeys + 1, kMetaG = 2 * kSortKeys + 1,
+                   kMetaClaim = 3 * kSortKeys + 2, kMetaWords = 3 * kSortKeys + 3;
+
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind
 constexpr int kGenMaxVar = 64;

@@ -231,7 +231,8 @@ def test_exact_big_tables(pk):
 
 # ---- C4: cuDNN-like kernels with 16-48 pointer arguments ------------------------
 
-@pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, force_path=3), dict(jit=0, force_path=3),
+@pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, sorted=0), dict(jit=1, force_path=3),
+                                 dict(jit=1, force_path=3, sorted=0), dict(jit=0, force_path=3),
                                  dict(jit=0, bucket=0)], ids=str)
 def test_c4_many_pointers(pk, opt):
     """Specialised pairwise, the K2 sort+sweep path and the table path agree

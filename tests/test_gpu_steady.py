@@ -121,11 +121,14 @@ def test_random_tiled_steady_state(pk, opt):
 
 
 def test_c4_tiled_steady_state(pk):
-    """C4 x 256 = 1,048,576 records on its auto geometry (2560-record tiles,
-    148 CTAs): ~2.8 tiles per CTA; plus 64-record tiles (>100 per CTA)."""
+    """C4 x 256 = 1,048,576 records on the shape-sorted schedule (the default
+    for many-argument summaries: ~32,800 claimed groups over 148 CTAs) and on
+    the tiled kernel (2560-record tiles, 148 CTAs: ~2.8 tiles per CTA; plus
+    64-record tiles, >100 per CTA)."""
     s, rec, args, meta = workloads.make_c4(n=1 << 12)
     want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
-    for R, opt in [(256, dict(jit=1)), (8, dict(jit=1, tile=64, threads=32, ctas=1, args_per_rec=20))]:
+    for R, opt in [(256, dict(jit=1)), (256, dict(jit=1, sorted=0)),
+                   (8, dict(jit=1, sorted=0, tile=64, threads=32, ctas=1, args_per_rec=20))]:
         rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
         flags, bits, counts = _run(pk, s, rec_t, args_t, **opt)
         _check(flags, bits, counts, np.tile(want, R))

@@ -49,7 +49,7 @@ def wide():
     return s, rec, args, np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
 
 
-WIDE_PATHS = [dict(jit=1), dict(jit=1, tile=64, threads=32, ctas=1, args_per_rec=8),
+WIDE_PATHS = [dict(jit=1), dict(jit=1, sorted=0), dict(jit=1, sorted=0, tile=64, threads=32, ctas=1, args_per_rec=8),
               dict(jit=0, bucket=1), dict(jit=0, bucket=0), dict(jit=0, force_path=3)]
 
 
