@@ -79,44 +79,56 @@ __global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ Bucke
   for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) S.hist[t * S.nblk + blockIdx.x] = cnt[t];
 }
 
-// One CTA: exclusive scan of hist (key-major), then the per-key tables.
+// One CTA: exclusive scan of hist (key-major), then the per-key tables.  Warp
+// w scans keys w and w + 32 over the blocks (coalesced 32-wide chunks with a
+// carried sum); one warp scans the 64 key totals; the warps add the offsets.
 __global__ void __launch_bounds__(kSortScanThreads) k_sort_scan(SortScratch S) {
-  __shared__ uint32_t s_part[kSortScanThreads];
-  __shared__ uint32_t s_tot[kSortKeys];
-  const uint32_t m = kSortKeys * S.nblk, per = (m + kSortScanThreads - 1) / kSortScanThreads;
-  const uint32_t b0 = min(m, threadIdx.x * per), b1 = min(m, b0 + per);
-  uint32_t sum = 0;
-  for (uint32_t b = b0; b < b1; ++b) sum += S.hist[b];
-  s_part[threadIdx.x] = sum;
-  __syncthreads();
-  for (int d = 1; d < kSortScanThreads; d <<= 1) {  // Hillis-Steele inclusive scan
-    const uint32_t v = threadIdx.x >= (unsigned)d ? s_part[threadIdx.x - d] : 0u;
-    __syncthreads();
-    s_part[threadIdx.x] += v;
-    __syncthreads();
-  }
-  uint32_t run = s_part[threadIdx.x] - sum;
-  for (uint32_t b = b0; b < b1; ++b) {
-    const uint32_t c = S.hist[b];
-    S.hist[b] = run;
-    run += c;
-  }
-  __syncthreads();
-  if (threadIdx.x < kSortKeys) {
-    const uint32_t k = threadIdx.x;
-    const uint32_t lo = S.hist[k * S.nblk];
-    const uint32_t hi = k + 1 < kSortKeys ? S.hist[(k + 1) * S.nblk] : s_part[kSortScanThreads - 1];
-    S.meta[kMetaOff + k] = lo;
-    S.meta[kMetaCnt + k] = hi - lo;
-    s_tot[k] = (hi - lo + 31) / 32;
+  __shared__ uint32_t s_tot[kSortKeys], s_base[kSortKeys];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (uint32_t k = warp; k < kSortKeys; k += kSortScanThreads / 32) {
+    uint32_t* h = S.hist + (size_t)k * S.nblk;
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < S.nblk; b0 += 32) {
+      const uint32_t b = b0 + lane;
+      const uint32_t c = b < S.nblk ? h[b] : 0u;
+      uint32_t v = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += o;
+      }
+      if (b < S.nblk) h[b] = carry + v - c;  // exclusive within the key
+      carry += __shfl_sync(0xffffffffu, v, 31);
+    }
+    if (lane == 0) s_tot[k] = carry;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    uint32_t g = 0;
-    for (uint32_t k = 0; k < kSortKeys; ++k) S.meta[kMetaG + k] = g, g += s_tot[k];
-    S.meta[kMetaG + kSortKeys] = g;
-    S.meta[kMetaOff + kSortKeys] = s_part[kSortScanThreads - 1];
-    S.meta[kMetaClaim] = 0;
+  if (warp == 0) {  // exclusive scan of the 64 totals (lane l: keys l and 32 + l)
+    const uint32_t t0 = s_tot[lane], t1 = s_tot[lane + 32];
+    const uint32_t g0 = (t0 + 31) / 32, g1 = (t1 + 31) / 32;
+    uint32_t v0 = t0, v1 = t1, w0 = g0, w1 = g1;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t a = __shfl_up_sync(0xffffffffu, v0, d), b = __shfl_up_sync(0xffffffffu, v1, d);
+      const uint32_t c = __shfl_up_sync(0xffffffffu, w0, d), e = __shfl_up_sync(0xffffffffu, w1, d);
+      if (lane >= d) v0 += a, v1 += b, w0 += c, w1 += e;
+    }
+    const uint32_t T0 = __shfl_sync(0xffffffffu, v0, 31), G0 = __shfl_sync(0xffffffffu, w0, 31);
+    v1 += T0, w1 += G0;
+    s_base[lane] = v0 - t0, s_base[lane + 32] = v1 - t1;
+    S.meta[kMetaOff + lane] = v0 - t0, S.meta[kMetaOff + lane + 32] = v1 - t1;
+    S.meta[kMetaCnt + lane] = t0, S.meta[kMetaCnt + lane + 32] = t1;
+    S.meta[kMetaG + lane] = w0 - g0, S.meta[kMetaG + lane + 32] = w1 - g1;
+    if (lane == 31) {
+      S.meta[kMetaOff + kSortKeys] = v1;
+      S.meta[kMetaG + kSortKeys] = w1;
+      S.meta[kMetaClaim] = 0;
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = warp; k < kSortKeys; k += kSortScanThreads / 32) {
+    uint32_t* h = S.hist + (size_t)k * S.nblk;
+    for (uint32_t b = lane; b < S.nblk; b += 32) h[b] += s_base[k];
   }
 }
 
@@ -154,6 +166,14 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   __syncthreads();
   const uint32_t ngroups = s_g[kSortKeys];
   unsigned char* slots = smem + (size_t)warp * 32 * kSortSlot;
+  __shared__ __align__(8) uint64_t s_bar[kSortWarps];
+  uint64_t* bar = s_bar + warp;
+  uint32_t phase = 0;
+  if (lane == 0) {
+    mbar_init(bar, 32);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
   const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
   for (;;) {
     uint32_t g = 0;
@@ -197,24 +217,22 @@ __global__ void __launch_bounds__(kSortThreads, 1)
         shift = (uint32_t)(a0 - c0);
       }
     }
-    // lanes over the 16-byte chunks of one record at a time: coalesced copies
-    for (uint32_t q = 0; q < rem; ++q) {
-      const uint64_t src = __shfl_sync(0xffffffffu, s0, q);
-      const uint32_t c = __shfl_sync(0xffffffffu, nch, q);
-      for (uint32_t ch = lane; ch < c; ch += 32)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(slots + q * kSortSlot + 16 * ch)),
-                     "l"(src + 16ull * ch)
-                     : "memory");
-    }
-    asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
-    __syncwarp();
+    // each lane stages its record's span with one TMA bulk copy into its slot;
+    // the warp's mbarrier completes when all 32 lanes arrived and the bytes landed
+    const uint32_t bytes = nch * 16u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+    if (bytes) tma_load_1d(slots + lane * kSortSlot, (const void*)s0, bytes, bar);
+    mbar_wait(bar, phase);
+    phase ^= 1u;
     if (valid) {
       const bool local = nch != 0;
       const int64_t* a = local ? reinterpret_cast<const int64_t*>(slots + lane * kSortSlot + shift)
                                : B.args + r.arg_off;
       flags[i] = Dispatch::eval(k, kb & 0xFFFFu, kn, local, P, r, a, B);
     }
-    __syncwarp();  // the slots are reused by the warp's next group
+    __syncwarp();  // the slots are reused by the warp's next group (the next copy is async-proxy)
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
 }
 
