@@ -121,7 +121,16 @@ struct Gen {
 // stride: the stride-aware variant (row f4, eval_stride.cuh): a read/write pair
 // whose intervals intersect is an overlap only if may_collide() holds for the
 // two descriptors' congruence classes (computed lazily, on intersection).
-std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
+// Streamed descriptors that differ only in their base argument (same kind,
+// activity, term sums and width: e.g. every 16-byte read of a tensor list with
+// one shape) are evaluated by a loop over a table of argument indices when a
+// class has at least kLoopMin members: many-pointer kernels (C4) otherwise
+// emit one straight-line block per descriptor, and a shape of ~4,000 SASS
+// instructions does not fit the 32 KB instruction cache.
+constexpr size_t kLoopMin = 3;
+uint64_t fnv1a(const std::string& s);
+
+std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs) {
   Gen g(K);
   std::ostringstream& s = g.s;
   const int np = (int)k.param_names.size();
@@ -312,9 +321,67 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     extent(di, "  ");
     kept.push_back((int)di);
   }
-  for (size_t di = 0; di < k.desc.size(); ++di) {  // the streamed side
+  // term sums of a descriptor without its base, constants as literals (the
+  // grouping key of the loop classes); false if it cannot join a loop
+  auto sums = [&](size_t di, Gen& gg, std::string& lb, std::string& ub) {
     const IrDesc& d = k.desc[di];
-    if (d.opaque || d.kind == kept_kind) continue;
+    if (stride || d.base < OPD_ARG0 || k.param_i32[d.base - OPD_ARG0]) return false;
+    lb = "0LL", ub = lb;
+    for (const IrTerm& t : d.terms) {
+      const std::string c = gg.prod(t.c);
+      if (t.var < 0) {
+        lb = "add64(" + lb + ", " + c + ")", ub = "add64(" + ub + ", " + c + ")";
+        continue;
+      }
+      const int x = sids[di][t.var];
+      const int sign = k.var_sign[di][t.var];
+      if (sign == 0) return false;
+      const std::string L = "vl" + std::to_string(x), H = "vh" + std::to_string(x);
+      auto phi = [&](const std::string& v) {
+        return t.div == 1 ? v : "floordiv64(" + v + ", " + std::to_string(t.div) + "u)";
+      };
+      const std::string mul = t.narrow ? "mulw" : "mul64";
+      const std::string lo_end = sign > 0 ? L : H, hi_end = sign > 0 ? H : L;
+      if (!(lo0[x] && sign > 0)) lb = "add64(" + lb + ", " + mul + "(" + c + ", " + phi(lo_end) + "))";
+      if (!(lo0[x] && sign < 0)) ub = "add64(" + ub + ", " + mul + "(" + c + ", " + phi(hi_end) + "))";
+    }
+    return true;  // the width is per member (the index table), not part of the class
+  };
+  auto literal = [](std::string e, const std::vector<int64_t>& kk) {
+    for (size_t p = kk.size(); p-- > 0;) {
+      const std::string tok = "__ldg(K + " + std::to_string(p) + ")";
+      for (size_t at = e.find(tok); at != std::string::npos; at = e.find(tok, at))
+        e.replace(at, tok.size(), "(" + std::to_string(kk[p]) + "LL)");
+    }
+    return e;
+  };
+  std::map<std::string, std::vector<int>> cls;  // key -> streamed members
+  std::vector<std::string> cls_order;
+  for (size_t di = 0; di < k.desc.size(); ++di) {
+    const IrDesc& d = k.desc[di];
+    if (d.opaque || d.kind == kept_kind || !defs) continue;
+    std::vector<int64_t> tk;
+    Gen tg(tk);
+    std::string lb, ub;
+    if (!sums(di, tg, lb, ub)) continue;
+    const std::string key = std::to_string(d.kind) + "|" + on_expr(di) + "|" + literal(lb, tk) + "|" + literal(ub, tk);
+    if (!cls.count(key)) cls_order.push_back(key);
+    cls[key].push_back((int)di);
+  }
+  std::vector<char> in_loop(k.desc.size(), 0);
+  bool any_loop = false;
+  for (auto& e : cls)
+    if (e.second.size() >= kLoopMin) {
+      any_loop = true;
+      for (int di : e.second) in_loop[di] = 1;
+    }
+  if (any_loop)  // kept extents with an empty interval when inactive (no on-flag per test)
+    for (int j : kept)
+      s << "  const int64_t mkl" << j << " = on" << j << " ? lb" << j << " : 9223372036854775807LL, mku" << j
+        << " = on" << j << " ? ub" << j << " : (-9223372036854775807LL - 1);\n";
+  for (size_t di = 0; di < k.desc.size(); ++di) {  // the streamed side, straight-line
+    const IrDesc& d = k.desc[di];
+    if (d.opaque || d.kind == kept_kind || in_loop[di]) continue;
     s << "  {\n    const bool on" << di << " = " << on_expr(di) << ";\n";
     s << "    act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
     extent(di, "    ");
@@ -328,6 +395,34 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride) {
     // (a hull pre-filter over the kept extents was measured slower on C4:
     // the branch per streamed extent grows the code, which is what bounds it)
     s << "    ov |= on" << di << " & (" << hit << ");\n  }\n";
+  }
+  for (const std::string& key : cls_order) {  // the streamed side, loop classes
+    const std::vector<int>& mem = cls[key];
+    if (mem.size() < kLoopMin) continue;
+    const int d0 = mem[0];
+    std::string idx;
+    for (int di : mem)  // argument index | (width - 1) << 8
+      idx += (idx.empty() ? "" : ", ") +
+             std::to_string((uint32_t)(k.desc[di].base - OPD_ARG0) | ((uint32_t)k.desc[di].width - 1) << 8) + "u";
+    char name[32];
+    snprintf(name, sizeof(name), "kI%016llx", (unsigned long long)fnv1a(idx));
+    (*defs)[name] = "__device__ __constant__ const uint32_t " + std::string(name) + "[" + std::to_string(mem.size()) +
+                    "] = {" + idx + "};\n";
+    std::string lb, ub;
+    sums((size_t)d0, g, lb, ub);
+    s << "  {\n    const bool onC = " << on_expr(d0) << ";\n";
+    s << "    act_" << (k.desc[d0].kind == KIND_R ? "r" : "w") << " |= onC;\n";
+    s << "    if (onC) {\n      const int64_t LOC = " << lb << ", HIC = " << ub << ";\n";
+    s << "#pragma unroll 1\n      for (int j = 0; j < " << mem.size() << "; ++j) {\n";
+    s << "        const uint32_t ej = " << name << "[j];\n";
+    s << "        const int64_t bj = a[ej & 0xFFu];\n";
+    s << "        const int64_t lbj = add64(bj, LOC), ubj = add64(add64(bj, HIC), (int64_t)(ej >> 8));\n";
+    std::string hit = "false";
+    for (int j : kept) {
+      const std::string J = std::to_string(j);
+      hit += " | ((lbj <= mku" + J + ") & (mkl" + J + " <= ubj))";
+    }
+    s << "        ov |= " << hit << ";\n      }\n    }\n  }\n";
   }
   auto any = [&](const std::vector<int>& a) {
     std::string e = "false";
@@ -451,9 +546,10 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
   std::vector<std::vector<size_t>> members;
   std::vector<std::vector<int64_t>> kconst(ks.size());
   std::vector<int> shape_of(ks.size(), -1);
+  std::map<std::string, std::string> idx_defs;  // argument-index tables of the loop classes
   for (size_t i = 0; i < ks.size(); ++i) {
     if (ks[i].path != PATH_JIT) continue;
-    std::string body = gen_body(ks[i], kconst[i], stride);
+    std::string body = gen_body(ks[i], kconst[i], stride, &idx_defs);
     auto it = shape_id.find(body);
     if (it == shape_id.end()) {
       it = shape_id.emplace(body, (uint32_t)shapes.size()).first;
@@ -534,6 +630,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
   P.meta[ks.size()] = JitMeta{SHAPE_UNKNOWN, 0, 0, 0};
   if (P.consts.empty()) P.consts.push_back(0);
   for (auto& m : P.meta) P.key_of.push_back((uint16_t)m.shape);
+  for (auto& d : idx_defs) src << d.second;
   for (size_t s = 0; s < shapes.size(); ++s)
     src << "__device__ __forceinline__ uint8_t ks" << s << shapes[s];
   // key = shape (warp-uniform); kn = the lane's kernel: constants offset |
@@ -798,9 +895,9 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
   }
   if (m->sk[3] && n < (1ULL << 32)) {  // shape-sorted schedule (k_sorted.cuh)
     SortScratch S{};
-    S.nblk = (uint32_t)std::min<uint64_t>((n + 2047) / 2048, (uint64_t)num_sms * 8);
+    S.nblk = (uint32_t)std::min<uint64_t>({(n + 4095) / 4096, (uint64_t)num_sms * 4, (uint64_t)kSortMaxBlk});
     S.chunk = (uint32_t)(((n + S.nblk - 1) / S.nblk + 31) & ~31ULL);
-    const uint32_t max_blk = (uint32_t)num_sms * 8;
+    const uint32_t max_blk = kSortMaxBlk;
     if (m->sort_cap < n) {  // keys, permutation, (key, block) counts, per-key tables
       if (m->sort_buf) cudaFree(m->sort_buf);
       m->sort_buf = nullptr;

@@ -58,22 +58,31 @@ __global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ Bucke
   for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) cnt[t] = 0;
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * S.chunk, end = min(n, base + S.chunk);
-  for (uint64_t i0 = base; i0 < end; i0 += blockDim.x) {
-    const uint64_t i = i0 + threadIdx.x;
-    uint32_t key = kSortNoKey;
-    if (i < end) {
-      const picker_rec_t* rp = B.rec + i;
-      uint32_t kb, kn;
-      kb_lookup(P, rp->kernel_id, kb, kn);
-      key = kb >> 16;
-      if (key == P.direct_key || key >= kSortKeys) {  // shortcut / unknown: final now
-        flags[i] = (uint8_t)direct_code(kn, rp->nargs, rp->arg_off, B.args_lo, B.args_hi);
-        key = kSortNoKey;
-      }
-      S.keys[i] = (uint8_t)key;
+  constexpr int U = 4;  // records per thread in flight (the kernel-id loads are latency-bound)
+  for (uint64_t i0 = base; i0 < end; i0 += U * blockDim.x) {
+    uint32_t kid[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+      kid[u] = i < end ? __ldg(&B.rec[i].kernel_id) : 0u;
     }
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    if (key != kSortNoKey && (threadIdx.x & 31) == 31 - __clz(peers)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+      uint32_t key = kSortNoKey;
+      if (i < end) {
+        uint32_t kb, kn;
+        kb_lookup(P, kid[u], kb, kn);
+        key = kb >> 16;
+        if (key == P.direct_key || key >= kSortKeys) {  // shortcut / unknown: final now
+          flags[i] = (uint8_t)direct_code(kn, __ldg(&B.rec[i].nargs), __ldg(&B.rec[i].arg_off), B.args_lo, B.args_hi);
+          key = kSortNoKey;
+        }
+        S.keys[i] = (uint8_t)key;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      if (key != kSortNoKey && (threadIdx.x & 31) == 31 - __clz(peers)) atomicAdd(cnt + key, (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
   for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) S.hist[t * S.nblk + blockIdx.x] = cnt[t];
@@ -85,22 +94,27 @@ __global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ Bucke
 __global__ void __launch_bounds__(kSortScanThreads) k_sort_scan(SortScratch S) {
   __shared__ uint32_t s_tot[kSortKeys], s_base[kSortKeys];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t per = (S.nblk + 31) / 32;  // blocks per lane (<= kSortMaxPer)
   for (uint32_t k = warp; k < kSortKeys; k += kSortScanThreads / 32) {
     uint32_t* h = S.hist + (size_t)k * S.nblk;
-    uint32_t carry = 0;
-    for (uint32_t b0 = 0; b0 < S.nblk; b0 += 32) {
-      const uint32_t b = b0 + lane;
-      const uint32_t c = b < S.nblk ? h[b] : 0u;
-      uint32_t v = c;
+    const uint32_t b0 = min(S.nblk, lane * per), b1 = min(S.nblk, b0 + per);
+    uint32_t c[kSortMaxPer];
+    uint32_t sum = 0;
 #pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
-        if (lane >= d) v += o;
-      }
-      if (b < S.nblk) h[b] = carry + v - c;  // exclusive within the key
-      carry += __shfl_sync(0xffffffffu, v, 31);
+    for (uint32_t q = 0; q < kSortMaxPer; ++q) c[q] = b0 + q < b1 ? h[b0 + q] : 0u;
+#pragma unroll
+    for (uint32_t q = 0; q < kSortMaxPer; ++q) sum += c[q];
+    uint32_t v = sum;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
+      if (lane >= d) v += o;
     }
-    if (lane == 0) s_tot[k] = carry;
+    uint32_t run = v - sum;
+#pragma unroll
+    for (uint32_t q = 0; q < kSortMaxPer; ++q)
+      if (b0 + q < b1) h[b0 + q] = run, run += c[q];
+    if (lane == 31) s_tot[k] = v;
   }
   __syncthreads();
   if (warp == 0) {  // exclusive scan of the 64 totals (lane l: keys l and 32 + l)
@@ -138,15 +152,25 @@ __global__ void __launch_bounds__(256) k_sort_scatter(uint64_t n, SortScratch S)
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * S.chunk, end = min(n, base + S.chunk);
   const int lane = threadIdx.x & 31;
-  for (uint64_t i0 = base; i0 < end; i0 += blockDim.x) {
-    const uint64_t i = i0 + threadIdx.x;
-    const uint32_t key = i < end ? S.keys[i] : kSortNoKey;
-    const unsigned peers = __match_any_sync(0xffffffffu, key);
-    const int leader = 31 - __clz(peers);
-    uint32_t b = 0;
-    if (key != kSortNoKey && lane == leader) b = atomicAdd(cur + key, (uint32_t)__popc(peers));
-    b = __shfl_sync(0xffffffffu, b, leader);
-    if (key != kSortNoKey) S.perm[b + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)i;
+  constexpr int U = 4;
+  for (uint64_t i0 = base; i0 < end; i0 += U * blockDim.x) {
+    uint32_t kk[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+      kk[u] = i < end ? S.keys[i] : kSortNoKey;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
+      const uint32_t key = kk[u];
+      const unsigned peers = __match_any_sync(0xffffffffu, key);
+      const int leader = 31 - __clz(peers);
+      uint32_t b = 0;
+      if (key != kSortNoKey && lane == leader) b = atomicAdd(cur + key, (uint32_t)__popc(peers));
+      b = __shfl_sync(0xffffffffu, b, leader);
+      if (key != kSortNoKey) S.perm[b + __popc(peers & ((1u << lane) - 1u))] = (uint32_t)i;
+    }
   }
 }
 
@@ -165,74 +189,75 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   }
   __syncthreads();
   const uint32_t ngroups = s_g[kSortKeys];
-  unsigned char* slots = smem + (size_t)warp * 32 * kSortSlot;
-  __shared__ __align__(8) uint64_t s_bar[kSortWarps];
-  uint64_t* bar = s_bar + warp;
-  uint32_t phase = 0;
-  if (lane == 0) {
-    mbar_init(bar, 32);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncwarp();
+  unsigned char* slot = smem + ((size_t)warp * 32 + lane) * kSortSlot;
   const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
-  for (;;) {
-    uint32_t g = 0;
-    if (lane == 0) g = atomicAdd(S.meta + kMetaClaim, 1u);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    if (g >= ngroups) break;
-    // key of group g: the last k with s_g[k] <= g (s_g is non-decreasing)
-    uint32_t k = 0;
+  // group g -> key, first sorted position, records
+  auto group = [&](uint32_t g, uint32_t& k, uint32_t& start, uint32_t& rem) {
+    k = 0;
 #pragma unroll
     for (uint32_t step = kSortKeys / 2; step > 0; step >>= 1)
-      if (s_g[k + step] <= g) k += step;
+      if (s_g[k + step] <= g) k += step;  // the last key whose groups start at or before g
     const uint32_t j = g - s_g[k];
-    const uint32_t start = s_off[k] + 32u * j, rem = min(32u, s_cnt[k] - 32u * j);
+    start = s_off[k] + 32u * j;
+    rem = min(32u, s_cnt[k] - 32u * j);
+  };
+  auto claim = [&]() {
+    uint32_t c = 0;
+    if (lane == 0) c = atomicAdd(S.meta + kMetaClaim, 1u);
+    return c;  // lane 0's value; broadcast where it is consumed
+  };
+  // software pipeline over a warp's groups: the claim of group g+1 and its
+  // permutation entries are loaded while group g is evaluated, and its headers
+  // are prefetched into L2 at the end of g, so the claim / permutation / header
+  // round trips are off the critical path
+  uint32_t g = __shfl_sync(0xffffffffu, claim(), 0);
+  uint32_t k = 0, start = 0, rem = 0, pi = 0;
+  if (g < ngroups) {
+    group(g, k, start, rem);
+    pi = (uint32_t)lane < rem ? S.perm[start + lane] : 0u;
+  }
+  uint32_t gn_lane0 = claim();
+  while (g < ngroups) {
+    const uint32_t gn = __shfl_sync(0xffffffffu, gn_lane0, 0);
+    uint32_t kn_ = 0, startn = 0, remn = 0, pin = 0;
+    if (gn < ngroups) {
+      group(gn, kn_, startn, remn);
+      pin = (uint32_t)lane < remn ? S.perm[startn + lane] : 0u;  // consumed next iteration
+    }
+    gn_lane0 = claim();
     if (kWidePath && k == P.wide_key) {  // K2: the whole warp on one record at a time
       for (uint32_t q = 0; q < rem; ++q) {
-        const uint32_t wi = S.perm[start + q];
+        const uint32_t wi = __shfl_sync(0xffffffffu, pi, q);
         const picker_rec_t r = load_rec(B.rec + wi);
         const uint8_t c = eval_wide_warp(P.T, r, B.args + r.arg_off, B.args_lo, B.args_hi, lane,
                                          wide_scratch(P, warp));
         if (lane == 0) flags[wi] = c;
       }
-      continue;
-    }
-    const bool valid = (uint32_t)lane < rem;
-    uint32_t i = 0, kb = 0, kn = 0;
-    picker_rec_t r{};
-    uint64_t s0 = 0;
-    uint32_t nch = 0, shift = 0;
-    if (valid) {
-      i = S.perm[start + lane];
-      r = load_rec(B.rec + i);
+    } else if ((uint32_t)lane < rem) {
+      const uint32_t i = pi;
+      const picker_rec_t r = load_rec(B.rec + i);
+      uint32_t kb, kn;
       kb_lookup(P, r.kernel_id, kb, kn);
-      // stage the argument span when the record is well-formed and it fits
+      // stage the record's argument span (16-byte chunks, cp.async per lane:
+      // a bulk copy per lane is serialised by the uniform datapath) when the
+      // record is well-formed and the span fits the slot
       const uintptr_t a0 = (uintptr_t)(B.args + r.arg_off), a1 = a0 + 8ull * r.nargs;
       const uintptr_t c0 = a0 & ~(uintptr_t)15, c1 = (a1 + 15) & ~(uintptr_t)15;
       const bool in_pool = r.arg_off >= B.args_lo && r.arg_off <= B.args_hi &&
                            (uint64_t)r.nargs <= B.args_hi - r.arg_off;
-      if (r.nargs == (kn >> 24) && in_pool && c0 >= p0 && c1 <= p1 && c1 - c0 <= kSortSlot) {
-        s0 = c0;
-        nch = (uint32_t)((c1 - c0) >> 4);
-        shift = (uint32_t)(a0 - c0);
+      const bool local = r.nargs == (kn >> 24) && in_pool && c0 >= p0 && c1 <= p1 && c1 - c0 <= kSortSlot;
+      if (local) {
+        for (uintptr_t c = c0; c < c1; c += 16)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(slot + (c - c0))), "l"(c)
+                       : "memory");
+        asm volatile("cp.async.commit_group;\ncp.async.wait_all;" ::: "memory");
       }
-    }
-    // each lane stages its record's span with one TMA bulk copy into its slot;
-    // the warp's mbarrier completes when all 32 lanes arrived and the bytes landed
-    const uint32_t bytes = nch * 16u;
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-                 : "memory");
-    if (bytes) tma_load_1d(slots + lane * kSortSlot, (const void*)s0, bytes, bar);
-    mbar_wait(bar, phase);
-    phase ^= 1u;
-    if (valid) {
-      const bool local = nch != 0;
-      const int64_t* a = local ? reinterpret_cast<const int64_t*>(slots + lane * kSortSlot + shift)
-                               : B.args + r.arg_off;
+      const int64_t* a = local ? reinterpret_cast<const int64_t*>(slot + (a0 - c0)) : B.args + r.arg_off;
       flags[i] = Dispatch::eval(k, kb & 0xFFFFu, kn, local, P, r, a, B);
     }
-    __syncwarp();  // the slots are reused by the warp's next group (the next copy is async-proxy)
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    // the next group's headers into L2 while this warp finishes
+    if ((uint32_t)lane < remn) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.rec + pin) : "memory");
+    g = gn, k = kn_, start = startn, rem = remn, pi = pin;
   }
 }
 

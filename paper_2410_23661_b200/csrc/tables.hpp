@@ -220,6 +220,8 @@ constexpr int kWideElemBytes = 32;
 constexpr uint32_t kSortKeys = kPipeKeys;  // grouping keys of the module (<= 64)
 constexpr uint32_t kSortNoKey = 0xFF;      // final code in S1, not sorted
 constexpr int kSortScanThreads = 1024;
+constexpr uint32_t kSortMaxBlk = 32 * 24;  // blocks of S1 / S3 (kSortMaxPer per scan lane)
+constexpr uint32_t kSortMaxPer = kSortMaxBlk / 32;
 
 // Device scratch of the sorted schedule (owned by the module, jit.cpp).
 struct SortScratch {
