@@ -57,7 +57,7 @@ struct JitModule {
   int nshapes = 0;
   int tile = 0, threads = 0, ctas = 0;
   bool stride = false;  // built with stride-aware shapes (row f4)
-  // shape-sorted schedule (k_sorted.cuh): S1 keys, S2 scan, S3 scatter,
+  // shape-sorted schedule (k_sorted.cuh): S1 keys, [1 unused], S3 scatter,
   // S4 validate, S5 emit; its scratch grows with the largest batch seen
   cudaKernel_t sk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int sort_warps = 0;
@@ -485,7 +485,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   nvrtcAddNameExpression(prog, small_expr);
   // the shape-sorted schedule's kernels (k_sorted.cuh), when the module has them
   const bool sorted = src.find("k_validate_sorted<JitDispatch>") != std::string::npos;
-  const char* sort_exprs[] = {"picker::k_sort_keys", "picker::k_sort_scan", "picker::k_sort_scatter",
+  const char* sort_exprs[] = {"picker::k_sort_keys", "picker::k_sort_scatter",
                               "picker::k_validate_sorted<picker::JitDispatch>", "picker::k_sort_emit"};
   if (sorted)
     for (const char* e : sort_exprs) nvrtcAddNameExpression(prog, e);
@@ -509,7 +509,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   nvrtcGetLoweredName(prog, small_expr, &low);
   lowered += std::string("\n") + (low ? low : "");  // main kernel, small-batch kernel
   if (sorted)
-    for (const char* e : sort_exprs) {  // then the sorted schedule's five kernels
+    for (const char* e : sort_exprs) {  // then the sorted schedule's four kernels
       low = nullptr;
       nvrtcGetLoweredName(prog, e, &low);
       lowered += std::string("\n") + (low ? low : "");
@@ -793,8 +793,9 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, names[0].c_str());
   if (e == cudaSuccess && names.size() > 1 && !names[1].empty())
     e = cudaLibraryGetKernel(&m->small_kernel, m->lib, names[1].c_str());
-  if (names.size() == 7)
-    for (int q = 0; q < 5 && e == cudaSuccess; ++q) e = cudaLibraryGetKernel(&m->sk[q], m->lib, names[2 + q].c_str());
+  if (names.size() == 6)  // S1 keys, S3 scatter, S4 validate, S5 emit
+    for (int q : {0, 2, 3, 4})
+      if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->sk[q], m->lib, names[2 + (q ? q - 1 : 0)].c_str());
   if (e == cudaSuccess && m->sk[3]) {
     m->sort_warps = opt.sort_warps;
     m->sort_smem = (size_t)opt.sort_warps * 32 * opt.sort_slot;
@@ -866,7 +867,7 @@ int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
 
 int jit_launch_count(const JitModule* m, uint64_t n) {
-  return m && m->sk[3] && n > kSmallMax && n < (1ULL << 32) ? 5 : 1;
+  return m && m->sk[3] && n > kSmallMax && n < (1ULL << 32) ? 4 : 1;
 }
 
 void jit_destroy(JitModule* m) {
@@ -914,11 +915,10 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     S.hist = (uint32_t*)(b + cap * 5);
     S.meta = S.hist + (size_t)kSortKeys * max_blk;
     void* a1[] = {(void*)&P, (void*)&B, (void*)&n, (void*)&S, (void*)&flags};
-    cudaError_t e = cudaLaunchKernel((const void*)m->sk[0], dim3(S.nblk), dim3(256), a1, 0, s);
-    void* a2[] = {(void*)&S};
-    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[1], dim3(1), dim3(kSortScanThreads), a2, 0, s);
+    cudaError_t e = cudaMemsetAsync(S.meta, 0, kMetaWords * 4, s);  // key totals, claim counter
+    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[0], dim3(S.nblk), dim3(kSortBlock), a1, 0, s);
     void* a3[] = {(void*)&n, (void*)&S};
-    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[2], dim3(S.nblk), dim3(256), a3, 0, s);
+    if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[2], dim3(S.nblk), dim3(kSortBlock), a3, 0, s);
     void* a4[] = {(void*)&P, (void*)&B, (void*)&S, (void*)&flags};
     if (e == cudaSuccess)
       e = cudaLaunchKernel((const void*)m->sk[3], dim3(num_sms), dim3(m->sort_warps * 32), a4, m->sort_smem, s);

@@ -10,11 +10,11 @@
 // in shape order removes those stalls but exposes the uncoalesced per-lane
 // argument loads (`lg_throttle`, 11 per issue).  This schedule fixes both:
 //   S1 k_sort_keys     thread per record: grouping key of its kernel (shortcut
-//                      kernels and unknown ids get their final code here), per
-//                      block key counts;
-//   S2 k_sort_scan     one CTA: offsets of every (key, block) in key-major order,
-//                      per-key record offsets and 32-record group counts;
-//   S3 k_sort_scatter  thread per record: record index into key order;
+//                      kernels and unknown ids get their final code here); per
+//                      block key counts, whose offsets within each key come
+//                      from atomic adds on the key totals (no scan pass);
+//   S3 k_sort_scatter  thread per record: record index into key order (key
+//                      bases from an in-CTA scan of the 64 totals);
 //   S4 k_validate_sorted  persistent; warps claim 32-record groups of ONE key in
 //                      global key order (one atomic counter), so at any moment
 //                      the whole GPU runs one or two shapes; the group's
@@ -51,7 +51,7 @@ __device__ __forceinline__ void kb_lookup(const BucketParams& P, uint32_t kid, u
   }
 }
 
-__global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ BucketParams P,
+__global__ void __launch_bounds__(kSortBlock) k_sort_keys(const __grid_constant__ BucketParams P,
                                                    const __grid_constant__ DevBatch B, uint64_t n, SortScratch S,
                                                    uint8_t* __restrict__ flags) {
   __shared__ uint32_t cnt[kSortKeys];
@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ Bucke
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-      kid[u] = i < end ? __ldg(&B.rec[i].kernel_id) : 0u;
+      kid[u] = __ldg(&B.rec[min(i, end - 1)].kernel_id);  // unconditional: all loads in flight
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
@@ -85,70 +85,35 @@ __global__ void __launch_bounds__(256) k_sort_keys(const __grid_constant__ Bucke
     }
   }
   __syncthreads();
-  for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) S.hist[t * S.nblk + blockIdx.x] = cnt[t];
+  for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x)
+    S.hist[t * S.nblk + blockIdx.x] = cnt[t] ? atomicAdd(S.meta + kMetaTot + t, cnt[t]) : 0u;
 }
 
-// One CTA: exclusive scan of hist (key-major), then the per-key tables.  Warp
-// w scans keys w and w + 32 over the blocks (coalesced 32-wide chunks with a
-// carried sum); one warp scans the 64 key totals; the warps add the offsets.
-__global__ void __launch_bounds__(kSortScanThreads) k_sort_scan(SortScratch S) {
-  __shared__ uint32_t s_tot[kSortKeys], s_base[kSortKeys];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const uint32_t per = (S.nblk + 31) / 32;  // blocks per lane (<= kSortMaxPer)
-  for (uint32_t k = warp; k < kSortKeys; k += kSortScanThreads / 32) {
-    uint32_t* h = S.hist + (size_t)k * S.nblk;
-    const uint32_t b0 = min(S.nblk, lane * per), b1 = min(S.nblk, b0 + per);
-    uint32_t c[kSortMaxPer];
-    uint32_t sum = 0;
+// Per-key tables from the key totals (warp 0 of a CTA): off[k] = first sorted
+// position of key k, cnt[k] = its records, gs[k] = its first 32-record group.
+__device__ __forceinline__ void key_tables(const SortScratch& S, uint32_t* off, uint32_t* cnt, uint32_t* gs) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t t0 = S.meta[kMetaTot + lane], t1 = S.meta[kMetaTot + lane + 32];
+  const uint32_t g0 = (t0 + 31) / 32, g1 = (t1 + 31) / 32;
+  uint32_t v0 = t0, v1 = t1, w0 = g0, w1 = g1;
 #pragma unroll
-    for (uint32_t q = 0; q < kSortMaxPer; ++q) c[q] = b0 + q < b1 ? h[b0 + q] : 0u;
-#pragma unroll
-    for (uint32_t q = 0; q < kSortMaxPer; ++q) sum += c[q];
-    uint32_t v = sum;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t o = __shfl_up_sync(0xffffffffu, v, d);
-      if (lane >= d) v += o;
-    }
-    uint32_t run = v - sum;
-#pragma unroll
-    for (uint32_t q = 0; q < kSortMaxPer; ++q)
-      if (b0 + q < b1) h[b0 + q] = run, run += c[q];
-    if (lane == 31) s_tot[k] = v;
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xffffffffu, v0, d), b = __shfl_up_sync(0xffffffffu, v1, d);
+    const uint32_t c = __shfl_up_sync(0xffffffffu, w0, d), e = __shfl_up_sync(0xffffffffu, w1, d);
+    if (lane >= d) v0 += a, v1 += b, w0 += c, w1 += e;
   }
-  __syncthreads();
-  if (warp == 0) {  // exclusive scan of the 64 totals (lane l: keys l and 32 + l)
-    const uint32_t t0 = s_tot[lane], t1 = s_tot[lane + 32];
-    const uint32_t g0 = (t0 + 31) / 32, g1 = (t1 + 31) / 32;
-    uint32_t v0 = t0, v1 = t1, w0 = g0, w1 = g1;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t a = __shfl_up_sync(0xffffffffu, v0, d), b = __shfl_up_sync(0xffffffffu, v1, d);
-      const uint32_t c = __shfl_up_sync(0xffffffffu, w0, d), e = __shfl_up_sync(0xffffffffu, w1, d);
-      if (lane >= d) v0 += a, v1 += b, w0 += c, w1 += e;
-    }
-    const uint32_t T0 = __shfl_sync(0xffffffffu, v0, 31), G0 = __shfl_sync(0xffffffffu, w0, 31);
-    v1 += T0, w1 += G0;
-    s_base[lane] = v0 - t0, s_base[lane + 32] = v1 - t1;
-    S.meta[kMetaOff + lane] = v0 - t0, S.meta[kMetaOff + lane + 32] = v1 - t1;
-    S.meta[kMetaCnt + lane] = t0, S.meta[kMetaCnt + lane + 32] = t1;
-    S.meta[kMetaG + lane] = w0 - g0, S.meta[kMetaG + lane + 32] = w1 - g1;
-    if (lane == 31) {
-      S.meta[kMetaOff + kSortKeys] = v1;
-      S.meta[kMetaG + kSortKeys] = w1;
-      S.meta[kMetaClaim] = 0;
-    }
-  }
-  __syncthreads();
-  for (uint32_t k = warp; k < kSortKeys; k += kSortScanThreads / 32) {
-    uint32_t* h = S.hist + (size_t)k * S.nblk;
-    for (uint32_t b = lane; b < S.nblk; b += 32) h[b] += s_base[k];
-  }
+  v1 += __shfl_sync(0xffffffffu, v0, 31), w1 += __shfl_sync(0xffffffffu, w0, 31);
+  off[lane] = v0 - t0, off[lane + 32] = v1 - t1;
+  cnt[lane] = t0, cnt[lane + 32] = t1;
+  gs[lane] = w0 - g0, gs[lane + 32] = w1 - g1;
+  if (lane == 31) off[kSortKeys] = v1, gs[kSortKeys] = w1;
 }
 
-__global__ void __launch_bounds__(256) k_sort_scatter(uint64_t n, SortScratch S) {
-  __shared__ uint32_t cur[kSortKeys];
-  for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) cur[t] = S.hist[t * S.nblk + blockIdx.x];
+__global__ void __launch_bounds__(kSortBlock) k_sort_scatter(uint64_t n, SortScratch S) {
+  __shared__ uint32_t cur[kSortKeys], s_off[kSortKeys + 1], s_cnt[kSortKeys], s_g[kSortKeys + 1];
+  if (threadIdx.x < 32) key_tables(S, s_off, s_cnt, s_g);
+  __syncthreads();
+  for (int t = threadIdx.x; t < (int)kSortKeys; t += blockDim.x) cur[t] = s_off[t] + S.hist[t * S.nblk + blockIdx.x];
   __syncthreads();
   const uint64_t base = (uint64_t)blockIdx.x * S.chunk, end = min(n, base + S.chunk);
   const int lane = threadIdx.x & 31;
@@ -158,12 +123,12 @@ __global__ void __launch_bounds__(256) k_sort_scatter(uint64_t n, SortScratch S)
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-      kk[u] = i < end ? S.keys[i] : kSortNoKey;
+      kk[u] = S.keys[min(i, end - 1)];  // unconditional: all loads in flight
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const uint64_t i = i0 + u * blockDim.x + threadIdx.x;
-      const uint32_t key = kk[u];
+      const uint32_t key = i < end ? kk[u] : kSortNoKey;
       const unsigned peers = __match_any_sync(0xffffffffu, key);
       const int leader = 31 - __clz(peers);
       uint32_t b = 0;
@@ -181,12 +146,7 @@ __global__ void __launch_bounds__(kSortThreads, 1)
   extern __shared__ __align__(128) unsigned char smem[];
   __shared__ uint32_t s_off[kSortKeys + 1], s_cnt[kSortKeys], s_g[kSortKeys + 1];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int t = tid; t < (int)kMetaClaim; t += kSortThreads) {
-    const uint32_t v = S.meta[t];
-    if (t < (int)kMetaCnt) s_off[t] = v;
-    else if (t < (int)kMetaG) s_cnt[t - kMetaCnt] = v;
-    else s_g[t - kMetaG] = v;
-  }
+  if (tid < 32) key_tables(S, s_off, s_cnt, s_g);
   __syncthreads();
   const uint32_t ngroups = s_g[kSortKeys];
   unsigned char* slot = smem + ((size_t)warp * 32 + lane) * kSortSlot;

@@ -220,6 +220,7 @@ constexpr int kWideElemBytes = 32;
 constexpr uint32_t kSortKeys = kPipeKeys;  // grouping keys of the module (<= 64)
 constexpr uint32_t kSortNoKey = 0xFF;      // final code in S1, not sorted
 constexpr int kSortScanThreads = 1024;
+constexpr int kSortBlock = 512;  // threads of S1 / S3
 constexpr uint32_t kSortMaxBlk = 32 * 24;  // blocks of S1 / S3 (kSortMaxPer per scan lane)
 constexpr uint32_t kSortMaxPer = kSortMaxBlk / 32;
 
@@ -227,13 +228,12 @@ constexpr uint32_t kSortMaxPer = kSortMaxBlk / 32;
 struct SortScratch {
   uint8_t* keys;   // [n]
   uint32_t* perm;  // [n]: key-sorted position -> record
-  uint32_t* hist;  // [kSortKeys * nblk]: (key, block) counts, scanned in place by S2
-  uint32_t* meta;  // key_off[kSortKeys + 1] | key_cnt[kSortKeys] | gstart[kSortKeys + 1] | claim
+  uint32_t* hist;  // [kSortKeys * nblk]: offset of (key, block) within the key (S1 atomics)
+  uint32_t* meta;  // key totals [kSortKeys] | claim counter (zeroed before S1)
   uint32_t nblk;   // blocks of S1 / S3
   uint32_t chunk;  // records per block (a multiple of 32)
 };
-constexpr uint32_t kMetaOff = 0, kMetaCnt = kSortKeys + 1, kMetaG = 2 * kSortKeys + 1,
-                   kMetaClaim = 3 * kSortKeys + 2, kMetaWords = 3 * kSortKeys + 3;
+constexpr uint32_t kMetaTot = 0, kMetaClaim = kSortKeys, kMetaWords = kSortKeys + 16;  // key totals, claim counter
 
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind
