@@ -66,7 +66,13 @@ def dist_env():
 # name -> (base generator kwargs, default replicas, description); SURVEY §8F / BASELINE.json configs
 WORKLOADS = {
     "c2": (dict(), REPLICAS,
-           "C2 paper-shaped trace (547 kernels / 18,217 instances / 6 apps)"),
+           "C2 paper-shaped trace (547 kernels / 18,217 instances / 6 apps; ~0.4 % precondition and ~0.6 % "
+           "global-condition violations, SURVEY §8F)"),
+    "c2r1": (dict(violations=False), REPLICAS,
+             "C2 paper-shaped trace, round-1 mix (547 kernels / 18,217 instances / 6 apps, no planted violations)"),
+    "c2heavy": (dict(heavy=True), 560,
+                "C2-heavy (547 kernels / 18,217 instances / 6 apps; a third of the PyTorch / TensorRT / FT COND "
+                "kernels heavily fused: up to 32 descriptors, R x W up to 112)"),
     "c3": (dict(n=1 << 14, n_kernels=64), 64,
            "C3 TVM-style tiled GEMM/conv kernels with affine strided ranges (64 kernels, 16,384-record base)"),
     "c4": (dict(n=1 << 13, n_kernels=32), 512,
@@ -80,22 +86,42 @@ WORKLOADS = {
 def make_base(workload):
     from tracegen import workloads as W
     kw = WORKLOADS[workload][0]
-    return {"c2": W.make_c2, "c3": W.make_c3, "c4": W.make_c4, "wide": W.make_wide}[workload](**kw)
+    return {"c2": W.make_c2, "c2r1": W.make_c2, "c2heavy": W.make_c2, "c3": W.make_c3, "c4": W.make_c4,
+            "wide": W.make_wide}[workload](**kw)
 
 
 def workload_config(args, world, n_base=None, flush=False):
     kw, _, desc = WORKLOADS[args.workload]
-    n_base = n_base or (18217 if args.workload == "c2" else kw["n"])
+    n_base = n_base or (18217 if args.workload.startswith("c2") else kw["n"])
     return {
         "workload": f"{desc} tiled x{args.replicas} per GPU with pointer relocation"
                     + (" (C5 stream)" if world > 1 and args.workload == "c2" else ""),
+        "mix": summary_mix(args.workload),
         "records_per_gpu": n_base * args.replicas,
         "records_total": n_base * args.replicas * world,
-        "seed": {"c2": 23661, "c3": 23662, "c4": 23663, "wide": 23665}[args.workload],
+        "seed": {"c2": 23661, "c2r1": 23661, "c2heavy": 23661, "c3": 23662, "c4": 23663, "wide": 23665}[args.workload],
         "l2": "L2 flushed (512 MB write) before every timed step" if flush
               else "inputs > 6x the 126 MB L2 per GPU, no flush needed",
         "parallelism": f"dp{world} (instance shards, all-gather of flag bits)" if world > 1 else "single GPU",
     }
+
+
+_MIX = {}
+
+
+def summary_mix(workload):
+    """Mean / max descriptors and read x write pairs of the COND kernels, mean
+    bytes per record (header + args + code + bit) of the base trace."""
+    if workload not in _MIX:
+        s, rec, a, _ = make_base(workload)
+        cond = [k for k in s["kernels"] if k["class"] == "COND"]
+        nd = [len(k["desc"]) for k in cond]
+        rw = [sum(d["kind"] == "R" for d in k["desc"]) * sum(d["kind"] == "W" for d in k["desc"]) for k in cond]
+        _MIX[workload] = {"cond_kernels": len(cond), "descriptors_mean": round(float(np.mean(nd)), 2),
+                          "descriptors_max": int(max(nd)), "rxw_mean": round(float(np.mean(rw)), 2),
+                          "rxw_max": int(max(rw)),
+                          "bytes_per_record": round(algorithmic_bytes(rec, a) / len(rec), 2)}
+    return _MIX[workload]
 
 
 def algorithmic_bytes(rec, args):
@@ -267,7 +293,7 @@ def run_reference(args):
     import oracle.picker_oracle as O
 
     s, rec, a, meta = make_base(args.workload)
-    if args.workload != "c2":
+    if not args.workload.startswith("c2"):
         rec = rec[:2048]  # bounded sample: the oracle takes ~ms per many-descriptor record
     cores = os.cpu_count() or 1
     for _ in range(args.warmup):
@@ -346,7 +372,7 @@ def main():
     got = flags.cpu().numpy()
     mism = int((got != np.tile(base_codes, args.replicas)).sum())
     # plus a directly-checked random sample of the relocated records
-    idx = np.random.default_rng(rank).choice(n, size=2000 if args.workload == "c2" else 200, replace=False)
+    idx = np.random.default_rng(rank).choice(n, size=2000 if args.workload.startswith("c2") else 200, replace=False)
     direct = np.array(O.oracle_batch(s, rec[idx], a), np.uint8)
     mism += int((direct != got[idx]).sum())
 

@@ -127,7 +127,7 @@ struct Gen {
 // class has at least kLoopMin members: many-pointer kernels (C4) otherwise
 // emit one straight-line block per descriptor, and a shape of ~4,000 SASS
 // instructions does not fit the 32 KB instruction cache.
-constexpr size_t kLoopMin = 3;
+constexpr size_t kLoopMin = 3, kLoopKernelMin = 12;  // class size; streamed descriptors of the kernel
 uint64_t fnv1a(const std::string& s);
 
 std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs) {
@@ -370,8 +370,10 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
   }
   std::vector<char> in_loop(k.desc.size(), 0);
   bool any_loop = false;
+  size_t nstreamed = 0;
+  for (auto& e : cls) nstreamed += e.second.size();
   for (auto& e : cls)
-    if (e.second.size() >= kLoopMin) {
+    if (e.second.size() >= kLoopMin && nstreamed >= kLoopKernelMin) {
       any_loop = true;
       for (int di : e.second) in_loop[di] = 1;
     }
@@ -398,7 +400,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
   }
   for (const std::string& key : cls_order) {  // the streamed side, loop classes
     const std::vector<int>& mem = cls[key];
-    if (mem.size() < kLoopMin) continue;
+    if (!in_loop[mem[0]]) continue;
     const int d0 = mem[0];
     std::string idx;
     for (int di : mem)  // argument index | (width - 1) << 8

@@ -143,6 +143,10 @@ def t_rowop(rng, *, kind=None):
                desc("R", w, "beta", [term(w, (), "ind0")], vi)]
     pre = ptr_pre([p for p, k in params if k == "ptr"]) + [{"op": "M", "lo": 1, "hi": 1 << 16}]
     bdim = rng_pick(rng, [128, 256, 1024])
+    # each thread keeps its M / bdim columns in registers: the loop is unrolled
+    # at most 32 times, so the summary holds only while M <= 32 bdim (the
+    # global condition of an unbounded loop)
+    glob = [{"op": "M", "lo": 1, "hi": 32 * bdim}]
 
     def sample(rng, st):
         M = st.hidden
@@ -153,7 +157,7 @@ def t_rowop(rng, *, kind=None):
             ptrs[0] = ptrs[1]  # in-place normalisation
         return ptrs + [M], (R, 1, 1), (bdim, 1, 1)
 
-    return (kind, params, ds, pre, []), sample
+    return (kind, params, ds, pre, glob), sample
 
 
 def t_stencil2d(rng):
@@ -453,6 +457,72 @@ def t_multi_tensor(rng, *, kind=None, ntensor=None):
     return (f"mt_{kind}", params, descs, pre, []), sample
 
 
+def t_fused_heavy(rng):
+    """Heavily fused kernel of a DL framework (C2-heavy, SURVEY §8F "2-40
+    descriptors per COND kernel, R x W of 4-100"): residual + bias + norm +
+    activation + dropout-style fusions reading 6-30 tensors of an [R, H] layout
+    (full tensors at row bid, per-column vectors), writing 2-4 outputs (full
+    tensors and per-row statistics)."""
+    w = rng_pick(rng, [2, 4])
+    nfull = int(rng.integers(3, 16))
+    nvec = int(rng.integers(3, 15))
+    nout = int(rng.integers(2, 5))
+    ins = [f"x{i}" for i in range(nfull)] + [f"v{i}" for i in range(nvec)]
+    outs = [f"y{i}" for i in range(nout)]
+    params = [(p, "ptr") for p in outs + ins] + [("H", "i32")]
+    v = {"bid.x": {"lo": [], "hi": []}, "ind0": {"lo": [bx(0)], "hi": [bx(-1, (1, ["H"]))]}}
+    vv = {"ind0": {"lo": [bx(0)], "hi": [bx(-1, (1, ["H"]))]}}
+    row = [term(w, ("H",), "bid.x"), term(w, (), "ind0")]
+    ds = [desc("R", w, f"x{i}", row, v) for i in range(nfull)]
+    ds += [desc("R", w, f"v{i}", [term(w, (), "ind0")], vv) for i in range(nvec)]
+    for j in range(nout):
+        if j == nout - 1 and nout > 2:  # per-row statistic (mean / rstd)
+            ds.append(desc("W", 4, f"y{j}", [term(4, (), "bid.x")], {"bid.x": {"lo": [], "hi": []}}))
+        else:
+            ds.append(desc("W", w, f"y{j}", row, v))
+    pre = ptr_pre(outs + ins) + [{"op": "H", "lo": 1, "hi": 1 << 16}]
+    bdim = rng_pick(rng, [128, 256, 512])
+
+    def sample(rng, st):
+        H = st.hidden
+        R = st.rows(rng)
+        ptrs = st.bufs(outs + ins, R * H * w, small={**{f"v{i}": H * w for i in range(nvec)}, outs[-1]: R * 4})
+        if st.alias(rng):  # in-place residual update
+            ptrs[0] = ptrs[nout + int(rng.integers(0, nfull))]
+        return ptrs + [H], (R, 1, 1), (bdim, 1, 1)
+
+    return ("fused_heavy", params, ds, pre, []), sample
+
+
+def _violate(prng, k, args, p_pre, p_glob):
+    """~0.5 % of the launches break a precondition (PAPER.md
+    l.976-979: a value outside the range the analyzer assumed) and loop kernels
+    sometimes run past their global condition (l.743-752): an argument set just
+    past the bound of one check, kept inside every other check on it.  Inputs
+    only: the code these launches get is the oracle's business."""
+    names = [p["name"] for p in k["params"]]
+    kinds = {p["name"]: p["kind"] for p in k["params"]}
+
+    def typemax(nm):
+        return I32_HI if kinds[nm] == "i32" else (1 << 63) - 1
+
+    if k["glob"] and prng.random() < p_glob:
+        c = k["glob"][int(prng.integers(0, len(k["glob"])))]
+        if c["op"] in kinds:
+            v = c["hi"] + 1
+            if v <= typemax(c["op"]) and all(pc["lo"] <= v <= pc["hi"] for pc in k["pre"] if pc["op"] == c["op"]):
+                args = list(args)
+                args[names.index(c["op"])] = v
+                return args
+    if prng.random() < p_pre:
+        cs = [c for c in k["pre"] if c["op"] in kinds and c["hi"] + 1 <= typemax(c["op"])]
+        if cs:
+            c = cs[int(prng.integers(0, len(cs)))]
+            args = list(args)
+            args[names.index(c["op"])] = c["hi"] + 1
+    return args
+
+
 def t_shortcut(rng, cls, reason=None):
     """Kernel-level I / NI kernels: memset-like writes; the
     validator returns their class without computing."""
@@ -541,10 +611,21 @@ def _finish(kid, name, params, ds, pre, glob, cls="COND", reason=None):
     return kernel(kid, name, params, ds, pre=pre, glob=glob, cls=cls, reason=reason)
 
 
-def make_c2(seed=23661):
+# launch shares of the SURVEY §8F boundary cases (separate generator stream,
+# so the rest of the trace is the same with or without them)
+P_PRE_VIOLATION = 0.005
+P_GLOB_VIOLATION = 0.05
+
+
+def make_c2(seed=23661, violations=True, heavy=False):
     """C2: returns (summary, rec, args, meta) with meta['app'][i] the app index
-    of record i and meta['ptr_mask'] marking pointer argument slots."""
+    of record i and meta['ptr_mask'] marking pointer argument slots.
+    ``violations``: plant ~0.5 % precondition violations and global-condition
+    violations on loop kernels (False gives round 1's mix).
+    ``heavy``: C2-heavy, a third of the PyTorch / TensorRT / FT COND kernels
+    are heavily fused (6-30 reads, 2-4 writes: up to 34 descriptors)."""
     rng = np.random.default_rng(seed)
+    prng = np.random.default_rng(seed + 1000)  # boundary cases (violations / heavy choice)
     alloc = Alloc(rng)
     kernels, rows_app, launches = [], [], []
     kid = 0
@@ -564,7 +645,9 @@ def make_c2(seed=23661):
                 short = True
             else:
                 menu = MENUS[app]
-                if app == "TVM" and rng.random() < 0.015:
+                if heavy and app in ("PyTorch", "TensorRT", "FT") and prng.random() < 1 / 3:
+                    (nm, p, d, pre, gl), smp = t_fused_heavy(prng)
+                elif app == "TVM" and rng.random() < 0.015:
                     (nm, p, d, pre, gl), smp = t_gemm_tvm(rng, concat=True)
                 else:
                     (nm, p, d, pre, gl), smp = menu[int(rng.integers(0, len(menu)))](rng)
@@ -602,6 +685,8 @@ def make_c2(seed=23661):
             st.step = step % 1024
             k_id, smp, short, k, _ = samplers[j]
             args, grid, block = smp(rng, st)
+            if violations and not short:
+                args = _violate(prng, k, args, P_PRE_VIOLATION, P_GLOB_VIOLATION)
             b.add(k_id, args, grid=grid, block=block)
             rows_app.append(ai)
             ptr_mask.extend(p["kind"] == "ptr" for p in k["params"])
