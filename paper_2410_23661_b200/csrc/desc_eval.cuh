@@ -252,9 +252,11 @@ static __device__ bool scratch_sweep(const WideElem* e, uint32_t np2, int lane) 
 }
 
 // Verdict of one record, computed by the whole warp (all lanes return it).
-// `scratch`: this warp's kWideMax elements (nullptr: pairwise for > 64).
+// `scratch`: this warp's `cap` elements (shared or global memory; nullptr:
+// pairwise for > 64 descriptors).
 static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r, const int64_t* a,
-                                         uint64_t alo, uint64_t ahi, int lane, WideElem* scratch) {
+                                         uint64_t alo, uint64_t ahi, int lane, WideElem* scratch,
+                                         uint32_t cap = kWideMax) {
   // prefix (Fig. 3 order); the preconditions / global condition are split over
   // the lanes: the first failing check in order decides (pre before glob)
   const uint32_t kid = r.kernel_id;
@@ -280,12 +282,13 @@ static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r,
   // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags,
   // extents (registers for <= 64 descriptors, else element d of the scratch)
   const bool in_regs = K.ndesc <= 64;
-  const bool in_scratch = !in_regs && scratch != nullptr && K.ndesc <= kWideMax;
+  const bool in_scratch = !in_regs && scratch != nullptr && K.ndesc <= cap;
   const uint32_t np2 = in_scratch ? max(64u, 1u << (32 - __clz((uint32_t)K.ndesc - 1))) : 0u;
   bool act_r = false, act_w = false, opq_r = false, opq_w = false;
   Ext e[2];
   e[0].kind = e[1].kind = 2;
   e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
+#pragma unroll 2
   for (int d = lane, k = 0; d < (in_scratch ? (int)np2 : K.ndesc); d += 32, ++k) {
     WideElem x{0, 0, 2, 0, 0};
     if (d < K.ndesc) {

@@ -53,9 +53,11 @@ void select_paths(std::vector<IrKernel>& ks, const Options& opt) {
   }
 }
 
+// The specialised module is built when some kernel is specialised or wide
+// (wide kernels run warp-cooperatively inside the module's schedules).
 bool any_jit(const std::vector<IrKernel>& ks) {
   for (auto& k : ks)
-    if (k.path == PATH_JIT) return true;
+    if (k.path == PATH_JIT || k.path == PATH_WIDE) return true;
   return false;
 }
 

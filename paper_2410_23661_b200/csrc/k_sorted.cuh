@@ -189,8 +189,12 @@ __global__ void __launch_bounds__(kSortThreads, 1)
       for (uint32_t q = 0; q < rem; ++q) {
         const uint32_t wi = __shfl_sync(0xffffffffu, pi, q);
         const picker_rec_t r = load_rec(B.rec + wi);
+        // the warp's argument slots (unused by K2) hold its sort scratch
+        const bool in_smem = P.T.kernels[r.kernel_id < P.T.nkernel_slots ? r.kernel_id : 0].ndesc <= kSortSlot;
         const uint8_t c = eval_wide_warp(P.T, r, B.args + r.arg_off, B.args_lo, B.args_hi, lane,
-                                         wide_scratch(P, warp));
+                                         in_smem ? reinterpret_cast<WideElem*>(smem + (size_t)warp * 32 * kSortSlot)
+                                                 : wide_scratch(P, warp),
+                                         in_smem ? kSortSlot : (uint32_t)kWideMax);
         if (lane == 0) flags[wi] = c;
       }
     } else if ((uint32_t)lane < rem) {
