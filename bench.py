@@ -1,18 +1,20 @@
 """Benchmark: batched instance-level idempotency validation on B200.
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c2|...]
     python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 \
         --master-port P bench.py --gpus N ...
 
 Workload: the C2 trace shaped like the paper's evaluation
-(547 kernels / 18,217 instances / 6 apps, Table 3) tiled to
-12,495,862 records per GPU (686 replicas, each relocating every pointer by
-r * 2^37; verdicts are translation invariant).  At 8 GPUs that is
-the 100M-instance stream of BASELINE.json's C5.  One step = one
-picker_validate_batch over the rank's whole shard (plus, for N > 1, the NCCL
-all-gather of the bit-packed flags and all-reduce of the counts).  Inputs
-(~0.83 GB per GPU) are 6.6x the 126 MB L2, so no L2 flush is needed between
-steps.
+(547 kernels / 18,217 instances / 6 apps, Table 3, with SURVEY §8F's
+planted precondition / global-condition violations) tiled to 12,496,862
+records per GPU (686 replicas, generated on the GPU by K6 = picker_replicate,
+each relocating every pointer by r * 2^37; verdicts are translation
+invariant).  At 8 GPUs that is the 100M-instance stream of
+BASELINE.json's C5.  One step = one picker_validate_batch over the rank's
+whole shard; for N > 1 the shard is validated in --chunks chunks whose
+bit-mask all-gathers (NCCL) overlap the next chunk's validation, then one
+all-reduce of the counts.  Inputs (~0.83 GB per GPU) are 6.6x the 126 MB L2,
+so no L2 flush is needed between steps (smaller workloads get one).
 
 Rank 0 prints one JSON line.  `--impl reference` times the CPU oracle
 (oracle/, test infrastructure) on the host cores on bounded samples of the same
@@ -48,6 +50,7 @@ def parse():
     ap.add_argument("--replicas", type=int, default=None, help="default: per workload")
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--chunks", type=int, default=4, help="N > 1: chunks whose all-gathers overlap validation")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-latency", action="store_true", help="skip the small-batch latency probe")
     ap.add_argument("--oracle-seconds", type=float, default=12.0)
@@ -102,7 +105,8 @@ def workload_config(args, world, n_base=None, flush=False):
         "seed": {"c2": 23661, "c2r1": 23661, "c2heavy": 23661, "c3": 23662, "c4": 23663, "wide": 23665}[args.workload],
         "l2": "L2 flushed (512 MB write) before every timed step" if flush
               else "inputs > 6x the 126 MB L2 per GPU, no flush needed",
-        "parallelism": f"dp{world} (instance shards, all-gather of flag bits)" if world > 1 else "single GPU",
+        "parallelism": f"dp{world} (instance shards generated on each GPU by K6; chunked all-gather of flag bits "
+                       f"overlapped with validation, all-reduce of counts)" if world > 1 else "single GPU",
     }
 
 
@@ -186,18 +190,6 @@ class ClockSampler:
                           if r[2 + i].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(sm)}
-
-
-def build_inputs(args, rank):
-    from tracegen.workloads import replicate
-
-    s, rec, a, meta = make_base(args.workload)
-    # this rank's replicas: r in [rank*R, (rank+1)*R)
-    R = args.replicas
-    rr, aa = replicate(rec, a, meta["ptr_mask"], R, DELTA)
-    if rank:
-        aa = aa + np.tile(meta["ptr_mask"].astype(np.int64), R) * (rank * R * DELTA)
-    return s, rec, a, meta, rr, aa
 
 
 def cpu_baseline(s, rec, a, seconds):
@@ -338,8 +330,6 @@ def main():
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
-    s, base_rec, base_args, meta, rec, a = build_inputs(args, rank)
-    n = len(rec)
     opts = {}
     if args.path == "generic":
         opts["jit"] = 0
@@ -347,21 +337,36 @@ def main():
         k, v = kv.split("=")
         opts[k] = int(v)
     p = pk.Picker(local, **opts)
+    # the rank's shard, generated on its GPU (K6, picker_replicate): replicas
+    # [rank*R, (rank+1)*R) of the base trace, every pointer moved by r * DELTA
+    s, base_rec, base_args, meta = make_base(args.workload)
+    rec_d, args_d = p.replicate(base_rec, base_args, meta["ptr_mask"], args.replicas,
+                                first_copy=rank * args.replicas, delta=DELTA)
+    rec = rec_d.cpu().numpy().reshape(-1).view(base_rec.dtype)  # host copies: samples, e2e
+    a = args_d.cpu().numpy()
+    n = len(rec)
     p.load(s)
     paths = p.kernel_paths()
-    rec_d = torch.from_numpy(rec.view(np.uint8).reshape(-1, 32)).to(dev)
-    args_d = torch.from_numpy(a).to(dev)
     flags = torch.empty(n, dtype=torch.uint8, device=dev)
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     counts = torch.empty(16, dtype=torch.int64, device=dev)
     stream = torch.cuda.current_stream()
     n_total = n * world
 
+    # N > 1: the shard in chunks, each chunk's bit all-gather overlapped with the
+    # next chunk's validation on a second stream (dist.ChunkedExchange)
+    ex = pdist.ChunkedExchange(p, n, args.chunks, dev) if world > 1 else None
+
+    def validate_step():
+        if ex is not None:
+            ex.run(rec_d, args_d)
+            flags.copy_(ex.flags)
+            counts.copy_(ex.counts)
+        else:
+            p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
+
     def step():
-        p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
-        if world > 1:
-            pdist.gather_bits_equal(bits)
-            pdist.reduce_counts(counts)
+        validate_step()
 
     # parity of the timed configuration: the base trace's oracle codes, tiled (G9)
     step()
@@ -399,12 +404,9 @@ def main():
             scratch.zero_()  # evict the inputs from L2 (outside the step's events)
         ev[i][0].record(stream)
         kev[i][0].record(stream)
-        p.validate(rec_d, args_d, out=(flags, bits, counts), stream=stream)
+        validate_step()
         kev[i][1].record(stream)
-        launches += p.last_launch_count()
-        if world > 1:
-            pdist.gather_bits_equal(bits)
-            pdist.reduce_counts(counts)
+        launches += p.last_launch_count() * (len(ex.bounds) if ex is not None else 1)
         ev[i][1].record(stream)
     t_all1.record(stream)
     torch.cuda.synchronize()

@@ -185,6 +185,22 @@ int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t 
                        uint8_t* exact_out, uint64_t* counts_out,
                        uint64_t max_points_per_instance, void* stream);
 
+/* Device-side replication of a launch-record stream (K6; SURVEY §8F C5 and
+ * §8 row e: shards generated on the GPU instead of copied over PCIe).  Writes
+ * `copies` copies of the n base records and their argument pool: record
+ * c*n + i is base record i with arg_off + c*args_len; slot c*args_len + j is
+ * args[j] + (ptr_mask[j] ? (first_copy + c) * delta : 0).  Moving every
+ * pointer argument of an instance by the same amount keeps its verdict
+ * (translation invariance) as long as the preconditions still
+ * hold -- the caller picks delta.  All pointers are DEVICE pointers: batch->rec
+ * (n records), batch->args (args_len slots), ptr_mask (args_len bytes),
+ * rec_out (n*copies records, 16-byte aligned), args_out (args_len*copies
+ * slots).  Asynchronous on `stream`.  PICKER_EINVAL on null / misaligned
+ * pointers or more than 2^40 output records.                                   */
+int picker_replicate(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n, const uint8_t* ptr_mask,
+                     uint64_t copies, uint64_t first_copy, int64_t delta, picker_rec_t* rec_out,
+                     int64_t* args_out, void* stream);
+
 /* Multi-kernel idempotency: the stream is cut into
  * consecutive windows of `window` launches (1..1024; record order = launch
  * order) and each window is validated as one unit.  mode 0 (sequential list):

@@ -62,6 +62,8 @@ SIGNATURES = {
     "picker_validate_batch_host": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P,
                                                   P]),
     "picker_exact_check": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, U64, P]),
+    "picker_replicate": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, U64, U64, ctypes.c_int64, P, P,
+                                        P]),
     "picker_validate_sequence": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, ctypes.c_uint32,
                                                 ctypes.c_uint32, P, P]),
     "picker_consumer_models": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P,

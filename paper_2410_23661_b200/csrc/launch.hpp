@@ -84,4 +84,8 @@ cudaError_t launch_exact(const Tables& T, const DevBatch& b, uint64_t n, uint8_t
                          void** arena, size_t* arena_bytes, int num_sms, cudaStream_t s, int* launches,
                          std::string& err);
 
+cudaError_t launch_replicate(const picker_rec_t* rec, uint64_t n, const int64_t* args, uint64_t args_len,
+                             const uint8_t* ptr_mask, uint64_t copies, uint64_t first, int64_t delta,
+                             picker_rec_t* rec_out, int64_t* args_out, int num_sms, cudaStream_t s);
+
 }  // namespace picker

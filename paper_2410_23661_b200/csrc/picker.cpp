@@ -500,6 +500,21 @@ int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
   return PICKER_OK;
 }
 
+int picker_replicate(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, const uint8_t* ptr_mask,
+                     uint64_t copies, uint64_t first_copy, int64_t delta, picker_rec_t* rec_out, int64_t* args_out,
+                     void* stream) {
+  if (!c || !b || (n && (!b->rec || !rec_out)) || (b->args_len && copies && (!b->args || !ptr_mask || !args_out)))
+    return fail(c, PICKER_EINVAL, "replicate: null pointer");
+  if (((uintptr_t)b->rec | (uintptr_t)rec_out) & 15) return fail(c, PICKER_EINVAL, "replicate: records not 16-B aligned");
+  if (copies && n > (1ULL << 40) / copies) return fail(c, PICKER_EINVAL, "replicate: more than 2^40 records");
+  DevGuard g(c->device);
+  cudaError_t e = launch_replicate(b->rec, n, b->args, b->args_len, ptr_mask, copies, first_copy, delta, rec_out,
+                                   args_out, c->num_sms, (cudaStream_t)stream);
+  if (e != cudaSuccess) return cuda_fail(c, e, "replicate");
+  c->last_launches = n && copies ? (b->args_len ? 2 : 1) : 0;
+  return PICKER_OK;
+}
+
 int picker_exact_check(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* out,
                        uint64_t* counts, uint64_t max_points, void* stream) {
   int st = check_batch(c, b, n, out);

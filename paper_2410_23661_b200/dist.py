@@ -71,3 +71,70 @@ def validate_sharded(picker, rec_shard, args_shard, n_total: int, *, stream=None
     gbits = gather_bits(bits, n_total, group)
     gcounts = reduce_counts(counts, group)
     return flags, gbits, gcounts
+
+
+class ChunkedExchange:
+    """Validation of a rank's shard in chunks, each chunk's flag-bit all-gather
+    overlapped with the next chunk's validation (SURVEY §8 row e: "chunked
+    overlap on a second stream hides the rest").
+
+    Every rank holds a shard of the same number of records, split into
+    `nchunks` chunks of whole 32-record words.  Chunk c is validated on the
+    compute stream; an event marks its end; the communication stream waits for
+    it and all-gathers the chunk's bit words into their final place in the
+    global mask (rank-major: rank r's shard is records [r*n_local, (r+1)*n_local)),
+    while chunk c+1 is already validating.  The counts are all-reduced once.
+    On CPU (gloo) the streams are absent and the same calls run in order.
+    """
+
+    def __init__(self, picker, n_local: int, nchunks: int, device, group=None):
+        self.p = picker
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.n_local = n_local
+        self.words = (n_local + 31) // 32
+        per = (self.words + nchunks - 1) // max(nchunks, 1)
+        self.bounds = [(w * 32, min(n_local, (w + per) * 32)) for w in range(0, self.words, per)] or [(0, 0)]
+        self.device = torch.device(device)
+        cuda = self.device.type == "cuda"
+        self.comm = torch.cuda.Stream(self.device) if cuda else None
+        self.flags = torch.empty(n_local, dtype=torch.uint8, device=self.device)
+        self.bits = torch.empty(self.words, dtype=torch.int32, device=self.device)
+        self.counts = torch.empty(16, dtype=torch.int64, device=self.device)
+        self.chunk_counts = torch.empty(len(self.bounds), 16, dtype=torch.int64, device=self.device)
+        self.gbits = torch.empty(self.world * self.words, dtype=torch.int32, device=self.device)
+
+    def _views(self, c):
+        lo, hi = self.bounds[c]
+        w0, w1 = lo // 32, (hi + 31) // 32
+        return [self.gbits[r * self.words + w0: r * self.words + w1] for r in range(self.world)]
+
+    def run(self, rec, args, *, validate=None):
+        """Validate `rec` (this rank's shard, device records) chunk by chunk and
+        exchange.  Returns (local flags, global bits i32[world * words], global
+        counts i64[16]); all valid on the current stream after the call.
+        `validate(rec_chunk, out)` overrides the picker call (tests)."""
+        cur = torch.cuda.current_stream(self.device) if self.comm is not None else None
+        works = []
+        for c, (lo, hi) in enumerate(self.bounds):
+            out = (self.flags[lo:hi], self.bits[lo // 32:(hi + 31) // 32], self.chunk_counts[c])
+            if validate is None:
+                self.p.validate(rec[lo:hi], args, out=out, stream=cur)
+            else:
+                validate(rec[lo:hi], out)
+            if self.comm is not None:
+                ev = torch.cuda.Event()
+                ev.record(cur)
+                self.comm.wait_event(ev)
+                with torch.cuda.stream(self.comm):
+                    works.append(dist.all_gather(self._views(c), out[1], group=self.group, async_op=True))
+            else:
+                dist.all_gather(self._views(c), out[1], group=self.group)
+        for w in works:
+            w.wait()
+        if self.comm is not None:
+            cur.wait_stream(self.comm)
+        torch.sum(self.chunk_counts, dim=0, out=self.counts)
+        dist.all_reduce(self.counts, op=dist.ReduceOp.SUM, group=self.group)
+        return self.flags, self.gbits, self.counts

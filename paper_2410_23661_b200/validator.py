@@ -194,6 +194,26 @@ class Picker:
             _stream_handle(stream)))
         return out, cnt
 
+    def replicate(self, rec, args, ptr_mask, copies, *, first_copy=0, delta=1 << 37, stream=None):
+        """K6 (picker_replicate): `copies` relocated copies of a device-resident
+        trace, generated on the GPU.  rec: u8[n,32] / numpy records; args:
+        int64; ptr_mask: bool per argument slot.  Returns (rec u8[n*copies,32],
+        args int64[len(args)*copies]) on the device, queued on `stream`."""
+        rec = records_tensor(rec, self.device)
+        if not torch.is_tensor(args):
+            args = torch.from_numpy(np.asarray(args, dtype=np.int64))
+        args = args.to(self.device)
+        mask = ptr_mask if torch.is_tensor(ptr_mask) else torch.from_numpy(np.asarray(ptr_mask, dtype=np.uint8))
+        mask = mask.to(self.device, torch.uint8)
+        n = rec.shape[0]
+        rec_out = torch.empty((n * copies, 32), dtype=torch.uint8, device=self.device)
+        args_out = torch.empty(args.numel() * copies, dtype=torch.int64, device=self.device)
+        b = self._batch(rec, args, True)
+        self._check(lib.picker_replicate(self._h, ctypes.byref(b), n, mask.data_ptr() if mask.numel() else None,
+                                         int(copies), int(first_copy), int(delta), rec_out.data_ptr(),
+                                         args_out.data_ptr() if args_out.numel() else None, _stream_handle(stream)))
+        return rec_out, args_out
+
     def consumer_models(self, rec, args, codes, ctx_bytes=None, *, kill_ns=1000, save_bytes_per_us=1000,
                         stream=None):
         """Row f3 (picker_consumer_models): AR checkpoint bytes and Chimera

@@ -174,3 +174,24 @@ def test_contradictory_preconditions(pk, opt):
     assert set(want[1::3]) == {7}
     flags, bits, counts = _run(pk, s, rec, args, **opt)
     _check(flags, bits, counts, want)
+
+
+def test_device_replication(pk, c2):
+    """K6 (picker_replicate) writes exactly the host generator's relocated
+    copies (tracegen.workloads.replicate), and their verdicts are the base
+    trace's tiled."""
+    s, rec, args, meta, want = c2
+    p = pk.Picker(0)
+    p.load(s)
+    R, first = 7, 3
+    rd, ad = p.replicate(rec, args, meta["ptr_mask"], R, first_copy=first, delta=1 << 37)
+    hr, ha = workloads.replicate(rec, args, meta["ptr_mask"], R + first)
+    hr, ha = hr[first * len(rec):], ha[first * len(args):]  # host copies first .. first + R - 1
+    got = rd.cpu().numpy().reshape(-1).view(hr.dtype)
+    for f in hr.dtype.names:  # device copy c: arg_off + c * len(args); host copy first + c
+        want_f = hr[f] - first * len(args) if f == "arg_off" else hr[f]
+        assert np.array_equal(got[f], want_f), f
+    assert np.array_equal(ad.cpu().numpy(), ha)
+    flags, bits, counts = p.validate(rd, ad)
+    _check(flags, bits, counts, np.tile(want, R))
+    p.close()
