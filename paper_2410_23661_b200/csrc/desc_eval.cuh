@@ -212,43 +212,59 @@ static __device__ bool desc_active_extent(const Tables& T, const DKernel& K, con
   return true;
 }
 
-static __device__ __forceinline__ bool elem_less(const WideElem& a, const WideElem& b) {
-  return a.kind != 2 && (b.kind == 2 || a.lb < b.lb);
-}
+// Scratch layout of the > 64-descriptor path (16-byte intervals):
+//   S[0, ns2)   the smaller kind's extents, sorted by lb (ns2 = pow2 >= 32;
+//               padding lb = INT64_MAX), then their exclusive-of-nothing
+//   M[0, ns2)   prefix maxima of ub in that order (int64),
+//   L[0, nl)    the other kind's extents.
+// An extent x of the larger kind overlaps some sorted extent iff, for the
+// last sorted index i with lb_i <= x.ub, max(ub_0..ub_i) >= x.lb (closed
+// intervals) -- the sweep line's running maximum, read by binary search.
+struct Iv64 {
+  int64_t lb, ub;
+};
 
-// Bitonic sort of the warp's scratch [0, np2) (np2 a power of two >= 64).
-static __device__ void scratch_sort(WideElem* e, uint32_t np2, int lane) {
-  for (uint32_t k = 2; k <= np2; k <<= 1) {
+// Bitonic sort of S[0, n2) by lb, ascending (n2 a power of two >= 32).
+static __device__ void iv_sort(Iv64* S, uint32_t n2, int lane) {
+  for (uint32_t k = 2; k <= n2; k <<= 1) {
     for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-      // pair p: i = p with bit j inserted as 0, partner i | j
-      for (uint32_t p = lane; p < np2 / 2; p += 32) {
+      for (uint32_t p = lane; p < n2 / 2; p += 32) {  // pair p: index with bit j cleared, partner | j
         const uint32_t i = ((p & ~(j - 1)) << 1) | (p & (j - 1)), q = i | j;
-        const WideElem a = e[i], b = e[q];
-        const bool asc = (i & k) == 0;
-        if (asc ? elem_less(b, a) : elem_less(a, b)) e[i] = b, e[q] = a;
+        const Iv64 a = S[i], b = S[q];
+        const bool swap = ((i & k) == 0) ? b.lb < a.lb : a.lb < b.lb;
+        if (swap) S[i] = b, S[q] = a;
       }
       __syncwarp();
     }
   }
 }
 
-// Sweep of the sorted scratch [0, np2): exclusive prefix max of ub per kind.
-static __device__ bool scratch_sweep(const WideElem* e, uint32_t np2, int lane) {
-  const int64_t NEG = (-9223372036854775807LL - 1);
-  int64_t carry_r = NEG, carry_w = NEG;
-  for (uint32_t h = 0; h < np2; h += 32) {
-    const WideElem x = e[h + lane];
-    if (__all_sync(0xffffffffu, x.kind == 2)) break;  // padding sorts last
-    const int64_t vr = x.kind == 0 ? x.ub : NEG, vw = x.kind == 1 ? x.ub : NEG;
-    const int64_t ir = max64(warp_incl_max(vr, lane), carry_r), iw = max64(warp_incl_max(vw, lane), carry_w);
-    int64_t xr = __shfl_up_sync(0xffffffffu, ir, 1), xw = __shfl_up_sync(0xffffffffu, iw, 1);
-    if (lane == 0) xr = carry_r, xw = carry_w;
-    const bool hit = (x.kind == 0 && xw >= x.lb) || (x.kind == 1 && xr >= x.lb);
-    if (__any_sync(0xffffffffu, hit)) return true;
-    carry_r = __shfl_sync(0xffffffffu, ir, 31);
-    carry_w = __shfl_sync(0xffffffffu, iw, 31);
+// Does any of the nl extents L overlap one of the sorted extents S (prefix
+// maxima M)?  Lanes over L, binary search in S.
+static __device__ bool iv_probe(const Iv64* S, const int64_t* M, uint32_t n2, const Iv64* L, uint32_t nl,
+                                int lane) {
+  bool hit = false;
+  for (uint32_t x = lane; x < nl; x += 32) {
+    const Iv64 e = L[x];
+    // last index i with S[i].lb <= e.ub (padding sorts last with lb = INT64_MAX)
+    int lo = -1;
+    for (uint32_t step = n2 >> 1; step > 0; step >>= 1)
+      if (S[lo + (int)step].lb <= e.ub) lo += (int)step;
+    if (lo + 1 < (int)n2 && S[lo + 1].lb <= e.ub) ++lo;
+    if (lo >= 0 && M[lo] >= e.lb) hit = true;
   }
-  return false;
+  return __any_sync(0xffffffffu, hit);
+}
+
+// Prefix maxima of ub over the sorted S (32 at a time, carried).
+static __device__ void iv_prefix_max(const Iv64* S, int64_t* M, uint32_t n2, int lane) {
+  int64_t carry = (-9223372036854775807LL - 1);
+  for (uint32_t h = 0; h < n2; h += 32) {
+    const int64_t v = max64(warp_incl_max(S[h + lane].ub, lane), carry);
+    M[h + lane] = v;
+    carry = __shfl_sync(0xffffffffu, v, 31);
+  }
+  __syncwarp();
 }
 
 // Verdict of one record, computed by the whole warp (all lanes return it).
@@ -282,30 +298,47 @@ static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r,
   // per-lane descriptors d = lane, lane + 32, ...: activity, opaque flags,
   // extents (registers for <= 64 descriptors, else element d of the scratch)
   const bool in_regs = K.ndesc <= 64;
-  const bool in_scratch = !in_regs && scratch != nullptr && K.ndesc <= cap;
-  const uint32_t np2 = in_scratch ? max(64u, 1u << (32 - __clz((uint32_t)K.ndesc - 1))) : 0u;
+  // > 64 descriptors: the smaller kind sorted in the scratch (+ prefix
+  // maxima), the larger kind probed against it; bytes needed: 16 per extent +
+  // 24 per padded sorted slot
+  const uint32_t cap_bytes = cap * (uint32_t)sizeof(WideElem);
+  const uint32_t ns_max = min((uint32_t)K.nr, (uint32_t)K.nw);
+  const uint32_t n2 = max(32u, 1u << (32 - __clz(max(ns_max, 1u) - 1)));
+  const bool in_scratch = !in_regs && scratch != nullptr &&
+                          (uint64_t)n2 * 24 + (uint64_t)(K.nr + K.nw) * 16 <= cap_bytes;
+  const bool sort_w = K.nw <= K.nr;  // the sorted side (per kernel: warp-uniform)
+  Iv64* S = reinterpret_cast<Iv64*>(scratch);
+  int64_t* M = reinterpret_cast<int64_t*>(S + n2);
+  Iv64* L = reinterpret_cast<Iv64*>(M + n2);
   bool act_r = false, act_w = false, opq_r = false, opq_w = false;
   Ext e[2];
   e[0].kind = e[1].kind = 2;
   e[0].lb = e[0].ub = e[1].lb = e[1].ub = 0;
+  uint32_t ns = 0, nl = 0;  // compacted counts (warp-uniform)
 #pragma unroll 2
-  for (int d = lane, k = 0; d < (in_scratch ? (int)np2 : K.ndesc); d += 32, ++k) {
-    WideElem x{0, 0, 2, 0, 0};
+  for (int d0 = 0, k = 0; d0 < K.ndesc; d0 += 32, ++k) {
+    const int d = d0 + lane;
+    bool have = false, is_r = false;
+    int64_t lb = 0, ub = 0;
     if (d < K.ndesc) {
       const DDesc D = T.descs[K.desc + d];
-      int64_t lb = 0, ub = 0;
       if (desc_active_extent(T, K, D, X, lb, ub)) {
         (D.kind == KIND_R ? act_r : act_w) = true;
         if (D.opaque)
           (D.kind == KIND_R ? opq_r : opq_w) = true;
         else
-          x = WideElem{lb, ub, D.kind == KIND_R ? 0u : 1u, 0, 0};
+          have = true, is_r = D.kind == KIND_R;
       }
     }
-    if (in_scratch) {
-      scratch[d] = x;
-    } else if (k < 2) {
-      e[k].lb = x.lb, e[k].ub = x.ub, e[k].kind = x.kind;
+    if (in_scratch) {  // compact into the sorted side / the probed side
+      const bool to_s = have && (is_r != sort_w);
+      const unsigned ms = __ballot_sync(0xffffffffu, to_s), ml = __ballot_sync(0xffffffffu, have && !to_s);
+      const unsigned lt = (1u << lane) - 1u;
+      if (to_s) S[ns + __popc(ms & lt)] = Iv64{lb, ub};
+      if (have && !to_s) L[nl + __popc(ml & lt)] = Iv64{lb, ub};
+      ns += __popc(ms), nl += __popc(ml);
+    } else if (k < 2 && have) {
+      e[k].lb = lb, e[k].ub = ub, e[k].kind = is_r ? 0u : 1u;
     }
   }
   act_r = __any_sync(0xffffffffu, act_r);
@@ -319,9 +352,17 @@ static __device__ uint8_t eval_wide_warp(const Tables& T, const picker_rec_t& r,
     return sweep64(e[0], e[1], lane) ? V_NI_OVERLAP : V_IDEM_CHECKED;
   }
   if (in_scratch) {
+    if (ns == 0 || nl == 0) {
+      __syncwarp();
+      return V_IDEM_CHECKED;
+    }
+    const uint32_t m2 = max(32u, 1u << (32 - __clz(ns - 1)));  // <= n2
+    for (uint32_t x = ns + lane; x < m2; x += 32)
+      S[x] = Iv64{9223372036854775807LL, (-9223372036854775807LL - 1)};  // padding sorts last, never reaches
     __syncwarp();
-    scratch_sort(scratch, np2, lane);
-    const bool hit = scratch_sweep(scratch, np2, lane);
+    iv_sort(S, m2, lane);
+    iv_prefix_max(S, M, m2, lane);
+    const bool hit = iv_probe(S, M, m2, L, nl, lane);
     __syncwarp();  // the scratch is reused by the warp's next record
     return hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
   }

@@ -316,18 +316,18 @@ def test_exact_far_apart_accesses(off, exact):
 
 # ---- many symbolic addresses (row a8, the wide path's inputs) ---------------------
 
-@pytest.mark.parametrize("kid,nr", [(0, 40), (1, 600), (2, 20)])
-def test_comb_kernels(kid, nr):
+@pytest.mark.parametrize("kid,nr,nw", [(0, 40, 40), (1, 600, 500), (2, 20, 20), (3, 1500, 1500)])
+def test_comb_kernels(kid, nr, nw):
     """Read teeth [A + 64 i, A + 64 i + 4 n - 1], write teeth at B (hand-derived,
     closed byte intervals, PAPER.md l.658-666 and reading Q4):
     B = A + 64 nr, n = 16: the first write byte follows the last read byte -> 0;
     B = A + 64 (nr - 1), n = 1: write tooth 0 = read tooth nr - 1 -> 10;
     B = A + 32, n = 8: teeth interleave and touch -> 0; n = 9: 4 bytes shared -> 10;
-    B = A - 64 * 600: every write tooth below A -> 0; n = 0: no tooth -> 0."""
+    B = A - 64 nw: every write tooth below A -> 0; n = 0: no tooth -> 0."""
     from tracegen.comb import comb_summary
     K = O.index_summary(comb_summary())
     A = 1 << 40
     got = [O.oracle_interval(K, _rec(kid, [A, B, n], (1, 1, 1), (32, 1, 1)))
-           for B, n in [(A + 64 * nr, 16), (A + 64 * (nr - 1), 1), (A + 32, 8), (A + 32, 9), (A - 64 * 600, 16),
+           for B, n in [(A + 64 * nr, 16), (A + 64 * (nr - 1), 1), (A + 32, 8), (A + 32, 9), (A - 64 * nw, 16),
                         (A, 0)]]
     assert got == [0, 10, 0, 10, 0, 0]

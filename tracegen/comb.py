@@ -19,7 +19,9 @@ def comb_kernel(kid, nr, nw):
 
 
 def comb_summary():
-    """Kernel 0: 40 x 40 sites (80 descriptors: the scratch sort); kernel 1:
-    600 x 500 sites (1,100 descriptors: beyond the scratch, lanes over pairs);
-    kernel 2: 20 x 20 (40 descriptors: the register sort)."""
-    return {"version": 1, "kernels": [comb_kernel(0, 40, 40), comb_kernel(1, 600, 500), comb_kernel(2, 20, 20)]}
+    """Kernel 0: 40 x 40 sites (80 descriptors: the smaller side sorted in the
+    scratch); kernel 1: 600 x 500 sites (1,100 descriptors, still in the
+    global scratch); kernel 2: 20 x 20 (40 descriptors: the register sort);
+    kernel 3: 1500 x 1500 (beyond any scratch: lanes over pairs)."""
+    return {"version": 1, "kernels": [comb_kernel(0, 40, 40), comb_kernel(1, 600, 500), comb_kernel(2, 20, 20),
+                                      comb_kernel(3, 1500, 1500)]}
