@@ -210,8 +210,11 @@ int picker_replicate(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
  * first record whose own check is decided before any address (0xFF, 0xFE, 2-8;
  * kernel-level idempotent instances take part with their writes) decides the
  * window; then the opaque rule (9); then the overlap (10); else 0.
- * out[ceil(n/window)] is a device pointer.  Kernels with more than 64
- * descriptors are rejected (PICKER_EINVAL).  Asynchronous on `stream`.        */
+ * Decided by sort + sweep passes over the window's extents (k_seq.cu):
+ * concurrent, one pass; sequential, a divide and conquer over launch order.
+ * out[ceil(n/window)] is a device pointer.  PICKER_EINVAL when window x (the
+ * most descriptors of a loaded kernel) exceeds 2^24.  Asynchronous on
+ * `stream`.                                                                    */
 int picker_validate_sequence(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                              uint32_t window, uint32_t mode, uint8_t* out, void* stream);
 

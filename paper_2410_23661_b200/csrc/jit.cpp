@@ -443,14 +443,28 @@ uint64_t fnv1a(const std::string& s) {
   return h;
 }
 
+// Module cache directory: $PICKER_JIT_CACHE, else $XDG_CACHE_HOME/picker_jit,
+// else $HOME/.cache/picker_jit; empty (no cache) when none is set.  There is no
+// shared fallback such as /tmp: a cubin found in the cache is loaded and run,
+// so the cache must belong to this user (checked in owned_private()).
 std::string cache_dir() {
-  const char* e = getenv("PICKER_JIT_CACHE");
-  if (e && *e) return e;
-  const char* home = getenv("HOME");
-  return std::string(home && *home ? home : "/tmp") + "/.cache/picker_jit";
+  if (const char* e = getenv("PICKER_JIT_CACHE"); e && *e) return e;
+  if (const char* x = getenv("XDG_CACHE_HOME"); x && *x) return std::string(x) + "/picker_jit";
+  if (const char* h = getenv("HOME"); h && *h) return std::string(h) + "/.cache/picker_jit";
+  return "";
+}
+
+// The path exists, belongs to the calling user and is not writable by group
+// or others (a directory or a regular file).
+bool owned_private(const std::string& p, bool dir) {
+  struct stat st;
+  if (lstat(p.c_str(), &st) != 0) return false;
+  if (dir ? !S_ISDIR(st.st_mode) : !S_ISREG(st.st_mode)) return false;
+  return st.st_uid == getuid() && (st.st_mode & (S_IWGRP | S_IWOTH)) == 0;
 }
 
 bool read_file(const std::string& p, std::string& out) {
+  if (!owned_private(p, false)) return false;
   std::ifstream f(p, std::ios::binary);
   if (!f) return false;
   std::stringstream ss;
@@ -461,7 +475,8 @@ bool read_file(const std::string& p, std::string& out) {
 
 void write_file_atomic(const std::string& dir, const std::string& name, const std::string& data) {
   for (size_t i = 1; i <= dir.size(); ++i)
-    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0755);
+    if (i == dir.size() || dir[i] == '/') mkdir(dir.substr(0, i).c_str(), 0700);
+  if (!owned_private(dir, true)) return;
   std::string tmp = dir + "/" + name + ".tmp" + std::to_string(getpid());
   {
     std::ofstream f(tmp, std::ios::binary);
@@ -712,6 +727,7 @@ bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, st
   char name[64];
   snprintf(name, sizeof(name), "%016llx.cubin", (unsigned long long)h);
   const std::string dir = cache_dir();
+  if (dir.empty() || (access(dir.c_str(), F_OK) == 0 && !owned_private(dir, true))) use_cache = false;
   const std::string meta_name = std::string(name) + ".name";
   if (use_cache && read_file(dir + "/" + name, cubin) && read_file(dir + "/" + meta_name, lowered))
     return true;

@@ -7,12 +7,26 @@
 // overlap of read and write addresses among all concurrent instances."
 //
 // The stream is cut into consecutive windows of `window` launches (launch
-// order = record order).  S1 (one thread per record) evaluates each record's
-// prefix and extents into scratch; S2 (one CTA per window) decides the window:
-// the first decisive record code, then the opaque rule, then the overlap of a
-// read of instance i with a write of instance j (sequential: i <= j;
-// concurrent: any i, j) -- reading Q23 in DESIGN.md, identical to
-// oracle.picker_oracle.oracle_sequence.
+// order = record order); one CTA decides one window at a time (persistent),
+// reading DESIGN.md Q23 (identical to oracle.picker_oracle.oracle_sequence):
+//   1. threads over the window's records: each record's decisive code (the
+//      first one in launch order decides), its activity / opaque flags, and its
+//      active non-opaque extents appended to the CTA's read and write lists;
+//   2. the opaque rule (sequential: an opaque read of i with a write of j >= i,
+//      or a read of i with an opaque write of j >= i; concurrent: any i, j);
+//   3. the overlap, as sort + sweep passes over the extents.  Concurrent: one
+//      pass, any read against any write.  Sequential ("a read of i and a write
+//      of j with i <= j"): divide and conquer over launch order -- a pass per
+//      level l of a binary split of the window checks the reads of every left
+//      half against the writes of the matching right half (instance bit l = 0
+//      vs 1, same higher bits), plus one pass within each instance.  Each pass
+//      tags the extents with a node id, sorts the writes by (node, lb) (bitonic,
+//      CTA-wide), takes the prefix maxima of ub within each node (the sweep
+//      line's running maximum), and probes every read by binary search in its
+//      node: some write of the node overlaps the read iff, at the last write
+//      with lb <= read.ub, the running maximum ub >= read.lb (closed intervals).
+// No per-record limit on descriptors; the lists live in a per-CTA slice of a
+// global scratch (window x max descriptors x 48 bytes, L1/L2-resident).
 #include <cuda_runtime.h>
 
 #include <string>
@@ -22,144 +36,219 @@
 
 namespace picker {
 
+constexpr int kSeqThreads = 512;
 constexpr uint8_t kEvaluable = 0x80;
-constexpr int kSeqMaxDesc = 64;  // extents kept per record
 
-struct SeqRec {
-  uint8_t status;  // decisive verdict, or kEvaluable
-  uint8_t flags;   // 1 act_r, 2 act_w, 4 opq_r, 8 opq_w
-  uint8_t n;       // active non-opaque extents
-  uint8_t pad[5];
-  uint64_t wmask;  // bit k: extent k is a write
+struct SeqIv {  // one extent: [lb, ub] of instance `inst` of the window
+  int64_t lb, ub;
+  uint32_t inst, node;
 };
 
-__global__ void k_seq_extents(Tables T, DevBatch B, uint64_t n, SeqRec* __restrict__ sr,
-                              int64_t* __restrict__ ext /* [n][kSeqMaxDesc][2] */) {
-  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (uint64_t)gridDim.x * blockDim.x) {
-    const picker_rec_t r = load_rec(B.rec + i);
-    SeqRec s{};
-    s.status = kEvaluable;
+__device__ __forceinline__ bool seq_less(const SeqIv& a, const SeqIv& b) {
+  return a.node < b.node || (a.node == b.node && a.lb < b.lb);
+}
+
+// One window: returns its code (CTA-uniform).
+__device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, uint32_t m, uint32_t mode, SeqIv* Rl,
+                              SeqIv* Wl, SeqIv* S, int64_t* PM, uint32_t cap) {
+  __shared__ uint32_t s_first, s_nr, s_nw, s_ns, s_hit;
+  __shared__ uint8_t s_flags[1024];  // per instance: 1 act_r, 2 act_w, 4 opq_r, 8 opq_w
+  __shared__ uint8_t s_code;
+  const int tid = threadIdx.x;
+  if (tid == 0) s_first = 0xFFFFFFFFu, s_nr = 0, s_nw = 0, s_hit = 0;
+  __syncthreads();
+  // 1. records of the window
+  for (uint32_t i = tid; i < m; i += blockDim.x) {
+    const picker_rec_t r = load_rec(B.rec + w0 + i);
+    uint8_t status = kEvaluable, fl = 0;
     const uint32_t kid = r.kernel_id;
     do {
       if (kid >= T.nkernel_slots || T.kernels[kid].shortcut == V_ERR_KERNEL) {
-        s.status = V_ERR_KERNEL;
+        status = V_ERR_KERNEL;
         break;
       }
       const DKernel K = T.kernels[kid];
       if (!args_in_range(r, K.nparams, B.args_lo, B.args_hi)) {
-        s.status = V_ERR_ARITY;
+        status = V_ERR_ARITY;
         break;
       }
       if (K.shortcut && K.shortcut != V_IDEM_KERNEL) {  // kernel-level NI
-        s.status = K.shortcut;
+        status = K.shortcut;
         break;
       }
       const RecVals X(r, B.args + r.arg_off, K.i32mask);
       if (!launch_limits_ok(X)) {
-        s.status = V_NI_PRECOND;
+        status = V_NI_PRECOND;
         break;
       }
-      bool fail = false;
-      for (int c = 0; c < K.npre + K.nglob && !fail; ++c) {
+      for (int c = 0; c < K.npre + K.nglob && status == kEvaluable; ++c) {
         const DCheck ch = T.checks[K.check + c];
         const int64_t v = X.get(ch.op);
-        if (v < ch.lo || v > ch.hi) {
-          s.status = c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
-          fail = true;
-        }
+        if (v < ch.lo || v > ch.hi) status = c < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
       }
-      if (fail) break;
+      if (status != kEvaluable) break;
+      // kernel-level idempotent instances take part with their writes (Q23)
       for (int d = 0; d < K.ndesc; ++d) {
         const DDesc D = T.descs[K.desc + d];
-        if (!desc_active(T, K, D, X)) continue;
-        s.flags |= D.kind == KIND_R ? 1 : 2;
+        int64_t lb = 0, ub = 0;
+        if (!desc_active_extent(T, K, D, X, lb, ub)) continue;
+        fl |= D.kind == KIND_R ? 1 : 2;
         if (D.opaque) {
-          s.flags |= D.kind == KIND_R ? 4 : 8;
+          fl |= D.kind == KIND_R ? 4 : 8;
           continue;
         }
-        int64_t lb, ub;
-        desc_extent(T, K, D, X, lb, ub);
-        ext[(i * kSeqMaxDesc + s.n) * 2] = lb;
-        ext[(i * kSeqMaxDesc + s.n) * 2 + 1] = ub;
-        if (D.kind == KIND_W) s.wmask |= 1ull << s.n;
-        ++s.n;
+        const uint32_t pos = atomicAdd(D.kind == KIND_R ? &s_nr : &s_nw, 1u);
+        if (pos < cap) (D.kind == KIND_R ? Rl : Wl)[pos] = SeqIv{lb, ub, i, 0};
       }
     } while (false);
-    sr[i] = s;
+    s_flags[i] = fl;
+    if (status != kEvaluable) atomicMin(&s_first, (i << 8) | status);
   }
+  __syncthreads();
+  // the first decisive record (launch order) decides the window
+  if (s_first != 0xFFFFFFFFu) return (uint8_t)(s_first & 0xFF);
+  // 2. opaque rule
+  if (tid == 0) {
+    uint8_t code = kEvaluable;
+    bool pre_opq_r = false, pre_act_r = false, opq_r = false, act_r = false, opq_w = false, act_w = false;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint8_t f = s_flags[j];
+      pre_opq_r |= (f & 4) != 0, pre_act_r |= (f & 1) != 0;
+      act_r |= (f & 1) != 0, act_w |= (f & 2) != 0, opq_r |= (f & 4) != 0, opq_w |= (f & 8) != 0;
+      if (mode == 0 && ((pre_opq_r && (f & 2)) || (pre_act_r && (f & 8)))) code = V_NI_OPAQUE;
+    }
+    if (mode == 1 && ((opq_r && act_w) || (act_r && opq_w))) code = V_NI_OPAQUE;
+    s_code = code;
+  }
+  __syncthreads();
+  if (s_code != kEvaluable) return s_code;
+  // 3. overlap passes
+  const uint32_t nr = s_nr, nw = s_nw;
+  if (nr == 0 || nw == 0) return V_IDEM_CHECKED;
+  uint32_t levels = 0;
+  while ((1u << levels) < m) ++levels;
+  // pass p: mode 1 -> one pass (node 0); mode 0 -> p = levels .. 0: p == levels is
+  // the within-instance pass (node = inst), p < levels the cross pass of level p
+  const int first_pass = mode == 1 ? -1 : (int)levels;
+  for (int p = first_pass; p >= (mode == 1 ? -1 : 0); --p) {
+    auto wnode = [&](uint32_t inst, bool& in) -> uint32_t {
+      if (p < 0) return in = true, 0u;
+      if (p == (int)levels) return in = true, inst;
+      in = (inst >> p) & 1;  // right half of its level-p node
+      return inst >> (p + 1);
+    };
+    auto rnode = [&](uint32_t inst, bool& in) -> uint32_t {
+      if (p < 0) return in = true, 0u;
+      if (p == (int)levels) return in = true, inst;
+      in = !((inst >> p) & 1);  // left half
+      return inst >> (p + 1);
+    };
+    if (tid == 0) s_ns = 0;
+    __syncthreads();
+    for (uint32_t x = tid; x < nw; x += blockDim.x) {
+      SeqIv w = Wl[x];
+      bool in;
+      w.node = wnode(w.inst, in);
+      if (in) S[atomicAdd(&s_ns, 1u)] = w;
+    }
+    __syncthreads();
+    const uint32_t ns = s_ns;
+    if (ns == 0) continue;
+    uint32_t n2 = 32;
+    while (n2 < ns) n2 <<= 1;
+    for (uint32_t x = ns + tid; x < n2; x += blockDim.x)
+      S[x] = SeqIv{9223372036854775807LL, (-9223372036854775807LL - 1), 0, 0xFFFFFFFFu};  // sorts last
+    __syncthreads();
+    for (uint32_t k = 2; k <= n2; k <<= 1)  // bitonic sort by (node, lb)
+      for (uint32_t j = k >> 1; j > 0; j >>= 1) {
+        for (uint32_t q = tid; q < n2 / 2; q += blockDim.x) {
+          const uint32_t i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), o = i | j;
+          const SeqIv a = S[i], b = S[o];
+          if (((i & k) == 0) ? seq_less(b, a) : seq_less(a, b)) S[i] = b, S[o] = a;
+        }
+        __syncthreads();
+      }
+    if (tid < 32) {  // prefix maxima of ub within each node segment (one warp, carried)
+      const int lane = tid;
+      int64_t carry = (-9223372036854775807LL - 1);
+      uint32_t carry_node = 0xFFFFFFFFu;
+      for (uint32_t h = 0; h < ns; h += 32) {
+        const uint32_t x = h + lane;
+        const SeqIv e = x < ns ? S[x] : SeqIv{0, (-9223372036854775807LL - 1), 0, 0xFFFFFFFEu};
+        int64_t v = e.ub;
+        // segmented inclusive max: only elements of the same node contribute
+        for (int d = 1; d < 32; d <<= 1) {
+          const int64_t o = __shfl_up_sync(0xffffffffu, v, d);
+          const uint32_t on = __shfl_up_sync(0xffffffffu, e.node, d);
+          if (lane >= d && on == e.node) v = max64(v, o);
+        }
+        if (e.node == carry_node) v = max64(v, carry);
+        if (x < ns) PM[x] = v;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+        carry_node = __shfl_sync(0xffffffffu, e.node, 31);
+      }
+    }
+    __syncthreads();
+    for (uint32_t x = tid; x < nr && !s_hit; x += blockDim.x) {
+      const SeqIv r = Rl[x];
+      bool in;
+      const uint32_t node = rnode(r.inst, in);
+      if (!in) continue;
+      // last index whose (node, lb) <= (node, r.ub)
+      int lo = -1;
+      for (uint32_t step = n2 >> 1; step > 0; step >>= 1) {
+        const SeqIv& c = S[lo + (int)step];
+        if (c.node < node || (c.node == node && c.lb <= r.ub)) lo += (int)step;
+      }
+      if (lo + 1 < (int)n2) {
+        const SeqIv& c = S[lo + 1];
+        if (c.node < node || (c.node == node && c.lb <= r.ub)) ++lo;
+      }
+      if (lo >= 0 && S[lo].node == node && PM[lo] >= r.lb) s_hit = 1;
+    }
+    __syncthreads();
+    if (s_hit) return V_NI_OVERLAP;
+  }
+  return V_IDEM_CHECKED;
 }
 
-__global__ void __launch_bounds__(256) k_seq_windows(const SeqRec* __restrict__ sr, const int64_t* __restrict__ ext,
-                                                     uint64_t n, uint32_t window, uint32_t mode,
-                                                     uint8_t* __restrict__ out) {
-  __shared__ uint8_t s_code;
-  __shared__ int s_hit;
-  const uint64_t w0 = (uint64_t)blockIdx.x * window;
-  const uint32_t m = (uint32_t)min((uint64_t)window, n - w0);
-  if (threadIdx.x == 0) {
-    uint8_t code = kEvaluable;
-    for (uint32_t i = 0; i < m && code == kEvaluable; ++i)
-      if (sr[w0 + i].status != kEvaluable) code = sr[w0 + i].status;
-    if (code == kEvaluable) {  // opaque rule: reads of instance i against writes of j
-      bool pre_opq_r = false, pre_act_r = false;  // over instances <= j (sequential)
-      bool opq_r = false, act_r = false, opq_w = false, act_w = false;  // whole window
-      for (uint32_t j = 0; j < m; ++j) {
-        const uint8_t f = sr[w0 + j].flags;
-        pre_opq_r |= (f & 4) != 0;
-        pre_act_r |= (f & 1) != 0;
-        act_r |= (f & 1) != 0, act_w |= (f & 2) != 0, opq_r |= (f & 4) != 0, opq_w |= (f & 8) != 0;
-        if (mode == 0 && ((pre_opq_r && (f & 2)) || (pre_act_r && (f & 8)))) code = V_NI_OPAQUE;
-      }
-      if (mode == 1 && ((opq_r && act_w) || (act_r && opq_w))) code = V_NI_OPAQUE;
-    }
-    s_code = code;
-    s_hit = 0;
+__global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch B, uint64_t n, uint32_t window,
+                                                              uint32_t mode, uint8_t* __restrict__ scratch,
+                                                              uint64_t slice, uint32_t cap, uint8_t* __restrict__ out) {
+  // per-CTA slice: reads [cap], writes [cap], sort buffer [2 cap], prefix maxima [2 cap]
+  SeqIv* Rl = reinterpret_cast<SeqIv*>(scratch + blockIdx.x * slice);
+  SeqIv* Wl = Rl + cap;
+  SeqIv* S = Wl + cap;
+  int64_t* PM = reinterpret_cast<int64_t*>(S + 2 * (uint64_t)cap);
+  const uint64_t nwin = (n + window - 1) / window;
+  for (uint64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
+    const uint64_t w0 = w * window;
+    const uint32_t m = (uint32_t)min((uint64_t)window, n - w0);
+    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap);
+    if (threadIdx.x == 0) out[w] = code;
+    __syncthreads();  // the slice and the shared state are reused by the next window
   }
-  __syncthreads();
-  if (s_code != kEvaluable) {
-    if (threadIdx.x == 0) out[blockIdx.x] = s_code;
-    return;
-  }
-  // overlap: instance pairs (i reads, j writes) over the threads
-  const uint32_t pairs = m * m;
-  for (uint32_t p = threadIdx.x; p < pairs; p += blockDim.x) {
-    const uint32_t i = p / m, j = p % m;
-    if (mode == 0 && i > j) continue;
-    const SeqRec a = sr[w0 + i], b = sr[w0 + j];
-    for (uint32_t x = 0; x < a.n; ++x) {
-      if ((a.wmask >> x) & 1) continue;
-      const int64_t rl = ext[((w0 + i) * kSeqMaxDesc + x) * 2], ru = ext[((w0 + i) * kSeqMaxDesc + x) * 2 + 1];
-      for (uint32_t y = 0; y < b.n; ++y) {
-        if (!((b.wmask >> y) & 1)) continue;
-        const int64_t wl = ext[((w0 + j) * kSeqMaxDesc + y) * 2], wu = ext[((w0 + j) * kSeqMaxDesc + y) * 2 + 1];
-        if (rl <= wu && wl <= ru) s_hit = 1;
-      }
-    }
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) out[blockIdx.x] = s_hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
 }
 
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
-                            uint8_t* out, int num_sms, cudaStream_t s, std::string& err) {
+                            uint32_t max_desc, uint8_t* out, int num_sms, cudaStream_t s, std::string& err) {
   if (n == 0) return cudaSuccess;
-  SeqRec* sr = nullptr;
-  int64_t* ext = nullptr;
-  cudaError_t e = cudaMallocAsync(&sr, n * sizeof(SeqRec), s);
-  if (e == cudaSuccess) e = cudaMallocAsync(&ext, n * kSeqMaxDesc * 2 * sizeof(int64_t), s);
+  // extents per window <= window x max descriptors per kernel
+  const uint32_t cap = std::max<uint32_t>(32, window * std::max<uint32_t>(max_desc, 1));
+  const uint64_t slice = (uint64_t)cap * (4 * sizeof(SeqIv) + 2 * sizeof(int64_t));
+  const uint64_t nwin = (n + window - 1) / window;
+  // as many CTAs as windows, up to 2 per SM and ~1 GB of scratch
+  uint64_t grid = std::min<uint64_t>(nwin, (uint64_t)num_sms * 2);
+  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (1ULL << 30) / slice));
+  uint8_t* scratch = nullptr;
+  cudaError_t e = cudaMallocAsync(&scratch, grid * slice, s);
   if (e != cudaSuccess) {
     err = "scratch allocation";
-    if (sr) cudaFreeAsync(sr, s);
     return e;
   }
-  const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 8);
-  k_seq_extents<<<(unsigned)blocks, 256, 0, s>>>(T, b, n, sr, ext);
-  const uint64_t nwin = (n + window - 1) / window;
-  k_seq_windows<<<(unsigned)nwin, 256, 0, s>>>(sr, ext, n, window, mode, out);
+  k_seq_windows<<<(unsigned)grid, kSeqThreads, 0, s>>>(T, b, n, window, mode, scratch, slice, cap, out);
   e = cudaGetLastError();
-  cudaFreeAsync(sr, s);
-  cudaFreeAsync(ext, s);
+  cudaFreeAsync(scratch, s);
   return e;
 }
 

@@ -71,7 +71,7 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             int* launches);
 
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
-                            uint8_t* out, int num_sms, cudaStream_t s, std::string& err);
+                            uint32_t max_desc, uint8_t* out, int num_sms, cudaStream_t s, std::string& err);
 
 cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const uint8_t* codes,
                           const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,

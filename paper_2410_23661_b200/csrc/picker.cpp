@@ -472,15 +472,16 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
   int st = check_batch(c, b, n, out);
   if (st) return st;
   if (window < 1 || window > 1024 || mode > 1) return fail(c, PICKER_EINVAL, "window must be 1..1024, mode 0/1");
-  for (auto& k : c->ir)
-    if (k.desc.size() > 64)
-      return fail(c, PICKER_EINVAL, "kernel " + std::to_string(k.id) + " has more than 64 descriptors");
+  uint32_t max_desc = 1;
+  for (auto& k : c->ir) max_desc = std::max<uint32_t>(max_desc, (uint32_t)k.desc.size());
+  if ((uint64_t)window * max_desc > (1u << 24))
+    return fail(c, PICKER_EINVAL, "window x descriptors per kernel exceeds 2^24 extents");
   DevGuard g(c->device);
   DevBatch db{b->rec, b->args, 0, b->args_len};
   std::string err;
-  cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, out, c->num_sms, (cudaStream_t)stream, err);
+  cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, max_desc, out, c->num_sms, (cudaStream_t)stream, err);
   if (e != cudaSuccess) return cuda_fail(c, e, ("sequence: " + err).c_str());
-  c->last_launches = n ? 2 : 0;
+  c->last_launches = n ? 1 : 0;
   return PICKER_OK;
 }
 

@@ -159,3 +159,69 @@ def test_gpu_sequence_golden_opaque(concurrent):
     p.load(golden.golden_summary())
     got = p.validate_sequence(rec, args, 2, concurrent=concurrent).cpu().numpy()
     assert got.tolist() == want
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("window", [32, 1024])
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_gpu_sequence_c2(window, concurrent):
+    """The C2 trace (547 kernels) cut into windows of 32 / 1024 launches: every
+    window's code against oracle_windows (sort + sweep passes vs the plain
+    pairwise definition)."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, _ = workloads.make_c2()
+    mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
+    want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
+    p = pk.Picker(0)
+    p.load(s)
+    got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+    assert len(set(want.tolist())) > 2
+    # the C2 records that reach the address check on their own (codes 0, 9,
+    # 10): windows decided by the sort + sweep passes, not by a decisive record
+    codes = np.array(O.oracle_batch(s, rec, args), np.uint8)
+    keep = np.isin(codes, [0, 9, 10])
+    sub = rec[keep]
+    w2 = 16 if window == 32 else 64
+    want = np.array(O.oracle_windows(s, sub, args, w2, mode), np.uint8)
+    got = p.validate_sequence(sub, args, w2, concurrent=concurrent).cpu().numpy()
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+    assert (want == 0).sum() > 0 and (want == 10).sum() > 0
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_gpu_sequence_wide(concurrent):
+    """Windows of multi-tensor kernels with 150-300 descriptors (no limit on
+    descriptors per kernel) and of the comb kernels (touching / interleaved
+    teeth across instances)."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    from tracegen.comb import comb_summary
+    mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
+    s, rec, args, _ = workloads.make_wide(n=96)
+    for window in (2, 5):
+        want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
+        p = pk.Picker(0)
+        p.load(s)
+        got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
+        assert np.array_equal(got, want), (np.nonzero(got != want)[0][:8])
+    s = comb_summary()
+    rng = np.random.default_rng(5)
+    b = RecordBuilder()
+    A = 1 << 40
+    for i in range(64):
+        kid = int(rng.integers(0, 3))
+        nr = [40, 600, 20][kid]
+        b.add(kid, [A + 64 * int(rng.integers(-nr, nr)), A + 64 * int(rng.integers(-nr, nr)) + int(rng.integers(0, 64)),
+                    int(rng.integers(0, 17))], grid=(1,), block=(32,))
+    rec, args = b.build()
+    for window in (1, 3, 8):
+        want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
+        p = pk.Picker(0)
+        p.load(s)
+        got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
+        assert np.array_equal(got, want), (window, np.nonzero(got != want)[0][:8])
