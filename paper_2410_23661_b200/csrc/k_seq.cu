@@ -237,8 +237,10 @@ cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint
   const uint32_t cap = std::max<uint32_t>(32, window * std::max<uint32_t>(max_desc, 1));
   const uint64_t slice = (uint64_t)cap * (4 * sizeof(SeqIv) + 2 * sizeof(int64_t));
   const uint64_t nwin = (n + window - 1) / window;
-  // as many CTAs as windows, up to 2 per SM and ~1 GB of scratch
-  uint64_t grid = std::min<uint64_t>(nwin, (uint64_t)num_sms * 2);
+  // a thread per record of a window (32..512 threads per CTA), as many CTAs as
+  // fill the SMs (2048 threads each), within ~1 GB of scratch
+  const uint32_t threads = std::min<uint32_t>(kSeqThreads, (window + 31) / 32 * 32);
+  uint64_t grid = std::min<uint64_t>(nwin, (uint64_t)num_sms * (2048 / threads));
   grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (1ULL << 30) / slice));
   uint8_t* scratch = nullptr;
   cudaError_t e = cudaMallocAsync(&scratch, grid * slice, s);
@@ -246,7 +248,7 @@ cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint
     err = "scratch allocation";
     return e;
   }
-  k_seq_windows<<<(unsigned)grid, kSeqThreads, 0, s>>>(T, b, n, window, mode, scratch, slice, cap, out);
+  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, scratch, slice, cap, out);
   e = cudaGetLastError();
   cudaFreeAsync(scratch, s);
   return e;
