@@ -762,8 +762,9 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   if (opt.sorted < 0) opt.sorted = mean > 6.0 && !opt.stride;
   if (opt.sorted) {
     const int slot = (int)((std::min<size_t>(std::max<size_t>(maxargs, 1), 62) * 8 + 16 + 15) / 16 * 16);
-    opt.sort_slot = slot;
-    opt.sort_warps = std::max(1, std::min(16, (200 * 1024) / (32 * slot)));
+    if (opt.sort_slot <= 0) opt.sort_slot = slot;
+    opt.sort_slot = (opt.sort_slot + 15) / 16 * 16;
+    if (opt.sort_warps <= 0) opt.sort_warps = std::max(1, std::min(16, (200 * 1024) / (32 * opt.sort_slot)));
   }
   if (opt.tile != 0) return opt;
   if (mean <= 6.0) {

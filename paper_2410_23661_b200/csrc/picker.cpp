@@ -142,6 +142,8 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "arg_bufs") c->opt.arg_bufs = (int)v;
   else if (k == "stride") c->opt.stride = v != 0;
   else if (k == "sorted") c->opt.sorted = v < 0 ? -1 : (int)(v != 0);
+  else if (k == "sort_slot") c->opt.sort_slot = (int)v;    // tuning: average argument bytes per lane
+  else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
