@@ -211,8 +211,9 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch
         }
         __syncthreads();
         if (s_on) {
-          const volatile int* found = &s_found;
-          for (uint64_t p = threadIdx.x; p < s_npts && !(pass == 1 && *found); p += blockDim.x) {
+          // early exit once any thread found a shared byte (atomic reads and
+          // writes of the flag: no shared-memory race)
+          for (uint64_t p = threadIdx.x; p < s_npts && !(pass == 1 && atomicOr(&s_found, 0)); p += blockDim.x) {
             int64_t x[16];
             uint64_t q = p;
             for (int v = 0; v < s_nv; ++v)
@@ -264,7 +265,7 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch
                   h = (h + 1) & tmask;
                 }
                 if (hit) {
-                  s_found = 1;
+                  atomicExch(&s_found, 1);
                   break;
                 }
               }
