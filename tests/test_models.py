@@ -121,9 +121,11 @@ def test_gpu_models_random(seed):
     p = pk.Picker(0)
     p.load(s)
     flags, _, _ = p.validate(rec, args)
+    codes = np.array(O.oracle_batch(s, rec, args), np.uint8)  # the oracle's verdicts, not the GPU's
+    assert np.array_equal(flags.cpu().numpy(), codes)
     ctx = np.random.default_rng(seed).integers(0, 200_000, len(rec)).astype(np.uint64)
-    got = p.consumer_models(rec, args, flags, ctx, kill_ns=1000, save_bytes_per_us=1500)
-    want = O.oracle_models(s, rec, args, flags.cpu().numpy(), ctx, kill_ns=1000, save_bytes_per_us=1500)
+    got = p.consumer_models(rec, args, codes, ctx, kill_ns=1000, save_bytes_per_us=1500)
+    want = O.oracle_models(s, rec, args, codes, ctx, kill_ns=1000, save_bytes_per_us=1500)
     assert got == want
 
 
@@ -134,10 +136,10 @@ def test_gpu_models_c2():
     s, rec, args, _ = workloads.make_c2()
     p = pk.Picker(0)
     p.load(s)
-    flags, _, _ = p.validate(rec, args)
+    codes = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)  # the oracle's verdicts
     ctx = np.random.default_rng(5).integers(4_000, 98_001, len(rec)).astype(np.uint64)
-    got = p.consumer_models(rec, args, flags, ctx)
-    want = O.oracle_models(s, rec, args, flags.cpu().numpy(), ctx)
+    got = p.consumer_models(rec, args, codes, ctx)
+    want = O.oracle_models(s, rec, args, codes, ctx)
     assert got == want
 
 
