@@ -663,7 +663,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
           : stride    ? "    if (key == 1 || key == 2) return eval_stride(P.T, r, a, B.args_lo, B.args_hi);\n"
                       : "    if (key == 1) return eval_generic(P.T, r, a, B.args_lo, B.args_hi);\n")
       // the pipelined kernel finishes shortcut / unknown records in its key pass
-      << (shape_shortcut + 1 <= kPipeKeys ? std::string()
+      << (shape_shortcut + 1 <= kPipeKeysMax ? std::string()
                                           : "    if (key == " + std::to_string(shape_shortcut) +
                                                 ") return (uint8_t)direct_code(kn, r.nargs, r.arg_off, B.args_lo, "
                                                 "B.args_hi);\n")
@@ -677,13 +677,13 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
   for (size_t s = 0; s < shapes.size(); ++s)
     src << "      case " << SHAPE_FIRST + s << ": return ks" << s << "(r, a, K);\n";
   src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
-         "template __global__ void " << (shape_shortcut + 1 <= kPipeKeys ? "k_validate_pipe" : "k_validate_bucket")
+         "template __global__ void " << (shape_shortcut + 1 <= kPipeKeysMax ? "k_validate_pipe" : "k_validate_bucket")
       << "<JitDispatch>(const __grid_constant__ BucketParams, "
          "const __grid_constant__ DevBatch, uint64_t, "
          "uint8_t*, uint32_t*, unsigned long long*);\n"
          "template __global__ void k_validate_small<JitDispatch>(const __grid_constant__ BucketParams, "
          "const __grid_constant__ DevBatch, uint32_t, uint8_t*, uint32_t*, unsigned long long*);\n"
-      << (sorted && shape_shortcut + 1 <= kPipeKeys
+      << (sorted && shape_shortcut + 1 <= kSortKeys
               ? "template __global__ void k_validate_sorted<JitDispatch>(const __grid_constant__ BucketParams, "
                 "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
               : "")
@@ -711,7 +711,8 @@ std::vector<std::string> geometry_defines(const Options& opt) {
           "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
           "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
           "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
-          "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot))};
+          "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot)),
+          "-DPICKER_PIPE_KEYS=" + std::to_string(opt.pipe_keys > 64 ? 128 : 64)};
 }
 
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,
@@ -782,7 +783,7 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
 }
 
 JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std::string& err) {
-  const Options opt = resolve_geometry(ks, opt_in);
+  Options opt = resolve_geometry(ks, opt_in);
   if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
       opt.threads > 1024 || opt.ctas < 1 || opt.ctas > 8 || opt.args_per_rec < 1 || opt.arg_bufs < 1 ||
       opt.arg_bufs > 2) {
@@ -790,7 +791,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     return nullptr;
   }
   JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0);
-  if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeys && opt.tile % opt.threads) {
+  opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
+  if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
     return nullptr;
   }
@@ -852,7 +854,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     return nullptr;
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes + 1;
-  m->smem = m->nkeys <= kPipeKeys ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
+  m->smem = m->nkeys <= kPipeKeysMax ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
                                                         (uint32_t)opt.arg_bufs)
                                   : bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {

@@ -555,33 +555,46 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // t-1, next used after B_b of t
     for (int b = tid; b < (int)kPipeKeys; b += kThreads) s_cnt[buf ^ 1][b] = 0;  // CTAs of < 64 threads too
     if (tid == 0) s_next[buf ^ 1] = kWarps;
-    // scan (every warp, registers): lane l holds keys l and 32 + l as
-    // count | groups << 16, inclusive
-    const uint32_t c0 = s_cnt[buf][lane], c1 = s_cnt[buf][lane + 32];
-    uint32_t v0 = c0 | ((c0 + 31) >> 5) << 16, v1 = c1 | ((c1 + 31) >> 5) << 16;
+    // scan (every warp, registers): lane l holds keys l, 32 + l, ... as
+    // count | groups << 16, inclusive (kKPL keys per lane, chained)
+    uint32_t cc[kKPL], vv[kKPL];
+#pragma unroll
+    for (int h = 0; h < kKPL; ++h) {
+      cc[h] = s_cnt[buf][lane + 32 * h];
+      vv[h] = cc[h] | ((cc[h] + 31) >> 5) << 16;
+    }
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t a0 = __shfl_up_sync(0xffffffffu, v0, d), a1 = __shfl_up_sync(0xffffffffu, v1, d);
-      if (lane >= d) v0 += a0, v1 += a1;
+#pragma unroll
+      for (int h = 0; h < kKPL; ++h) {
+        const uint32_t a = __shfl_up_sync(0xffffffffu, vv[h], d);
+        if (lane >= d) vv[h] += a;
+      }
     }
-    v1 += __shfl_sync(0xffffffffu, v0, 31);
-    const uint32_t off0 = (v0 & 0xFFFFu) - c0, off1 = (v1 & 0xFFFFu) - c1;
-    const uint32_t ginc0 = v0 >> 16, ginc1 = v1 >> 16;
-    const uint32_t ngrp = __shfl_sync(0xffffffffu, ginc1, 31);
+#pragma unroll
+    for (int h = 1; h < kKPL; ++h) vv[h] += __shfl_sync(0xffffffffu, vv[h - 1], 31);
+    uint32_t off[kKPL];
+#pragma unroll
+    for (int h = 0; h < kKPL; ++h) off[h] = (vv[h] & 0xFFFFu) - cc[h];
+    const uint32_t ngrp = __shfl_sync(0xffffffffu, vv[kKPL - 1] >> 16, 31);
     // scatter
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const uint32_t key = kr[q] & 0xFFu;
-      const uint32_t o0 = __shfl_sync(0xffffffffu, off0, key & 31), o1 = __shfl_sync(0xffffffffu, off1, key & 31);
-      if (key != 0xFFu) s_perm[(key < 32 ? o0 : o1) + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
+      uint32_t o = 0;
+#pragma unroll
+      for (int h = 0; h < kKPL; ++h) {
+        const uint32_t oh = __shfl_sync(0xffffffffu, off[h], key & 31);
+        if ((key >> 5) == (uint32_t)h) o = oh;
+      }
+      if (key != 0xFFu) s_perm[o + (kr[q] >> 8)] = make_uint2(rb[q], kn[q]);
     }
     // group table: warp w writes groups j = w, w + kWarps, ... of every key
-    {
-      const uint32_t gs0 = ginc0 - ((c0 + 31) >> 5), gs1 = ginc1 - ((c1 + 31) >> 5);
-      for (uint32_t j = warp; 32 * j < c0; j += kWarps)
-        s_grp[gs0 + j] = (off0 + 32 * j) | min(32u, c0 - 32 * j) << 13 | (uint32_t)lane << 19;
-      for (uint32_t j = warp; 32 * j < c1; j += kWarps)
-        s_grp[gs1 + j] = (off1 + 32 * j) | min(32u, c1 - 32 * j) << 13 | (uint32_t)(lane + 32) << 19;
+#pragma unroll
+    for (int h = 0; h < kKPL; ++h) {
+      const uint32_t gs = (vv[h] >> 16) - ((cc[h] + 31) >> 5);
+      for (uint32_t j = warp; 32 * j < cc[h]; j += kWarps)
+        s_grp[gs + j] = (off[h] + 32 * j) | min(32u, cc[h] - 32 * j) << 13 | (uint32_t)(lane + 32 * h) << 19;
     }
     __syncthreads();  // B_b
     // the previous tile's buffers are free: start the copy of the next tile

@@ -31,6 +31,7 @@ struct Options {
   // for many-argument summaries, the geometry of C4); its warps per CTA and
   // per-record argument slot bytes are resolved with the geometry
   int sorted = -1, sort_warps = 0, sort_slot = 0;
+  int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
 };
 
 struct JitModule;

@@ -294,8 +294,9 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     Options opt;
     select_paths(ks, opt);
     order_by_shape(ks);
-    const Options geo = resolve_geometry(ks, opt);
+    Options geo = resolve_geometry(ks, opt);
     JitPlan plan = jit_plan(ks, false, geo.sorted > 0);
+    geo.pipe_keys = 3 + plan.nshapes + 1;  // SHAPE_FIRST + shapes + the shortcut key
     std::string cubin, lowered, err;
     if (!jit_compile(plan, geo, cubin, lowered, false, err)) {
       put(msg, msg_len, err);

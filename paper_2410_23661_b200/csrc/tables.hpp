@@ -199,7 +199,14 @@ constexpr size_t bucket_smem_bytes(uint32_t nkeys) {
 // Pipelined variant for at most kPipeKeys grouping keys (k_validate_pipe):
 // staging buffers, s_perm (u32 x 2) and two s_code (u8) per record; the per-key
 // counters are static shared memory.
-constexpr uint32_t kPipeKeys = 64;
+// The specialised module is compiled with PICKER_PIPE_KEYS = 64 or 128 (its
+// key count); kPipeKeysMax is the host's limit for choosing this kernel.
+#ifndef PICKER_PIPE_KEYS
+#define PICKER_PIPE_KEYS 64
+#endif
+constexpr uint32_t kPipeKeys = PICKER_PIPE_KEYS;
+constexpr uint32_t kPipeKeysMax = 128;
+constexpr int kKPL = (int)(kPipeKeys / 32);  // grouping keys per lane in the scan
 // Small-batch kernel of the specialised module (k_validate_small): one CTA.
 constexpr uint32_t kSmallMax = 1024, kSmallThreads = 256;
 #ifndef PICKER_ARG_BUFS
@@ -217,7 +224,7 @@ constexpr int kWideMax = 1024;
 constexpr int kWideElemBytes = 32;
 
 // Shape-sorted schedule (k_sorted.cuh): host-visible layout of its scratch.
-constexpr uint32_t kSortKeys = kPipeKeys;  // grouping keys of the module (<= 64)
+constexpr uint32_t kSortKeys = 64;  // grouping keys of a module on the sorted schedule (<= 64)
 constexpr uint32_t kSortNoKey = 0xFF;      // final code in S1, not sorted
 constexpr int kSortScanThreads = 1024;
 constexpr int kSortBlock = 512;  // threads of S1 / S3

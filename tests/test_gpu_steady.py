@@ -195,3 +195,14 @@ def test_device_replication(pk, c2):
     flags, bits, counts = p.validate(rd, ad)
     _check(flags, bits, counts, np.tile(want, R))
     p.close()
+
+
+def test_c2heavy_128_keys(pk):
+    """C2-heavy has 66 shapes: the pipelined kernel with 128 grouping keys (4
+    per lane in the scan), every record against the oracle, many tiles per CTA."""
+    s, rec, args, meta = workloads.make_c2(heavy=True)
+    want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
+    for R, opt in [(1, dict(jit=1)), (40, dict(jit=1)), (4, dict(jit=1, tile=64, threads=32, ctas=1, args_per_rec=8))]:
+        rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
+        flags, bits, counts = _run(pk, s, rec_t, args_t, **opt)
+        _check(flags, bits, counts, np.tile(want, R))
