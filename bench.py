@@ -206,9 +206,46 @@ def cpu_baseline(s, rec, a, seconds):
         done += len(rec)
         copies += 1
     dt = time.perf_counter() - t0
-    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+    return {"value": done / dt, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"{copies} full copies of the C2 base trace ({len(rec)} records each), "
                       f"oracle_interval over a {cores}-process pool, {dt:.1f} s"}
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def as_is_batch(p, base_rec, base_args, dev, reps=50):
+    """the base trace as it is (18,217 records for C2, L2-resident,
+    launch-bound): one picker_validate_batch, device time p50 / p90 in us."""
+    import torch
+
+    rd = torch.from_numpy(base_rec.view(np.uint8).reshape(-1, 32)).to(dev)
+    ad = torch.from_numpy(base_args).to(dev)
+    n = len(base_rec)
+    f = torch.empty(n, dtype=torch.uint8, device=dev)
+    b = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+    c = torch.empty(16, dtype=torch.int64, device=dev)
+    st = torch.cuda.current_stream()
+    for _ in range(5):
+        p.validate(rd, ad, out=(f, b, c), stream=st)
+    ts = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        p.validate(rd, ad, out=(f, b, c), stream=st)
+        e1.record(st)
+        st.synchronize()
+        ts.append(1e3 * e0.elapsed_time(e1))
+    return {"records": n, "device_us_p50": float(np.median(ts)), "device_us_p90": float(np.percentile(ts, 90)),
+            "instances_per_s": n / (float(np.median(ts)) / 1e6)}
 
 
 def small_batch_latency(p, rec_d, args_d, dev, sizes=(1, 32, 1024), reps=200):
@@ -302,7 +339,7 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "int (exact Python integers)",
         "data": "synthetic", "config": workload_config(args, world),
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
                          "sample": f"each step: {len(rec)} records of the {args.workload.upper()} base trace, "
                                    f"{cores}-process pool"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -457,6 +494,7 @@ def main():
         mism += 0 if e2e_ok else 1
 
     latency = small_batch_latency(p, rec_d, args_d, dev) if rank == 0 and not args.no_latency else None
+    as_is = as_is_batch(p, base_rec, base_args, dev) if rank == 0 else None
 
     if rank != 0:
         if world > 1:
@@ -499,6 +537,7 @@ def main():
         "p50_us_per_instance": 1e3 * float(np.median(step_ms)) / n,
         "p90_us_per_instance": 1e3 * float(np.percentile(step_ms, 90)) / n,
         "small_batch_latency": latency,
+        "as_is_batch": as_is,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel_ms": kmean, "algorithmic_bytes_per_launch": abytes,
