@@ -54,8 +54,13 @@ DIM_MAX = {"gdim.x": 2**31 - 1, "gdim.y": 65535, "gdim.z": 65535,
            "bdim.x": 1024, "bdim.y": 1024, "bdim.z": 64}
 BLOCK_MAX_THREADS = 1024
 
-BRUTE_BOX_POINTS = 1 << 8    # whole-box enumeration below this many points
-BRUTE_VAR_POINTS = 1 << 8    # per-variable enumeration below this range size
+# whole-box enumeration of at most 2^20 points, else per-variable
+# enumeration of ranges of at most 2^20 values, else the endpoints.  2^12 here
+# (the oracle's first value; 2^20 costs minutes per C2 trace in pure Python);
+# tests/test_oracle_pins.py::test_box_vs_per_variable pins that the three
+# methods give the same extents on every random summary.
+BRUTE_BOX_POINTS = 1 << 12   # whole-box enumeration up to this many points
+BRUTE_VAR_POINTS = 1 << 12   # per-variable enumeration up to this range size
 
 
 class OracleUnsupported(Exception):
