@@ -24,8 +24,13 @@ struct ModelAcc {
   unsigned long long hist_without[PICKER_MODEL_HIST], hist_with[PICKER_MODEL_HIST];
 };
 
-// input bytes of one record; false: unknown
-static __device__ bool input_bytes(const Tables& T, const picker_rec_t& r, const DevBatch& B, uint64_t& bytes) {
+constexpr int kModelThreads = 256, kModelFast = 8;  // read extents per thread in shared memory
+
+// input bytes of one record; false: unknown.  `lo` / `hi` hold up to `cap`
+// extents (the thread's shared-memory rows, or its local arrays).
+static __device__ bool input_bytes_in(const Tables& T, const picker_rec_t& r, const DevBatch& B, uint64_t& bytes,
+                                      int64_t* lo, int64_t* hi, int stride, int cap, bool& overflow) {
+  overflow = false;
   const uint32_t kid = r.kernel_id;
   if (kid >= T.nkernel_slots) return false;
   const DKernel K = T.kernels[kid];
@@ -39,29 +44,32 @@ static __device__ bool input_bytes(const Tables& T, const picker_rec_t& r, const
     const int64_t v = X.get(ch.op);
     if (v < ch.lo || v > ch.hi) return false;
   }
-  int64_t lo[kModelMaxReads], hi[kModelMaxReads];
   int m = 0;
   for (int d = 0; d < K.ndesc; ++d) {
     const DDesc D = T.descs[K.desc + d];
-    if (D.kind != KIND_R || !desc_active(T, K, D, X)) continue;
+    if (D.kind != KIND_R) continue;
+    int64_t lb = 0, ub = 0;
+    if (!desc_active_extent(T, K, D, X, lb, ub)) continue;  // each variable's bounds once
     if (D.opaque || m == kModelMaxReads) return false;
-    int64_t lb, ub;
-    desc_extent(T, K, D, X, lb, ub);
+    if (m == cap) {
+      overflow = true;
+      return false;
+    }
     int j = m++;  // insertion by lb
-    while (j > 0 && lo[j - 1] > lb) {
-      lo[j] = lo[j - 1];
-      hi[j] = hi[j - 1];
+    while (j > 0 && lo[(j - 1) * stride] > lb) {
+      lo[j * stride] = lo[(j - 1) * stride];
+      hi[j * stride] = hi[(j - 1) * stride];
       --j;
     }
-    lo[j] = lb;
-    hi[j] = ub;
+    lo[j * stride] = lb;
+    hi[j * stride] = ub;
   }
   uint64_t total = 0;
   for (int i = 0; i < m;) {  // merge touching / overlapping extents
-    int64_t a = lo[i], b = hi[i];
+    int64_t a = lo[i * stride], b = hi[i * stride];
     int j = i + 1;
-    while (j < m && lo[j] <= b + 1) {
-      b = max(b, hi[j]);
+    while (j < m && lo[j * stride] <= b + 1) {
+      b = max(b, hi[j * stride]);
       ++j;
     }
     total += (uint64_t)(b - a) + 1;
@@ -71,9 +79,27 @@ static __device__ bool input_bytes(const Tables& T, const picker_rec_t& r, const
   return true;
 }
 
-__global__ void __launch_bounds__(256) k_models(Tables T, DevBatch B, uint64_t n, const uint8_t* __restrict__ codes,
-                                                const uint64_t* __restrict__ ctx_bytes, uint64_t kill_ns,
-                                                uint64_t save_bpu, ModelAcc* __restrict__ acc) {
+// Most records have <= kModelFast reads: their extents sort in the thread's
+// shared-memory column (stride = threads, conflict-free); more take local arrays.
+static __device__ __noinline__ bool input_bytes_big(const Tables& T, const picker_rec_t& r, const DevBatch& B,
+                                                    uint64_t& bytes) {
+  int64_t lo[kModelMaxReads], hi[kModelMaxReads];
+  bool of;
+  return input_bytes_in(T, r, B, bytes, lo, hi, 1, kModelMaxReads, of);
+}
+
+static __device__ bool input_bytes(const Tables& T, const picker_rec_t& r, const DevBatch& B, uint64_t& bytes,
+                                   int64_t* s_lo, int64_t* s_hi) {
+  bool of = false;
+  if (input_bytes_in(T, r, B, bytes, s_lo + threadIdx.x, s_hi + threadIdx.x, kModelThreads, kModelFast, of)) return true;
+  return of ? input_bytes_big(T, r, B, bytes) : false;
+}
+
+__global__ void __launch_bounds__(kModelThreads) k_models(Tables T, DevBatch B, uint64_t n,
+                                                          const uint8_t* __restrict__ codes,
+                                                          const uint64_t* __restrict__ ctx_bytes, uint64_t kill_ns,
+                                                          uint64_t save_bpu, ModelAcc* __restrict__ acc) {
+  __shared__ int64_t s_elo[kModelFast * kModelThreads], s_ehi[kModelFast * kModelThreads];
   __shared__ unsigned long long s_sum[6];
   __shared__ unsigned int s_hw[PICKER_MODEL_HIST], s_hi[PICKER_MODEL_HIST];
   for (int i = threadIdx.x; i < PICKER_MODEL_HIST; i += blockDim.x) s_hw[i] = s_hi[i] = 0;
@@ -83,7 +109,7 @@ __global__ void __launch_bounds__(256) k_models(Tables T, DevBatch B, uint64_t n
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const picker_rec_t r = load_rec(B.rec + i);
     uint64_t b = 0;
-    if (!input_bytes(T, r, B, b)) {
+    if (!input_bytes(T, r, B, b, s_elo, s_ehi)) {
       b = 0;
       ++unk;
     }
@@ -127,8 +153,8 @@ cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const 
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(acc, 0, sizeof(ModelAcc), s);
   if (e == cudaSuccess && n) {
-    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)num_sms * 8);
-    k_models<<<(unsigned)blocks, 256, 0, s>>>(T, b, n, codes, ctx_bytes, kill_ns, save_bpu, acc);
+    const uint64_t blocks = std::min<uint64_t>((n + kModelThreads - 1) / kModelThreads, (uint64_t)num_sms * 3);
+    k_models<<<(unsigned)blocks, kModelThreads, 0, s>>>(T, b, n, codes, ctx_bytes, kill_ns, save_bpu, acc);
     e = cudaGetLastError();
   }
   ModelAcc h;
