@@ -61,7 +61,8 @@ struct JitModule {
   // S4 validate, S5 emit; its scratch grows with the largest batch seen
   cudaKernel_t sk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int sort_warps = 0;
-  size_t sort_smem = 0;
+  bool sort_ws = false;  // S4 warp-specialised (sk[1], k_validate_sorted_ws)
+  size_t sort_smem = 0, sort_ws_smem = 0;
   void* sort_buf = nullptr;
   size_t sort_cap = 0;  // records the scratch holds
 };
@@ -502,10 +503,13 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   nvrtcAddNameExpression(prog, small_expr);
   // the shape-sorted schedule's kernels (k_sorted.cuh), when the module has them
   const bool sorted = src.find("k_validate_sorted<JitDispatch>") != std::string::npos;
+  const bool sorted_ws = src.find("k_validate_sorted_ws<JitDispatch>") != std::string::npos;
   const char* sort_exprs[] = {"picker::k_sort_keys", "picker::k_sort_scatter",
-                              "picker::k_validate_sorted<picker::JitDispatch>", "picker::k_sort_emit"};
+                              "picker::k_validate_sorted<picker::JitDispatch>", "picker::k_sort_emit",
+                              "picker::k_validate_sorted_ws<picker::JitDispatch>"};
+  const int nsort = sorted_ws ? 5 : 4;
   if (sorted)
-    for (const char* e : sort_exprs) nvrtcAddNameExpression(prog, e);
+    for (int q = 0; q < nsort; ++q) nvrtcAddNameExpression(prog, sort_exprs[q]);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
                                    "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
   for (auto& d : defines) opts.push_back(d.c_str());
@@ -526,9 +530,9 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   nvrtcGetLoweredName(prog, small_expr, &low);
   lowered += std::string("\n") + (low ? low : "");  // main kernel, small-batch kernel
   if (sorted)
-    for (const char* e : sort_exprs) {  // then the sorted schedule's four kernels
+    for (int q = 0; q < nsort; ++q) {  // then the sorted schedule's kernels
       low = nullptr;
-      nvrtcGetLoweredName(prog, e, &low);
+      nvrtcGetLoweredName(prog, sort_exprs[q], &low);
       lowered += std::string("\n") + (low ? low : "");
     }
   size_t n = 0;
@@ -541,7 +545,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws) {
   JitPlan P;
   std::ostringstream src;
   // paths no kernel of this summary takes are left out of the module (code size)
@@ -687,6 +691,10 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted) {
               ? "template __global__ void k_validate_sorted<JitDispatch>(const __grid_constant__ BucketParams, "
                 "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
               : "")
+      << (sorted && sort_ws && shape_shortcut + 1 <= kSortKeys
+              ? "template __global__ void k_validate_sorted_ws<JitDispatch>(const __grid_constant__ BucketParams, "
+                "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
+              : "")
       << ""
          "}  // namespace picker\n";
   P.src = src.str();
@@ -712,6 +720,7 @@ std::vector<std::string> geometry_defines(const Options& opt) {
           "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
           "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
           "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot)),
+          "-DPICKER_SORT_STAGES=" + std::to_string(std::max(2, opt.sort_warps)),
           "-DPICKER_PIPE_KEYS=" + std::to_string(opt.pipe_keys > 64 ? 128 : 64)};
 }
 
@@ -765,7 +774,12 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
     const int slot = (int)((std::min<size_t>(std::max<size_t>(maxargs, 1), 62) * 8 + 16 + 15) / 16 * 16);
     if (opt.sort_slot <= 0) opt.sort_slot = slot;
     opt.sort_slot = (opt.sort_slot + 15) / 16 * 16;
-    if (opt.sort_warps <= 0) opt.sort_warps = std::max(1, std::min(16, (200 * 1024) / (32 * opt.sort_slot)));
+    if (opt.sort_ws < 0) opt.sort_ws = 0;  // measured: the warp-specialised S4 is slower (r02_ab_log)
+    // plain: one slot per lane; warp-specialised: one stage (32 headers + 32
+    // slots) per warp (stages >= consumers + 1)
+    if (opt.sort_warps <= 0)
+      opt.sort_warps = opt.sort_ws ? std::max(2, std::min(16, (210 * 1024) / (32 * (opt.sort_slot + 32))))
+                                   : std::max(1, std::min(16, (200 * 1024) / (32 * opt.sort_slot)));
   }
   if (opt.tile != 0) return opt;
   if (mean <= 6.0) {
@@ -790,7 +804,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
@@ -814,13 +828,20 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, names[0].c_str());
   if (e == cudaSuccess && names.size() > 1 && !names[1].empty())
     e = cudaLibraryGetKernel(&m->small_kernel, m->lib, names[1].c_str());
-  if (names.size() == 6)  // S1 keys, S3 scatter, S4 validate, S5 emit
+  if (names.size() >= 6) {  // S1 keys, S3 scatter, S4 validate, S5 emit [, S4 warp-specialised]
     for (int q : {0, 2, 3, 4})
       if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->sk[q], m->lib, names[2 + (q ? q - 1 : 0)].c_str());
+    if (e == cudaSuccess && names.size() == 7) e = cudaLibraryGetKernel(&m->sk[1], m->lib, names[6].c_str());
+  }
   if (e == cudaSuccess && m->sk[3]) {
     m->sort_warps = opt.sort_warps;
+    m->sort_ws = opt.sort_ws != 0;
     m->sort_smem = (size_t)opt.sort_warps * 32 * opt.sort_slot;
+    m->sort_ws_smem = (size_t)opt.sort_warps * (32 * 32 + 32 * (size_t)opt.sort_slot);  // stages = warps
     e = cudaFuncSetAttribute((const void*)m->sk[3], cudaFuncAttributeMaxDynamicSharedMemorySize, (int)m->sort_smem);
+    if (e == cudaSuccess && m->sk[1])
+      e = cudaFuncSetAttribute((const void*)m->sk[1], cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)m->sort_ws_smem);
   }
   if (e == cudaSuccess) e = cudaMalloc(&m->d_consts, plan.consts.size() * sizeof(int64_t));
   // kernel id -> (bin | shape << 16); bins are positions in `ks`
@@ -941,8 +962,11 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     void* a3[] = {(void*)&n, (void*)&S};
     if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[2], dim3(S.nblk), dim3(kSortBlock), a3, 0, s);
     void* a4[] = {(void*)&P, (void*)&B, (void*)&S, (void*)&flags};
-    if (e == cudaSuccess)
-      e = cudaLaunchKernel((const void*)m->sk[3], dim3(num_sms), dim3(m->sort_warps * 32), a4, m->sort_smem, s);
+    if (e == cudaSuccess) {
+      const bool ws = m->sort_ws && m->sk[1] && n < (1ULL << 30);
+      e = cudaLaunchKernel((const void*)(ws ? m->sk[1] : m->sk[3]), dim3(num_sms), dim3(m->sort_warps * 32), a4,
+                           ws ? m->sort_ws_smem : m->sort_smem, s);
+    }
     const uint64_t words = (n + 31) / 32;
     const unsigned eb = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)num_sms * 8);
     const uint8_t* cf = flags;

@@ -36,6 +36,9 @@ namespace picker {
 #ifndef PICKER_SORT_WARPS
 #define PICKER_SORT_WARPS 16
 #endif
+#ifndef PICKER_SORT_STAGES
+#define PICKER_SORT_STAGES 13
+#endif
 #ifndef PICKER_SORT_SLOT
 #define PICKER_SORT_SLOT 432  // bytes of one record's argument slot (multiple of 16)
 #endif
@@ -222,6 +225,163 @@ __global__ void __launch_bounds__(kSortThreads, 1)
     // the next group's headers into L2 while this warp finishes
     if ((uint32_t)lane < remn) asm volatile("prefetch.global.L2 [%0];" ::"l"(B.rec + pin) : "memory");
     g = gn, k = kn_, start = startn, rem = remn, pi = pin;
+  }
+}
+
+// S4, warp-specialised (PICKER_SORT_WS): warp 0 of each CTA is a producer
+// that claims the CTA's groups in order and stages each one -- permutation
+// entries, headers and 16-byte-rounded argument spans, all with cp.async --
+// into the next stage of a ring in shared memory, completing the stage's
+// `full` mbarrier (32 cp.async-tracked arrivals + one arrival that publishes
+// the stage's metadata); the other warps are consumers that take stages in
+// ring order, evaluate their 32 records from shared memory and release the
+// stage (`empty`).  The producer runs up to kSortStages groups ahead, so the
+// consumers never wait on a memory round trip of their own; after the last
+// group it publishes one DONE stage per consumer.
+constexpr uint32_t kSortStages = PICKER_SORT_STAGES;
+constexpr uint32_t kStageBytes = 32 * 32 + 32 * kSortSlot;  // headers, argument slots
+constexpr uint32_t kGroupDone = 0xFFFFFFFFu;
+
+template <class Dispatch>
+__global__ void __launch_bounds__(kSortThreads, 1)
+    k_validate_sorted_ws(const __grid_constant__ BucketParams P, const __grid_constant__ DevBatch B, SortScratch S,
+                         uint8_t* __restrict__ flags) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ uint32_t s_off[kSortKeys + 1], s_cnt[kSortKeys], s_g[kSortKeys + 1];
+  __shared__ __align__(8) uint64_t s_full[kSortStages], s_empty[kSortStages];
+  __shared__ uint32_t s_meta_g[kSortStages];
+  __shared__ uint32_t s_meta_i[kSortStages][32];  // record index | local << 31 | shift (8 B) << 28
+  __shared__ uint32_t s_take;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid < 32) key_tables(S, s_off, s_cnt, s_g);
+  if (tid == 0) {
+    for (uint32_t b = 0; b < kSortStages; ++b) mbar_init(&s_full[b], 33), mbar_init(&s_empty[b], 1);
+    s_take = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const uint32_t ngroups = s_g[kSortKeys];
+  auto group = [&](uint32_t g, uint32_t& k, uint32_t& start, uint32_t& rem) {
+    k = 0;
+#pragma unroll
+    for (uint32_t step = kSortKeys / 2; step > 0; step >>= 1)
+      if (s_g[k + step] <= g) k += step;
+    const uint32_t j = g - s_g[k];
+    start = s_off[k] + 32u * j;
+    rem = min(32u, s_cnt[k] - 32u * j);
+  };
+  constexpr uint32_t kConsumers = kSortWarps - 1;
+  if (warp == 0) {
+    // ---- producer ----
+    const uintptr_t p0 = (uintptr_t)(B.args + B.args_lo), p1 = (uintptr_t)(B.args + B.args_hi);
+    // the CTA's groups: blockIdx.x + j * gridDim.x (static: increasing, so the
+    // DONE stages come last; every CTA walks the shapes in the same order).
+    // Lookahead: the permutation entry of j+2 and the header of j+1 are loaded
+    // during j, so no load of the producer waits for its own result.
+    const uint32_t G = gridDim.x;
+    uint32_t g = blockIdx.x;
+    uint32_t k = 0, start = 0, rem = 0, pi = 0;
+    uint32_t k1 = 0, start1 = 0, rem1 = 0, pi1 = 0;
+    picker_rec_t r{};
+    if (g < ngroups) {
+      group(g, k, start, rem);
+      pi = (uint32_t)lane < rem ? S.perm[start + lane] : 0u;
+    }
+    if (g + G < ngroups) {
+      group(g + G, k1, start1, rem1);
+      pi1 = (uint32_t)lane < rem1 ? S.perm[start1 + lane] : 0u;
+    }
+    if (g < ngroups && (uint32_t)lane < rem) r = load_rec(B.rec + pi);
+    uint32_t done = 0;
+    for (uint32_t t = 0; done < kConsumers; ++t, g += G) {
+      const uint32_t b = t % kSortStages, round = t / kSortStages;
+      // group j+2's permutation entries, j+1's headers: in flight during j
+      uint32_t k2 = 0, start2 = 0, rem2 = 0, pi2 = 0;
+      if (g + 2 * G < ngroups) {
+        group(g + 2 * G, k2, start2, rem2);
+        pi2 = (uint32_t)lane < rem2 ? S.perm[start2 + lane] : 0u;
+      }
+      picker_rec_t r1{};
+      if (g + G < ngroups && (uint32_t)lane < rem1) r1 = load_rec(B.rec + pi1);
+      mbar_wait(&s_empty[b], (round & 1) ^ 1);  // released by its consumer of the previous round
+      unsigned char* st = smem + (size_t)b * kStageBytes;
+      if (g < ngroups) {
+        uint32_t info = 0;
+        if ((uint32_t)lane < rem) {
+          // header into the stage; the argument span when well-formed and small
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n\tcp.async.cg.shared.global [%2], [%3], 16;" ::"r"(
+                           smem_u32(st + 32 * lane)),
+                       "l"(B.rec + pi), "r"(smem_u32(st + 32 * lane + 16)),
+                       "l"(reinterpret_cast<const char*>(B.rec + pi) + 16)
+                       : "memory");
+          uint32_t kb, kn;
+          kb_lookup(P, r.kernel_id, kb, kn);
+          const uintptr_t a0 = (uintptr_t)(B.args + r.arg_off), a1 = a0 + 8ull * r.nargs;
+          const uintptr_t c0 = a0 & ~(uintptr_t)15, c1 = (a1 + 15) & ~(uintptr_t)15;
+          const bool in_pool = r.arg_off >= B.args_lo && r.arg_off <= B.args_hi &&
+                               (uint64_t)r.nargs <= B.args_hi - r.arg_off;
+          const bool local = !(kWidePath && k == P.wide_key) && r.nargs == (kn >> 24) && in_pool && c0 >= p0 &&
+                             c1 <= p1 && c1 - c0 <= kSortSlot;
+          if (local) {
+            unsigned char* slot = st + 32 * 32 + lane * kSortSlot;
+            for (uintptr_t c = c0; c < c1; c += 16)
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(slot + (c - c0))), "l"(c)
+                           : "memory");
+          }
+          info = pi | (local ? 1u << 31 : 0u) | ((uint32_t)(a0 - c0) >> 3) << 30;  // pi < 2^30
+        }
+        s_meta_i[b][lane] = info;
+        if (lane == 0) s_meta_g[b] = g;
+      } else {
+        if (lane == 0) s_meta_g[b] = kGroupDone;
+        ++done;
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&s_full[b])) : "memory");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_full[b])) : "memory");
+      k = k1, start = start1, rem = rem1, pi = pi1, r = r1;
+      k1 = k2, start1 = start2, rem1 = rem2, pi1 = pi2;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    return;
+  }
+  // ---- consumers ----
+  for (;;) {
+    uint32_t t = 0;
+    if (lane == 0) t = atomicAdd(&s_take, 1u);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    const uint32_t b = t % kSortStages, round = t / kSortStages;
+    mbar_wait(&s_full[b], round & 1);
+    const uint32_t g = s_meta_g[b];
+    if (g == kGroupDone) return;
+    uint32_t k, start, rem;
+    group(g, k, start, rem);
+    unsigned char* st = smem + (size_t)b * kStageBytes;
+    if (kWidePath && k == P.wide_key) {  // K2: the whole warp on one record at a time, scratch = the slots
+      for (uint32_t q = 0; q < rem; ++q) {
+        const uint32_t wi = s_meta_i[b][q] & 0x3FFFFFFFu;
+        const picker_rec_t r = rec_from_smem(st + 32 * q);
+        const bool in_smem = P.T.kernels[r.kernel_id < P.T.nkernel_slots ? r.kernel_id : 0].ndesc <= kSortSlot;
+        const uint8_t c = eval_wide_warp(P.T, r, B.args + r.arg_off, B.args_lo, B.args_hi, lane,
+                                         in_smem ? reinterpret_cast<WideElem*>(st + 32 * 32) : wide_scratch(P, warp),
+                                         in_smem ? kSortSlot : (uint32_t)kWideMax);
+        if (lane == 0) flags[wi] = c;
+      }
+    } else if ((uint32_t)lane < rem) {
+      const uint32_t info = s_meta_i[b][lane];
+      const uint32_t i = info & 0x3FFFFFFFu;
+      const bool local = info >> 31;
+      const picker_rec_t r = rec_from_smem(st + 32 * lane);
+      uint32_t kb, kn;
+      kb_lookup(P, r.kernel_id, kb, kn);
+      const int64_t* a = local ? reinterpret_cast<const int64_t*>(st + 32 * 32 + lane * kSortSlot +
+                                                                 8 * ((info >> 30) & 1u))
+                               : B.args + r.arg_off;
+      flags[i] = Dispatch::eval(k, kb & 0xFFFFu, kn, local, P, r, a, B);
+    }
+    __syncwarp();
+    if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&s_empty[b])) : "memory");
   }
 }
 

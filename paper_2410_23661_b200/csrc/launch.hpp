@@ -32,6 +32,7 @@ struct Options {
   // per-record argument slot bytes are resolved with the geometry
   int sorted = -1, sort_warps = 0, sort_slot = 0;
   int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
+  int sort_ws = -1;   // sorted schedule: warp-specialised S4 (1), one warp per group (0), -1 auto
 };
 
 struct JitModule;
@@ -49,7 +50,7 @@ struct JitPlan {
   std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
   int nshapes = 0;
 };
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false);
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false);
 bool jit_is_stride(const JitModule* m);
 // Kernel launches one picker_validate_batch of n records makes on the module.
 int jit_launch_count(const JitModule* m, uint64_t n);

@@ -144,6 +144,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sorted") c->opt.sorted = v < 0 ? -1 : (int)(v != 0);
   else if (k == "sort_slot") c->opt.sort_slot = (int)v;    // tuning: average argument bytes per lane
   else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
+  else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
@@ -295,7 +296,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     select_paths(ks, opt);
     order_by_shape(ks);
     Options geo = resolve_geometry(ks, opt);
-    JitPlan plan = jit_plan(ks, false, geo.sorted > 0);
+    JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0);
     geo.pipe_keys = 3 + plan.nshapes + 1;  // SHAPE_FIRST + shapes + the shortcut key
     std::string cubin, lowered, err;
     if (!jit_compile(plan, geo, cubin, lowered, false, err)) {

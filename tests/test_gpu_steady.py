@@ -127,7 +127,7 @@ def test_c4_tiled_steady_state(pk):
     64-record tiles, >100 per CTA)."""
     s, rec, args, meta = workloads.make_c4(n=1 << 12)
     want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
-    for R, opt in [(256, dict(jit=1)), (256, dict(jit=1, sorted=0)),
+    for R, opt in [(256, dict(jit=1)), (256, dict(jit=1, sort_ws=1)), (256, dict(jit=1, sorted=0)),
                    (8, dict(jit=1, sorted=0, tile=64, threads=32, ctas=1, args_per_rec=20))]:
         rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
         flags, bits, counts = _run(pk, s, rec_t, args_t, **opt)
