@@ -185,24 +185,6 @@ int picker_exact_check(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t 
                        uint8_t* exact_out, uint64_t* counts_out,
                        uint64_t max_points_per_instance, void* stream);
 
-/* Resident validator: the paper's per-launch check ("validates
- * the idempotency ... before launching" in under 5 us on the CPU) without a
- * kernel launch per check.  Set option "serve" = 1 before
- * picker_load_summaries; picker_serve_start launches one resident warp on its
- * own stream that polls a request mailbox in mapped pinned host memory (one SM
- * is given up while it runs); picker_serve_validate (HOST pointers: n <= 32
- * records whose arg_off index args[0..nargs), nargs <= 2048) writes the
- * request, spins until the warp has written the n codes back and copies them to
- * codes_out; synchronous, PICKER_ECUDA after timeout_us without an answer.
- * picker_serve_stop ends the warp (also done by picker_destroy).  While it
- * runs, a device-wide synchronisation (cudaDeviceSynchronize) would wait for
- * it: synchronise streams instead.  Reloading summaries requires a stop first
- * (PICKER_EINVAL).                                                            */
-int picker_serve_start(picker_ctx_t* ctx);
-int picker_serve_validate(picker_ctx_t* ctx, const picker_rec_t* rec, uint32_t n, const int64_t* args,
-                          uint32_t nargs, uint8_t* codes_out, uint64_t timeout_us);
-int picker_serve_stop(picker_ctx_t* ctx);
-
 /* Device-side replication of a launch-record stream (K6; SURVEY §8F C5 and
  * §8 row e: shards generated on the GPU instead of copied over PCIe).  Writes
  * `copies` copies of the n base records and their argument pool: record

@@ -62,9 +62,6 @@ SIGNATURES = {
     "picker_validate_batch_host": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P,
                                                   P]),
     "picker_exact_check": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, U64, P]),
-    "picker_serve_start": (ctypes.c_int, [P]),
-    "picker_serve_validate": (ctypes.c_int, [P, P, ctypes.c_uint32, P, ctypes.c_uint32, P, U64]),
-    "picker_serve_stop": (ctypes.c_int, [P]),
     "picker_replicate": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, U64, U64, ctypes.c_int64, P, P,
                                         P]),
     "picker_validate_sequence": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, ctypes.c_uint32,

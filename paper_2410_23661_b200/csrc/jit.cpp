@@ -62,7 +62,6 @@ struct JitModule {
   cudaKernel_t sk[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   int sort_warps = 0;
   bool sort_ws = false;  // S4 warp-specialised (sk[1], k_validate_sorted_ws)
-  cudaKernel_t serve_kernel = nullptr;  // k_serve (option serve set before loading)
   size_t sort_smem = 0, sort_ws_smem = 0;
   void* sort_buf = nullptr;
   size_t sort_cap = 0;  // records the scratch holds
@@ -511,9 +510,6 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
   const int nsort = sorted_ws ? 5 : 4;
   if (sorted)
     for (int q = 0; q < nsort; ++q) nvrtcAddNameExpression(prog, sort_exprs[q]);
-  const bool serve = src.find("k_serve<JitDispatch>") != std::string::npos;
-  const char* serve_expr = "picker::k_serve<picker::JitDispatch>";
-  if (serve) nvrtcAddNameExpression(prog, serve_expr);
   std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-default-device",
                                    "-lineinfo", "-DPICKER_NO_LIBC_HEADERS"};
   for (auto& d : defines) opts.push_back(d.c_str());
@@ -523,7 +519,15 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
     nvrtcGetProgramLogSize(prog, &n);
     std::string log(n, '\0');
     nvrtcGetProgramLog(prog, &log[0]);
-    err = std::string(nvrtcGetErrorString(r)) + ": " + log.substr(0, 4000);
+    // the errors first (the log starts with the generated code's warnings)
+    std::string errs;
+    for (size_t a = 0, b; a < log.size(); a = b + 1) {
+      b = log.find('\n', a);
+      if (b == std::string::npos) b = log.size();
+      const std::string ln = log.substr(a, b - a);
+      if (ln.find("error") != std::string::npos) errs += ln + "\n";
+    }
+    err = std::string(nvrtcGetErrorString(r)) + ": " + (errs + log).substr(0, 4000);
     nvrtcDestroyProgram(&prog);
     return false;
   }
@@ -539,11 +543,6 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
       nvrtcGetLoweredName(prog, sort_exprs[q], &low);
       lowered += std::string("\n") + (low ? low : "");
     }
-  if (serve) {  // the resident validator, tagged so it is found whatever precedes it
-    low = nullptr;
-    nvrtcGetLoweredName(prog, serve_expr, &low);
-    lowered += std::string("\nserve:") + (low ? low : "");
-  }
   size_t n = 0;
   nvrtcGetCUBINSize(prog, &n);
   cubin.assign(n, '\0');
@@ -554,7 +553,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws, bool serve) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws) {
   JitPlan P;
   std::ostringstream src;
   // paths no kernel of this summary takes are left out of the module (code size)
@@ -568,7 +567,6 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
          "typedef unsigned long long uint64_t; typedef unsigned long size_t; typedef unsigned long uintptr_t;\n"
          "#include \"eval_generic.cuh\"\n#include \"eval_stride.cuh\"\n#include \"k_bucket.cuh\"\n"
       << (sorted ? "#include \"k_sorted.cuh\"\n" : "")
-      << (serve ? "#include \"k_serve.cuh\"\n" : "")
       << ""
          "namespace picker {\n";
   // pass 1: body text with every constant as a load, grouped into shapes
@@ -701,9 +699,6 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
               ? "template __global__ void k_validate_sorted<JitDispatch>(const __grid_constant__ BucketParams, "
                 "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
               : "")
-      << (serve ? "template __global__ void k_serve<JitDispatch>(const __grid_constant__ BucketParams, ServeRequest*, "
-                  "ServeResponse*);\n"
-                : "")
       << (sorted && sort_ws && shape_shortcut + 1 <= kSortKeys
               ? "template __global__ void k_validate_sorted_ws<JitDispatch>(const __grid_constant__ BucketParams, "
                 "const __grid_constant__ DevBatch, SortScratch, uint8_t*);\n"
@@ -817,7 +812,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.serve);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
@@ -833,17 +828,11 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->ctas = opt.ctas;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   std::vector<std::string> names;  // main, small, [the sorted schedule's kernels]
-  std::string serve_name;
   for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
     b = lowered.find('\n', a);
     if (b == std::string::npos) b = lowered.size();
-    const std::string nm = lowered.substr(a, b - a);
-    if (nm.rfind("serve:", 0) == 0)
-      serve_name = nm.substr(6);
-    else
-      names.push_back(nm);
+    names.push_back(lowered.substr(a, b - a));
   }
-  if (e == cudaSuccess && !serve_name.empty()) e = cudaLibraryGetKernel(&m->serve_kernel, m->lib, serve_name.c_str());
   if (e == cudaSuccess) e = cudaLibraryGetKernel(&m->kernel, m->lib, names[0].c_str());
   if (e == cudaSuccess && names.size() > 1 && !names[1].empty())
     e = cudaLibraryGetKernel(&m->small_kernel, m->lib, names[1].c_str());
@@ -926,19 +915,6 @@ bool jit_is_stride(const JitModule* m) { return m && m->stride; }
 int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 : 0; }
 
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
-
-const void* jit_serve_kernel(const JitModule* m) { return m ? (const void*)m->serve_kernel : nullptr; }
-
-BucketParams jit_params(const JitModule* m, const BucketParams& P0) {
-  BucketParams P = P0;
-  P.jit_consts = m->d_consts;
-  P.kb_of = m->d_kb;
-  P.kb_unknown = m->kb_unknown;
-  P.nkeys = m->nkeys;
-  P.wide_key = m->stride ? 0xFFFFFFFFu : SHAPE_WIDE;
-  P.direct_key = m->shortcut_key;
-  return P;
-}
 
 int jit_launch_count(const JitModule* m, uint64_t n) {
   return m && m->sk[3] && n > kSmallMax && n < (1ULL << 32) ? 4 : 1;

@@ -33,7 +33,6 @@ struct Options {
   int sorted = -1, sort_warps = 0, sort_slot = 0;
   int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
   int sort_ws = -1;   // sorted schedule: warp-specialised S4 (1), one warp per group (0), -1 auto
-  bool serve = false;  // compile the resident validator (k_serve.cuh) into the module
 };
 
 struct JitModule;
@@ -51,13 +50,8 @@ struct JitPlan {
   std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
   int nshapes = 0;
 };
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false,
-                 bool serve = false);
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false);
 bool jit_is_stride(const JitModule* m);
-// The resident validator of the module (nullptr unless option serve), and the
-// launch parameters of the module's kernels.
-const void* jit_serve_kernel(const JitModule* m);
-BucketParams jit_params(const JitModule* m, const BucketParams& P0);
 // Kernel launches one picker_validate_batch of n records makes on the module.
 int jit_launch_count(const JitModule* m, uint64_t n);
 // Warps per SM of the specialised module's persistent kernel (CTAs x threads / 32).

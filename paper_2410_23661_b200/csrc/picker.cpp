@@ -4,15 +4,12 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
-#include <atomic>
-#include <chrono>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "launch.hpp"
 #include "loader.hpp"
-#include "serve.hpp"
 
 using namespace picker;
 
@@ -40,11 +37,6 @@ struct picker_ctx {
   uint32_t max_width = 1;       // widest descriptor of the loaded summaries
   int last_launches = 0;
   bool bucket_auto = false;  // table-driven grouping when opt.bucket = -1 (launch.hpp)
-  // resident validator (picker_serve_*): mailboxes in mapped pinned host memory
-  ServeRequest* serve_req = nullptr;
-  ServeResponse* serve_resp = nullptr;
-  cudaStream_t serve_stream = nullptr;
-  uint32_t serve_seq = 0;
 };
 
 static std::string g_create_err;
@@ -118,7 +110,6 @@ int picker_create(picker_ctx_t** out, int device) {
 
 void picker_destroy(picker_ctx_t* c) {
   if (!c) return;
-  picker_serve_stop(c);
   {
     DevGuard g(c->device);
     if (c->dev_tables) cudaFree(c->dev_tables);
@@ -154,14 +145,12 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sort_slot") c->opt.sort_slot = (int)v;    // tuning: average argument bytes per lane
   else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
   else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
-  else if (k == "serve") c->opt.serve = v != 0;  // compile the resident validator at the next load
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
 
 int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   if (!c) return PICKER_EINVAL;
-  if (c->serve_req) return fail(c, PICKER_EINVAL, "stop the resident validator before loading");
   if (!text && len) return fail(c, PICKER_EINVAL, "null summary text");
   DevGuard g(c->device);
   if (!g.ok) return fail(c, PICKER_ECUDA, "cudaSetDevice failed");
@@ -307,9 +296,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     select_paths(ks, opt);
     order_by_shape(ks);
     Options geo = resolve_geometry(ks, opt);
-    // (PICKER_COMPILE_SERVE: also instantiate the resident validator -- a CPU
-    // compile check of k_serve.cuh)
-    JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0, getenv("PICKER_COMPILE_SERVE") != nullptr);
+    JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0);
     geo.pipe_keys = 3 + plan.nshapes + 1;  // SHAPE_FIRST + shapes + the shortcut key
     std::string cubin, lowered, err;
     if (!jit_compile(plan, geo, cubin, lowered, false, err)) {
@@ -515,82 +502,6 @@ int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
                                 c->num_sms, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "consumer models");
   c->last_launches = n ? 1 : 0;
-  return PICKER_OK;
-}
-
-int picker_serve_start(picker_ctx_t* c) {
-  if (!c) return PICKER_EINVAL;
-  if (!c->loaded) return fail(c, PICKER_ENOTLOADED, "no summaries loaded");
-  if (c->serve_req) return PICKER_OK;
-  const void* kern = jit_serve_kernel(c->jit);
-  if (!kern) return fail(c, PICKER_EINVAL, "set option serve = 1 before picker_load_summaries");
-  DevGuard g(c->device);
-  cudaError_t e = cudaHostAlloc((void**)&c->serve_req, sizeof(ServeRequest), cudaHostAllocMapped);
-  if (e == cudaSuccess) e = cudaHostAlloc((void**)&c->serve_resp, sizeof(ServeResponse), cudaHostAllocMapped);
-  if (e != cudaSuccess) {
-    if (c->serve_req) cudaFreeHost(c->serve_req);
-    c->serve_req = nullptr;
-    return fail(c, PICKER_ENOMEM, "pinned mailboxes");
-  }
-  memset(c->serve_req, 0, sizeof(ServeRequest));
-  memset(c->serve_resp, 0, sizeof(ServeResponse));
-  c->serve_seq = 0;
-  ServeRequest* dreq = nullptr;
-  ServeResponse* dresp = nullptr;
-  e = cudaHostGetDevicePointer((void**)&dreq, c->serve_req, 0);
-  if (e == cudaSuccess) e = cudaHostGetDevicePointer((void**)&dresp, c->serve_resp, 0);
-  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&c->serve_stream, cudaStreamNonBlocking);
-  BucketParams P = jit_params(c->jit, c->P);
-  void* argv[] = {(void*)&P, (void*)&dreq, (void*)&dresp};
-  if (e == cudaSuccess) e = cudaLaunchKernel(kern, dim3(1), dim3(32), argv, 0, c->serve_stream);
-  if (e != cudaSuccess) {
-    cudaFreeHost(c->serve_req);
-    cudaFreeHost(c->serve_resp);
-    c->serve_req = nullptr, c->serve_resp = nullptr;
-    return cuda_fail(c, e, "resident validator launch");
-  }
-  return PICKER_OK;
-}
-
-int picker_serve_validate(picker_ctx_t* c, const picker_rec_t* rec, uint32_t n, const int64_t* args, uint32_t nargs,
-                          uint8_t* codes_out, uint64_t timeout_us) {
-  if (!c || (n && (!rec || !codes_out)) || (nargs && !args)) return PICKER_EINVAL;
-  if (!c->serve_req) return fail(c, PICKER_EINVAL, "resident validator not started");
-  if (n > kServeMax || nargs > kServeArgs)
-    return fail(c, PICKER_EINVAL, "at most 32 records and 2048 argument slots per request");
-  if (n == 0) return PICKER_OK;
-  ServeRequest* q = c->serve_req;
-  memcpy(q->rec, rec, n * sizeof(picker_rec_t));
-  if (nargs) memcpy(q->args, args, nargs * sizeof(int64_t));
-  q->n = n;
-  q->nargs = nargs;
-  const uint32_t seq = ++c->serve_seq;
-  std::atomic_thread_fence(std::memory_order_seq_cst);  // the body before the sequence number
-  q->seq = seq;
-  const auto t0 = std::chrono::steady_clock::now();
-  uint64_t spins = 0;
-  while (c->serve_resp->seq != seq) {
-    if ((++spins & 1023) == 0 && (uint64_t)std::chrono::duration_cast<std::chrono::microseconds>(
-                                     std::chrono::steady_clock::now() - t0).count() > timeout_us)
-      return fail(c, PICKER_ECUDA, "resident validator did not answer in time");
-  }
-  std::atomic_thread_fence(std::memory_order_seq_cst);  // the codes after the sequence number
-  memcpy(codes_out, (const void*)c->serve_resp->codes, n);
-  return PICKER_OK;
-}
-
-int picker_serve_stop(picker_ctx_t* c) {
-  if (!c) return PICKER_EINVAL;
-  if (!c->serve_req) return PICKER_OK;
-  DevGuard g(c->device);
-  c->serve_req->stop = 1;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  cudaError_t e = cudaStreamSynchronize(c->serve_stream);
-  cudaStreamDestroy(c->serve_stream);
-  cudaFreeHost(c->serve_req);
-  cudaFreeHost(c->serve_resp);
-  c->serve_req = nullptr, c->serve_resp = nullptr, c->serve_stream = nullptr;
-  if (e != cudaSuccess) return cuda_fail(c, e, "resident validator stop");
   return PICKER_OK;
 }
 

@@ -194,24 +194,6 @@ class Picker:
             _stream_handle(stream)))
         return out, cnt
 
-    def serve_start(self):
-        """Start the resident validator (option serve=1 set before load)."""
-        self._check(lib.picker_serve_start(self._h))
-
-    def serve_stop(self):
-        self._check(lib.picker_serve_stop(self._h))
-
-    def serve_validate(self, rec, args, *, timeout_us=1_000_000, out=None):
-        """Validate up to 32 HOST records (numpy REC_DTYPE, arg_off into `args`)
-        through the resident warp; returns their u8 codes (numpy)."""
-        rec = np.ascontiguousarray(rec)
-        args = np.ascontiguousarray(np.asarray(args, dtype=np.int64))
-        codes = out if out is not None else np.empty(len(rec), np.uint8)
-        self._check(lib.picker_serve_validate(
-            self._h, rec.ctypes.data if len(rec) else None, len(rec), args.ctypes.data if len(args) else None,
-            len(args), codes.ctypes.data if len(rec) else None, int(timeout_us)))
-        return codes
-
     def replicate(self, rec, args, ptr_mask, copies, *, first_copy=0, delta=1 << 37, stream=None):
         """K6 (picker_replicate): `copies` relocated copies of a device-resident
         trace, generated on the GPU.  rec: u8[n,32] / numpy records; args:

@@ -84,11 +84,3 @@ def test_contradictory_preconditions_compile(pk):
     # the same kernel alone (no specialised kernel in the module at all)
     r, msg, _ = pk.compile_summaries({"version": 1, "kernels": [k]}, want_source=True)
     assert r == 0, msg
-
-
-def test_resident_validator_compiles(pk, monkeypatch):
-    """The resident validator (k_serve.cuh) instantiates in a module with the
-    specialised shapes (NVRTC for sm_100a, no GPU)."""
-    monkeypatch.setenv("PICKER_COMPILE_SERVE", "1")
-    r, msg, _ = pk.compile_summaries(golden.golden_summary(), want_source=True)
-    assert r > 0 and "k_serve" in msg, msg
