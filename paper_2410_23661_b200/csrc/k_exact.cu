@@ -23,7 +23,9 @@
 //      value = 64-bit byte mask; atomicCAS on the key, atomicOr on the mask) --
 //      then every read point tests its blocks' masks.  The table is sized from
 //      the write points (<= 2 entries per block), so its size is bounded by the
-//      point cap, not by the window: no window limit (reading Q22).  Records
+//      point cap, not by the window: no window limit (reading Q22).  Windows of
+//      up to 256 KB use a bitmap in shared memory instead (one bit per byte, 64-bit
+//      atomicOr per touched block).  Records
 //      whose table exceeds a slice of the small pass go to the big pass, whose
 //      slices hold the largest table the point cap allows.
 #include <cuda_runtime.h>
@@ -41,6 +43,7 @@ namespace picker {
 constexpr uint32_t kPending = 0x100;
 constexpr int kExactThreads = 256;
 constexpr unsigned long long kEmptyKey = ~0ULL;
+constexpr uint64_t kSmemBlocks = 4096;  // shared-memory bitmap: windows up to 256 KB
 
 __device__ __forceinline__ uint64_t sat_mul(uint64_t a, uint64_t b, uint64_t lim) {
   if (a == 0 || b == 0) return 0;
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch
   __shared__ uint64_t s_npts;
   __shared__ int s_on, s_found, s_nv, s_nt;
   __shared__ uint32_t s_claim;
+  __shared__ unsigned long long s_bits[kSmemBlocks];
   unsigned long long* keys = arena + ((uint64_t)blockIdx.x << (slice_log2 + 1));
   unsigned long long* masks = keys + (1ULL << slice_log2);
   const uint32_t npend = L.count[which];
@@ -176,7 +180,14 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch
     const int64_t wlo = win[2 * i], whi = win[2 * i + 1];
     const uint32_t tl = tlog[i];
     const uint64_t tmask = (1ULL << tl) - 1;
-    for (uint64_t e = threadIdx.x; e <= tmask; e += blockDim.x) keys[e] = kEmptyKey, masks[e] = 0;
+    // small windows: a bitmap of the window's 64-byte blocks in shared memory
+    // (one bit per byte); larger ones: the hash table in the CTA's slice
+    const uint64_t wblocks = ((uint64_t)(whi - wlo) >> 6) + 1;
+    const bool in_smem = wblocks <= kSmemBlocks;
+    if (in_smem)
+      for (uint64_t e = threadIdx.x; e < wblocks; e += blockDim.x) s_bits[e] = 0;
+    else
+      for (uint64_t e = threadIdx.x; e <= tmask; e += blockDim.x) keys[e] = kEmptyKey, masks[e] = 0;
     if (threadIdx.x == 0) s_found = 0;
     __syncthreads();
     for (int pass = 0; pass < 2; ++pass) {
@@ -243,6 +254,15 @@ __global__ void __launch_bounds__(kExactThreads) k_exact_enum(Tables T, DevBatch
               const uint32_t s0 = blk == (o0 >> 6) ? (uint32_t)(o0 & 63) : 0;
               const uint32_t s1 = blk == (o1 >> 6) ? (uint32_t)(o1 & 63) : 63;
               const unsigned long long m = (~0ULL >> (63 - s1)) & (~0ULL << s0);
+              if (in_smem) {
+                if (pass == 0) {
+                  atomicOr(s_bits + blk, m);
+                } else if (s_bits[blk] & m) {
+                  atomicExch(&s_found, 1);
+                  break;
+                }
+                continue;
+              }
               uint64_t h = (blk * 0x9E3779B97F4A7C15ULL) >> (64 - tl);
               if (pass == 0) {
                 for (;;) {
