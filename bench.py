@@ -362,8 +362,16 @@ def main():
     from paper_2410_23661_b200 import dist as pdist
 
     rank, world, local = dist_env()
+    # PICKER_BENCH_SHARE_GPU=1 (tests only): every rank on GPU 0 with gloo, to run
+    # the N > 1 code path on a one-GPU box (NCCL needs one GPU per rank)
+    share = os.environ.get("PICKER_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
@@ -513,7 +521,10 @@ def main():
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(args.workload, {}).get("bytes_per_launch")
+            t = json.load(open(tp)).get(args.workload, {})
+            # measured for the default shard only (and the code it was measured on)
+            if t.get("replicas") == WORKLOADS[args.workload][1] and world == 1:
+                traffic = t.get("bytes_per_launch")
         except Exception:
             traffic = None
     cpu = None
