@@ -62,7 +62,7 @@ bool any_jit(const std::vector<IrKernel>& ks) {
 }
 
 bool validate_writes_counts(JitModule* jit, const Options& opt, uint64_t n) {
-  if (n == 0 || opt.stride != jit_is_stride(jit)) return false;  // as launch_validate chooses below
+  if (n == 0 || opt.stride != jit_is_stride(jit) || use_wide_kernel(opt)) return false;  // as launch_validate chooses below
   return jit_small_path(jit, n);
 }
 
@@ -71,6 +71,10 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches) {
   if (n == 0) return cudaSuccess;
+  if (use_wide_kernel(opt)) {  // every evaluating kernel is wide: K2 on its own
+    *launches += 1;
+    return launch_wide(P, b, n, flags, bits, counts, num_sms, s);
+  }
   *launches += jit && opt.stride == jit_is_stride(jit) ? jit_launch_count(jit, n) : 1;
   // stride mode: the specialised module if it was built stride-aware (option
   // set before picker_load_summaries), else the table-driven evaluator

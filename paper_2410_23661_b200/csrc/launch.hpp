@@ -33,6 +33,10 @@ struct Options {
   int sorted = -1, sort_warps = 0, sort_slot = 0;
   int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
   int sort_ws = -1;   // sorted schedule: warp-specialised S4 (1), one warp per group (0), -1 auto
+  // summaries whose evaluating kernels are all wide: the K2 persistent kernel
+  // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
+  int wide_kernel = -1;
+  bool wide_only = false;  // set at load: every kernel is a shortcut or PATH_WIDE
 };
 
 struct JitModule;
@@ -71,6 +75,12 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
                             const DevBatch& b, uint64_t n, uint8_t* flags, uint32_t* bits,
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches);
+
+// K2 persistent kernel (k_wide.cu) and its warps per SM.
+cudaError_t launch_wide(const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags, uint32_t* bits,
+                        unsigned long long* counts, int num_sms, cudaStream_t s);
+int wide_warps_per_sm();
+inline bool use_wide_kernel(const Options& o) { return o.wide_only && o.wide_kernel != 0 && !o.stride; }
 
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
                             uint32_t max_desc, uint8_t* out, int num_sms, cudaStream_t s, std::string& err);

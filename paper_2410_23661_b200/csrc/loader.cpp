@@ -564,6 +564,23 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
         }
       (d.kind == KIND_R ? dk.nr : dk.nw)++;
       t.descs.push_back(dd);
+      // compact form (wide path): guards, > 2 variables or > 2 terms go through dd
+      DWDesc w{};
+      w.kind = dd.kind;
+      w.opaque = dd.opaque;
+      w.base = dd.base;
+      w.width = dd.width;
+      w.inl = dd.nguard == 0 && dd.nvar <= 2 && dd.nterm <= 2;
+      w.vs[0] = w.vs[1] = w.tp[0] = w.tp[1] = w.tv[0] = w.tv[1] = kNone16;
+      if (w.inl) {
+        for (size_t v = 0; v < sid.size(); ++v) w.vs[v] = sid[v];
+        for (uint16_t j = 0; j < 2; ++j) w.tdiv[j] = 1;
+        for (uint16_t j = 0; j < dd.nterm; ++j) {
+          const DTerm& tm = t.terms[dd.term + j];
+          w.tp[j] = tm.prod, w.tv[j] = tm.var, w.tdiv[j] = tm.div;
+        }
+      }
+      t.wdescs.push_back(w);
     }
     for (auto& s : slots) {
       DVar dv{};

@@ -98,7 +98,8 @@ struct HostTables {
   std::vector<uint16_t> varlist;
   std::vector<DVarDef> vardef;
   std::vector<uint8_t> term_lvar;
-  std::vector<KbEntry> kb;       // kernel id -> {bin | bin << 16, 0} (table-driven grouping key)
+  std::vector<DWDesc> wdescs;    // parallel to descs
+  std::vector<KbEntry> kb;      // kernel id -> {bin | bin << 16, 0} (table-driven grouping key)
   uint32_t kb_unknown = 0;
 };
 

@@ -145,6 +145,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sort_slot") c->opt.sort_slot = (int)v;    // tuning: average argument bytes per lane
   else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
   else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
+  else if (k == "wide_kernel") c->opt.wide_kernel = v < 0 ? -1 : (int)(v != 0);  // K2 kernel (k_wide.cu)
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
 }
@@ -175,7 +176,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
          o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
          o_l = append_bytes(blob, ht.varlist),
          o_kb = append_bytes(blob, ht.kb), o_vd = append_bytes(blob, ht.vardef),
-         o_tl = append_bytes(blob, ht.term_lvar);
+         o_tl = append_bytes(blob, ht.term_lvar), o_wd = append_bytes(blob, ht.wdescs);
   blob.resize(blob.size() + 256);
   void* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, blob.size());
@@ -199,7 +200,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   size_t scratch_bytes = 0;
   for (auto& k : ks)
     if (k.path == PATH_WIDE && k.desc.size() > 64) {
-      const int wps = std::max({kCtasPerSm * kWarps, jit_warps_per_sm(jm), (int)(kSmallThreads / 32)});
+      const int wps = std::max({kCtasPerSm * kWarps, jit_warps_per_sm(jm), (int)(kSmallThreads / 32),
+                                wide_warps_per_sm()});
       scratch_bytes = (size_t)c->num_sms * wps * kWideMax * kWideElemBytes;
       break;
     }
@@ -237,6 +239,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.kb_of = (const KbEntry*)(b + o_kb);
   c->P.T.vardef = (const DVarDef*)(b + o_vd);
   c->P.T.term_lvar = (const uint8_t*)(b + o_tl);
+  c->P.T.wdescs = (const DWDesc*)(b + o_wd);
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
   c->P.wide_key = c->P.nbins + 1;  // table-driven grouping (the JIT module uses its own)
@@ -246,6 +249,12 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
     for (auto& k : ks)
       if (k.path != PATH_SHORTCUT) nd += k.desc.size(), ++nc;
     c->bucket_auto = nc && nd > 8 * nc;
+    bool any_wide = false, all_wide = true;
+    for (auto& k : ks) {
+      any_wide |= k.path == PATH_WIDE;
+      all_wide &= k.path == PATH_WIDE || k.path == PATH_SHORTCUT;
+    }
+    c->opt.wide_only = any_wide && all_wide;
   }
   c->ir = std::move(ks);
   c->ht = std::move(ht);

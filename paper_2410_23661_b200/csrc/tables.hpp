@@ -100,6 +100,20 @@ struct DKernel {  // 64 B
 };
 static_assert(sizeof(DKernel) == 64, "DKernel layout");
 
+// One descriptor in two 16-byte loads (the wide path, k_wide.cu): parallel
+// to descs[].  `inl` = 1 when the descriptor has no guard, <= 2 variables and
+// <= 2 terms, which are then inline (variable-slot ids, product ids; a missing
+// term has tp = kNone16); other descriptors are read through DDesc / DTerm.
+struct alignas(16) DWDesc {   // 32 B
+  uint8_t kind, opaque, base, inl;
+  uint16_t vs[2];          // variable slots whose ranges must be non-empty (kNone16: none)
+  uint16_t tp[2], tv[2];   // term i: product id, variable slot (kNone16: constant)
+  uint32_t width;
+  uint32_t tdiv[2];
+  uint32_t pad;
+};
+static_assert(sizeof(DWDesc) == 32, "DWDesc layout");
+
 enum : uint8_t { DEF_OP_NONE = 0, DEF_OP_MOD = 1, DEF_OP_AND = 2 };
 
 // Exact-verifier extras, parallel to varlist[] / terms[] (picker_exact_check).
@@ -124,6 +138,7 @@ struct Tables {
   const uint16_t* varlist;
   const DVarDef* vardef;     // [varlist size]
   const uint8_t* term_lvar;  // [terms size]: term's variable as an index into its descriptor's vars
+  const DWDesc* wdescs;      // [descs size]: compact form of descs[] (the wide path)
 };
 
 // Records [0, n) at rec; argument slots valid at indices [args_lo, args_hi) of args.

@@ -49,8 +49,12 @@ def wide():
     return s, rec, args, np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
 
 
-WIDE_PATHS = [dict(jit=1), dict(jit=1, sorted=0), dict(jit=1, sorted=0, tile=64, threads=32, ctas=1, args_per_rec=8),
-              dict(jit=0, bucket=1), dict(jit=0, bucket=0), dict(jit=0, force_path=3)]
+# wide-only summaries take the K2 persistent kernel (k_wide.cu) by default;
+# wide_kernel=0 routes them through the module's schedules / the table path
+WIDE_PATHS = [dict(jit=1), dict(jit=1, wide_kernel=0), dict(jit=1, wide_kernel=0, sorted=0),
+              dict(jit=1, wide_kernel=0, sorted=0, tile=64, threads=32, ctas=1, args_per_rec=8),
+              dict(jit=0, bucket=1), dict(jit=0, wide_kernel=0, bucket=1), dict(jit=0, wide_kernel=0, bucket=0),
+              dict(jit=0, force_path=3)]
 
 
 @pytest.mark.parametrize("opt", WIDE_PATHS, ids=str)
@@ -65,13 +69,53 @@ def test_wide_family(pk, wide, opt):
         assert set(paths.values()) == {"wide"}, paths
 
 
-def test_wide_small_batches(pk, wide):
-    """The small-batch kernel (n <= 1024) runs K2 records warp-cooperatively
+@pytest.mark.parametrize("opt", [dict(), dict(wide_kernel=0)], ids=str)
+def test_wide_small_batches(pk, wide, opt):
+    """Small batches: the K2 kernel with a partial last chunk, and the
+    small-batch kernel (n <= 1024), which runs K2 records warp-cooperatively
     with its own scratch slices."""
     s, rec, args, want = wide
-    for n in (1, 33, 1024):
-        (flags, bits, counts), _ = _run(pk, s, rec[:n], args)
+    for n in (1, 31, 33, 1024):
+        (flags, bits, counts), _ = _run(pk, s, rec[:n], args, **opt)
         _check(flags, bits, counts, want[:n])
+
+
+@pytest.fixture(scope="module")
+def wide_shuffled():
+    """The wide family with every record's pointer arguments permuted among
+    themselves: extents out of address order (the K2 kernel's chunk sort runs,
+    not only its sortedness test) and many more overlaps."""
+    s, rec, args, meta = workloads.make_wide(n=2000, seed=5)
+    rng = np.random.default_rng(11)
+    args = args.copy()
+    mask = meta["ptr_mask"]
+    for r in rec:
+        o, k = int(r["arg_off"]), int(r["nargs"])
+        idx = o + np.nonzero(mask[o:o + k])[0]
+        if rng.random() < 0.7:
+            args[idx] = args[rng.permutation(idx)]
+    want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
+    return s, rec, args, want
+
+
+@pytest.mark.parametrize("opt", [dict(), dict(wide_kernel=0), dict(jit=0, force_path=3)], ids=str)
+def test_wide_shuffled(pk, wide_shuffled, opt):
+    s, rec, args, want = wide_shuffled
+    assert (want == 0).sum() > 50 and (want == 10).sum() > 50
+    (flags, bits, counts), _ = _run(pk, s, rec, args, **opt)
+    _check(flags, bits, counts, want)
+
+
+def test_wide_kernel_steady_state(pk, wide):
+    """The wide family x 40 (120,000 records: >= 1.5 chunks of 32 records per
+    warp of the K2 kernel's 148 x 16 warps, so warps carry the argument /
+    header pipeline across chunks); expected codes = the base trace's oracle
+    codes tiled (pointer relocation)."""
+    s, rec, args, want = wide
+    _, _, _, meta = workloads.make_wide(n=3000)
+    R, A = workloads.replicate(rec, args, meta["ptr_mask"], 40)
+    (flags, bits, counts), _ = _run(pk, s, R, A)
+    _check(flags, bits, counts, np.tile(want, 40))
 
 
 def _comb_records(seed):
@@ -89,7 +133,7 @@ def _comb_records(seed):
 
 
 @pytest.mark.parametrize("opt", [dict(jit=1), dict(jit=1, wide_pairs=4), dict(jit=0, force_path=3),
-                                 dict(jit=0, bucket=1)], ids=str)
+                                 dict(jit=0, force_path=3, wide_kernel=0), dict(jit=0, bucket=1)], ids=str)
 def test_comb_edges(pk, opt):
     """Touching / overlapping / interleaved teeth: register sort (40
     descriptors, forced wide), the smaller side sorted in the scratch (80,
