@@ -40,7 +40,7 @@
 namespace picker {
 
 constexpr int kWideWarps = 8, kWideCtas = 2;
-constexpr int kWProd = 256, kWVar = 96, kWExt = 320;
+constexpr int kWProd = 192, kWVar = 64, kWExt = 320;
 constexpr int kWArgBuf = 64 + 2048 + 16;  // 8 operand slots + a 16-byte-rounded span of <= 248 slots
 constexpr int64_t kI64Min = (-9223372036854775807LL - 1), kI64Max = 9223372036854775807LL;
 
@@ -49,7 +49,13 @@ struct __align__(16) WideWarpSmem {
   int64_t pv[kWProd];
   int64_t vlo[kWVar], vhi[kWVar];
   Iv64 ext[kWExt];  // reads from the front, writes from the back
-  Iv64 chunk[64];   // one sorted chunk: (lb, prefix max of ub)
+  union {
+    struct {
+      int64_t lo[kWideSigs], hi[kWideSigs];  // summed term offsets per signature
+      uint8_t act[kWideSigs];                // activity per signature
+    } s;
+    Iv64 chunk[64];  // after the descriptors: one sorted chunk (lb, prefix max of ub)
+  } sg;
 };
 static_assert(sizeof(WideWarpSmem) % 16 == 0, "warp workspace alignment");
 constexpr size_t kWideSmem = sizeof(WideWarpSmem) * kWideWarps;
@@ -132,14 +138,14 @@ __device__ __forceinline__ uint8_t eval_wide_ws(const Tables& T, const DKernel& 
                                 int lane) {
   // preconditions and global condition, split over the lanes: the first
   // failing check in order decides (pre before glob)
+  // (no early exit: the loop unrolls and its table loads overlap)
   int first_fail = 0x7FFFFFFF;
-  for (int c = lane; c < K.npre + K.nglob; c += 32) {
+  const int nchk = K.npre + K.nglob;
+#pragma unroll 4
+  for (int c = nchk - 1 - lane; c >= 0; c -= 32) {  // descending: the last failure seen is the first
     const DCheck ch = T.checks[K.check + c];
     const int64_t v = ops[ch.op];
-    if (v < ch.lo || v > ch.hi) {
-      first_fail = c;
-      break;
-    }
+    if (v < ch.lo || v > ch.hi) first_fail = c;
   }
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) first_fail = min(first_fail, __shfl_xor_sync(0xffffffffu, first_fail, d));
@@ -182,35 +188,51 @@ __device__ __forceinline__ uint8_t eval_wide_ws(const Tables& T, const DKernel& 
     lb = add64(lb, min64(x0, x1));
     ub = add64(ub, max64(x0, x1));
   };
+  // signatures (activity + summed term offsets shared by descriptors): lanes over them
+  for (int g = lane; g < K.nsig; g += 32) {
+    const uint4* sp = reinterpret_cast<const uint4*>(T.wsigs + K.desc + g);
+    const uint4 s0 = __ldg(sp), s1 = __ldg(sp + 1);
+    const uint32_t vs0 = s0.x & 0xFFFFu, vs1 = s0.x >> 16;
+    bool on = true;
+    if (vs0 != kNone16) on = W.vlo[vs0] <= W.vhi[vs0];
+    if (vs1 != kNone16) on = on && W.vlo[vs1] <= W.vhi[vs1];
+    int64_t lo = 0, hi = 0;
+    const uint32_t tp0 = s0.y & 0xFFFFu, tp1 = s0.y >> 16, tv0 = s0.z & 0xFFFFu, tv1 = s0.z >> 16;
+    if (tp0 != kNone16) term((uint16_t)tp0, (uint16_t)tv0, s0.w, lo, hi);
+    if (tp1 != kNone16) term((uint16_t)tp1, (uint16_t)tv1, s1.x, lo, hi);
+    W.sg.s.act[g] = on;
+    W.sg.s.lo[g] = lo, W.sg.s.hi[g] = hi;
+  }
+  __syncwarp();
+
   bool act_r = false, act_w = false, opq_r = false, opq_w = false;
   int nr = 0, nw = 0;
   const unsigned lt = (1u << lane) - 1u;
-  // one descriptor per lane and round, its two 16-byte words loaded a round ahead
+  // one descriptor per lane and round (one 16-byte load, issued a round ahead)
   const uint4* wd = reinterpret_cast<const uint4*>(T.wdescs + K.desc);
-  uint4 q0 = make_uint4(0, 0, 0, 0), q1 = q0;
-  if (lane < K.ndesc) q0 = __ldg(wd + 2 * lane), q1 = __ldg(wd + 2 * lane + 1);
+  uint4 q = make_uint4(0, 0, 0, 0);
+  if (lane < K.ndesc) q = __ldg(wd + lane);
   for (int d0 = 0; d0 < K.ndesc; d0 += 32) {
     const int d = d0 + lane;
-    const uint4 w0 = q0, w1 = q1;
-    if (d + 32 < K.ndesc) q0 = __ldg(wd + 2 * (d + 32)), q1 = __ldg(wd + 2 * (d + 32) + 1);
+    const uint4 w = q;
+    if (d + 32 < K.ndesc) q = __ldg(wd + d + 32);
     bool have = false, is_r = false;
     int64_t lb = 0, ub = 0;
     if (d < K.ndesc) {
-      // DWDesc fields: kind, opaque, base, inl | vs0, vs1 | tp0, tp1 | tv0, tv1 ; width, div0, div1
-      const uint32_t kind = w0.x & 0xFFu, opaque = (w0.x >> 8) & 0xFFu, base = (w0.x >> 16) & 0xFFu;
+      // DWDesc: kind, opaque, base, mode | a, b | wm1
+      const uint32_t kind = w.x & 0xFFu, opaque = (w.x >> 8) & 0xFFu, base = (w.x >> 16) & 0xFFu, mode = w.x >> 24;
+      const uint32_t ia = w.y & 0xFFFFu, ib = w.y >> 16;
       bool on = true;
-      if (w0.x >> 24) {  // inline
-        const uint32_t vs0 = w0.y & 0xFFFFu, vs1 = w0.y >> 16;
-        if (vs0 != kNone16) on = W.vlo[vs0] <= W.vhi[vs0];
-        if (vs1 != kNone16) on = on && W.vlo[vs1] <= W.vhi[vs1];
-        if (on && !opaque) {
-          lb = ops[base];  // ops[OPD_NONE] = 0
-          ub = lb;
-          const uint32_t tp0 = w0.z & 0xFFFFu, tp1 = w0.z >> 16, tv0 = w0.w & 0xFFFFu, tv1 = w0.w >> 16;
-          if (tp0 != kNone16) term((uint16_t)tp0, (uint16_t)tv0, w1.y, lb, ub);
-          if (tp1 != kNone16) term((uint16_t)tp1, (uint16_t)tv1, w1.z, lb, ub);
-          ub = add64(ub, (int64_t)w1.x - 1);
-        }
+      if (mode == WD_SIG) {
+        on = W.sg.s.act[ia];
+        const int64_t b0 = ops[base];  // ops[OPD_NONE] = 0
+        lb = add64(b0, W.sg.s.lo[ia]);
+        ub = add64(add64(b0, W.sg.s.hi[ia]), (int64_t)w.z);
+      } else if (mode == WD_CONST) {
+        int64_t c = ops[base];
+        if (ia != kNone16) c = add64(c, W.pv[ia]);
+        if (ib != kNone16) c = add64(c, W.pv[ib]);
+        lb = c, ub = add64(c, (int64_t)w.z);
       } else {  // guards, > 2 variables or > 2 terms: the full tables
         const DDesc D = T.descs[K.desc + d];
         for (int g = 0; g < D.nguard && on; ++g) {
@@ -279,10 +301,10 @@ __device__ __forceinline__ uint8_t eval_wide_ws(const Tables& T, const DKernel& 
     const int64_t m0 = warp_incl_max(e0.ub, lane);
     const int64_t m1 = max64(warp_incl_max(e1.ub, lane), __shfl_sync(0xffffffffu, m0, 31));
     __syncwarp();  // the previous chunk's probes are done
-    W.chunk[lane] = Iv64{e0.lb, m0};
-    W.chunk[32 + lane] = Iv64{e1.lb, m1};
+    W.sg.chunk[lane] = Iv64{e0.lb, m0};
+    W.sg.chunk[32 + lane] = Iv64{e1.lb, m1};
     __syncwarp();
-    if (probe_chunk(W.chunk, L, nl, lane)) return V_NI_OVERLAP;
+    if (probe_chunk(W.sg.chunk, L, nl, lane)) return V_NI_OVERLAP;
   }
   return V_IDEM_CHECKED;
 }
@@ -394,7 +416,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, kWideCtas)
         code = K.shortcut;
       } else if (!launch_limits_rec(r)) {
         code = V_NI_PRECOND;
-      } else if (K.ndesc > kWExt || K.nprod > kWProd || K.nvar > kWVar) {
+      } else if (K.ndesc > kWExt || K.nprod > kWProd || K.nvar > kWVar || K.nsig > kWideSigs) {
         code = wide_fallback(T, r, B.args + r.arg_off, B.args_lo, B.args_hi, lane, wide_scratch(P, warp));
       } else {
         // operand slots 0..7: launch dimensions, 1, 0; i32 parameters sign-extended

@@ -527,6 +527,7 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
     };
     dk.desc = (uint32_t)t.descs.size();
     dk.ndesc = (uint16_t)k.desc.size();
+    std::vector<DWSig> sigs;  // wide-path signatures of this kernel (<= ndesc)
     for (auto& d : k.desc) {
       DDesc dd{};
       dd.kind = d.kind;
@@ -564,24 +565,38 @@ void flatten(const std::vector<IrKernel>& ks, HostTables& t) {
         }
       (d.kind == KIND_R ? dk.nr : dk.nw)++;
       t.descs.push_back(dd);
-      // compact form (wide path): guards, > 2 variables or > 2 terms go through dd
+      // compact form (wide path, tables.hpp): signature, constant or full
       DWDesc w{};
       w.kind = dd.kind;
       w.opaque = dd.opaque;
       w.base = dd.base;
-      w.width = dd.width;
-      w.inl = dd.nguard == 0 && dd.nvar <= 2 && dd.nterm <= 2;
-      w.vs[0] = w.vs[1] = w.tp[0] = w.tp[1] = w.tv[0] = w.tv[1] = kNone16;
-      if (w.inl) {
-        for (size_t v = 0; v < sid.size(); ++v) w.vs[v] = sid[v];
-        for (uint16_t j = 0; j < 2; ++j) w.tdiv[j] = 1;
+      w.wm1 = dd.width - 1;
+      w.a = w.b = kNone16;
+      w.mode = WD_FULL;
+      if (dd.nguard == 0 && dd.nvar <= 2 && dd.nterm <= 2) {
+        DWSig sg{};
+        sg.vs[0] = sg.vs[1] = sg.tp[0] = sg.tp[1] = sg.tv[0] = sg.tv[1] = kNone16;
+        sg.tdiv[0] = sg.tdiv[1] = 1;
+        for (size_t v = 0; v < sid.size(); ++v) sg.vs[v] = sid[v];
+        bool any_var = !sid.empty();
         for (uint16_t j = 0; j < dd.nterm; ++j) {
           const DTerm& tm = t.terms[dd.term + j];
-          w.tp[j] = tm.prod, w.tv[j] = tm.var, w.tdiv[j] = tm.div;
+          sg.tp[j] = tm.prod, sg.tv[j] = tm.var, sg.tdiv[j] = tm.div;
+          any_var |= tm.var != kNone16;
+        }
+        if (!any_var) {
+          w.mode = WD_CONST, w.a = sg.tp[0], w.b = sg.tp[1];
+        } else {
+          size_t s = 0;
+          while (s < sigs.size() && memcmp(&sigs[s], &sg, sizeof(DWSig)) != 0) ++s;
+          if (s == sigs.size() && s < (size_t)kWideSigs) sigs.push_back(sg);
+          if (s < sigs.size()) w.mode = WD_SIG, w.a = (uint16_t)s;
         }
       }
       t.wdescs.push_back(w);
     }
+    dk.nsig = (uint16_t)sigs.size();
+    for (size_t i = 0; i < k.desc.size(); ++i) t.wsigs.push_back(i < sigs.size() ? sigs[i] : DWSig{});
     for (auto& s : slots) {
       DVar dv{};
       dv.skind = s.skind;

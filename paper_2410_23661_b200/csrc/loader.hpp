@@ -99,6 +99,7 @@ struct HostTables {
   std::vector<DVarDef> vardef;
   std::vector<uint8_t> term_lvar;
   std::vector<DWDesc> wdescs;    // parallel to descs
+  std::vector<DWSig> wsigs;      // parallel to descs (first nsig of each kernel used)
   std::vector<KbEntry> kb;      // kernel id -> {bin | bin << 16, 0} (table-driven grouping key)
   uint32_t kb_unknown = 0;
 };

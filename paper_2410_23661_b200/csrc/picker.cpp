@@ -176,7 +176,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
          o_g = append_bytes(blob, ht.guards), o_d = append_bytes(blob, ht.descs),
          o_l = append_bytes(blob, ht.varlist),
          o_kb = append_bytes(blob, ht.kb), o_vd = append_bytes(blob, ht.vardef),
-         o_tl = append_bytes(blob, ht.term_lvar), o_wd = append_bytes(blob, ht.wdescs);
+         o_tl = append_bytes(blob, ht.term_lvar), o_wd = append_bytes(blob, ht.wdescs),
+         o_ws = append_bytes(blob, ht.wsigs);
   blob.resize(blob.size() + 256);
   void* dev = nullptr;
   cudaError_t e = cudaMalloc(&dev, blob.size());
@@ -240,6 +241,7 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.T.vardef = (const DVarDef*)(b + o_vd);
   c->P.T.term_lvar = (const uint8_t*)(b + o_tl);
   c->P.T.wdescs = (const DWDesc*)(b + o_wd);
+  c->P.T.wsigs = (const DWSig*)(b + o_ws);
   c->P.kb_unknown = ht.kb_unknown;
   c->P.nbins = (uint32_t)ks.size();
   c->P.wide_key = c->P.nbins + 1;  // table-driven grouping (the JIT module uses its own)

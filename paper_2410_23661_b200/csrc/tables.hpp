@@ -93,26 +93,37 @@ struct DKernel {  // 64 B
   uint32_t check;
   uint16_t nprod, nvar;
   uint32_t prod, var;     // prods[prod..], vars[var..]
-  uint16_t ndesc, nr, nw, pad1;
+  uint16_t ndesc, nr, nw, nsig;  // nsig: wide-path signatures (DWSig)
   uint32_t desc;
   uint32_t jit_slot;      // index of the specialised function (PATH_JIT)
   uint32_t i32mask[6];    // bit i: param i is i32 (sign-extend the low 32 bits); params < 192
 };
 static_assert(sizeof(DKernel) == 64, "DKernel layout");
 
-// One descriptor in two 16-byte loads (the wide path, k_wide.cu): parallel
-// to descs[].  `inl` = 1 when the descriptor has no guard, <= 2 variables and
-// <= 2 terms, which are then inline (variable-slot ids, product ids; a missing
-// term has tp = kNone16); other descriptors are read through DDesc / DTerm.
-struct alignas(16) DWDesc {   // 32 B
-  uint8_t kind, opaque, base, inl;
-  uint16_t vs[2];          // variable slots whose ranges must be non-empty (kNone16: none)
-  uint16_t tp[2], tv[2];   // term i: product id, variable slot (kNone16: constant)
-  uint32_t width;
-  uint32_t tdiv[2];
+// The wide path (k_wide.cu) reads each descriptor in one 16-byte load.  A
+// descriptor without guards, with <= 2 variables and <= 2 terms is
+//   mode WD_SIG:   base + the offsets of a *signature* -- its activity slots
+//                  and terms, shared by every descriptor of the kernel with the
+//                  same ones (a multi-tensor kernel's T tensors of one size
+//                  share one), evaluated once per record;
+//   mode WD_CONST: no variable: base + P[a] (+ P[b]), always active;
+// any other descriptor (WD_FULL) is read through DDesc / DTerm.
+enum : uint8_t { WD_SIG = 0, WD_CONST = 1, WD_FULL = 2 };
+constexpr int kWideSigs = 128;  // signatures per kernel (more: WD_FULL)
+struct alignas(16) DWDesc {  // 16 B, parallel to descs[]
+  uint8_t kind, opaque, base, mode;
+  uint16_t a, b;             // WD_SIG: a = signature; WD_CONST: product ids (kNone16: absent)
+  uint32_t wm1;              // width - 1
   uint32_t pad;
 };
-static_assert(sizeof(DWDesc) == 32, "DWDesc layout");
+static_assert(sizeof(DWDesc) == 16, "DWDesc layout");
+struct alignas(16) DWSig {   // 32 B; the kernel's signatures are at wsigs[K.desc ..)
+  uint16_t vs[2];            // variable slots whose ranges must be non-empty (kNone16: none)
+  uint16_t tp[2], tv[2];     // term i: product id (kNone16: absent), variable slot (kNone16: constant)
+  uint32_t tdiv[2];
+  uint32_t pad[3];
+};
+static_assert(sizeof(DWSig) == 32, "DWSig layout");
 
 enum : uint8_t { DEF_OP_NONE = 0, DEF_OP_MOD = 1, DEF_OP_AND = 2 };
 
@@ -139,6 +150,7 @@ struct Tables {
   const DVarDef* vardef;     // [varlist size]
   const uint8_t* term_lvar;  // [terms size]: term's variable as an index into its descriptor's vars
   const DWDesc* wdescs;      // [descs size]: compact form of descs[] (the wide path)
+  const DWSig* wsigs;        // [descs size]: kernel k's signatures at [k.desc, k.desc + k.nsig)
 };
 
 // Records [0, n) at rec; argument slots valid at indices [args_lo, args_hi) of args.
