@@ -125,6 +125,31 @@ __device__ __forceinline__ bool launch_limits_rec(const picker_rec_t& r) {
 
 __device__ __forceinline__ int count_bin(uint8_t code) { return code <= 11 ? code : 15; }
 
+// The CTA's histogram s_hist (final; every thread of the CTA calls this) into
+// the caller's counts.  slot == nullptr: atomic adds into counts (the caller
+// zeroed them).  Otherwise the CTAs add into the launch's slot and the last
+// CTA to finish (ticket) writes counts and leaves the slot zeroed for its
+// next launch: no memset launch before the kernel.
+__device__ __forceinline__ void flush_counts(const uint32_t* s_hist, unsigned long long* counts, CountSlot* slot) {
+  const int tid = threadIdx.x;
+  if (counts == nullptr) return;
+  if (slot == nullptr) {
+    if (tid < PICKER_NUM_COUNTS && s_hist[tid]) atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+    return;
+  }
+  __shared__ uint32_t s_last;
+  if (tid < PICKER_NUM_COUNTS && s_hist[tid]) atomicAdd(&slot->acc[tid], (unsigned long long)s_hist[tid]);
+  __threadfence();
+  __syncthreads();
+  if (tid == 0) s_last = atomicAdd(&slot->ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last) {
+    __threadfence();
+    if (tid < PICKER_NUM_COUNTS) counts[tid] = atomicExch(&slot->acc[tid], 0ull);
+    if (tid == 0) atomicExch(&slot->ticket, 0u);
+  }
+}
+
 // Epilogue: u8 code, ballot-packed idempotent bit, histogram.
 // Lane 0 of each warp must hold a record index that is a multiple of 32.
 __device__ __forceinline__ void emit(uint64_t i, bool valid, uint8_t code, uint8_t* flags,

@@ -61,16 +61,19 @@ bool any_jit(const std::vector<IrKernel>& ks) {
   return false;
 }
 
-bool validate_writes_counts(JitModule* jit, const Options& opt, uint64_t n) {
-  if (n == 0 || opt.stride != jit_is_stride(jit) || use_wide_kernel(opt)) return false;  // as launch_validate chooses below
-  return jit_small_path(jit, n);
-}
-
-cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options& opt,
+cudaError_t launch_validate(const BucketParams& P0, JitModule* jit, const Options& opt,
                             const DevBatch& b, uint64_t n, uint8_t* flags, uint32_t* bits,
                             unsigned long long* counts, int num_sms, cudaStream_t s,
                             int* launches) {
   if (n == 0) return cudaSuccess;
+  BucketParams P = P0;
+  // P.count_slot set: the launch writes counts (flush_counts).  The paths
+  // whose kernels only accumulate get the counts zeroed here instead.
+  auto accumulate = [&]() -> cudaError_t {
+    if (!counts || !P.count_slot) return cudaSuccess;
+    P.count_slot = nullptr;
+    return cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
+  };
   if (use_wide_kernel(opt)) {  // every evaluating kernel is wide: K2 on its own
     *launches += 1;
     return launch_wide(P, b, n, flags, bits, counts, num_sms, s);
@@ -78,12 +81,16 @@ cudaError_t launch_validate(const BucketParams& P, JitModule* jit, const Options
   *launches += jit && opt.stride == jit_is_stride(jit) ? jit_launch_count(jit, n) : 1;
   // stride mode: the specialised module if it was built stride-aware (option
   // set before picker_load_summaries), else the table-driven evaluator
-  if (opt.stride && !jit_is_stride(jit)) return launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);
+  if (opt.stride && !jit_is_stride(jit)) {
+    cudaError_t e = accumulate();
+    return e != cudaSuccess ? e : launch_stride(P, b, n, flags, bits, counts, opt.bucket, num_sms, s);
+  }
   if (!opt.stride && jit_is_stride(jit)) jit = nullptr;  // stride-aware module, plain verdicts wanted
   if (jit) return launch_jit(jit, P, b, n, flags, bits, counts, num_sms, s);
   if (opt.bucket && bucket_smem_bytes(P.nbins + 2) <= kMaxSmem)
     return launch_bucket_generic(P, b, n, flags, bits, counts, num_sms, s);
-  return launch_generic(P.T, b, n, flags, bits, counts, num_sms, s);
+  cudaError_t e = accumulate();
+  return e != cudaSuccess ? e : launch_generic(P.T, b, n, flags, bits, counts, num_sms, s);
 }
 
 }  // namespace picker

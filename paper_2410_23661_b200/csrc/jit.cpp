@@ -128,7 +128,8 @@ struct Gen {
 // class has at least kLoopMin members: many-pointer kernels (C4) otherwise
 // emit one straight-line block per descriptor, and a shape of ~4,000 SASS
 // instructions does not fit the 32 KB instruction cache.
-constexpr size_t kLoopMin = 3, kLoopKernelMin = 12;  // class size; streamed descriptors of the kernel
+constexpr size_t kLoopMin = 3;  // class size
+size_t g_loop_kernel_min = 6;  // streamed descriptors of the kernel (Options.loop_min, set by jit_plan)
 uint64_t fnv1a(const std::string& s);
 
 std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs) {
@@ -374,7 +375,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
   size_t nstreamed = 0;
   for (auto& e : cls) nstreamed += e.second.size();
   for (auto& e : cls)
-    if (e.second.size() >= kLoopMin && nstreamed >= kLoopKernelMin) {
+    if (e.second.size() >= kLoopMin && nstreamed >= g_loop_kernel_min) {
       any_loop = true;
       for (int di : e.second) in_loop[di] = 1;
     }
@@ -553,7 +554,8 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws, int loop_min) {
+  g_loop_kernel_min = (size_t)std::max(1, loop_min);
   JitPlan P;
   std::ostringstream src;
   // paths no kernel of this summary takes are left out of the module (code size)
@@ -812,7 +814,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
@@ -949,7 +951,9 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     S.nblk = (uint32_t)std::min<uint64_t>({(n + 4095) / 4096, (uint64_t)num_sms * 4, (uint64_t)kSortMaxBlk});
     S.chunk = (uint32_t)(((n + S.nblk - 1) / S.nblk + 31) & ~31ULL);
     const uint32_t max_blk = kSortMaxBlk;
+    bool fresh = false;
     if (m->sort_cap < n) {  // keys, permutation, (key, block) counts, per-key tables
+      fresh = true;
       if (m->sort_buf) cudaFree(m->sort_buf);
       m->sort_buf = nullptr;
       m->sort_cap = 0;
@@ -965,7 +969,9 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     S.hist = (uint32_t*)(b + cap * 5);
     S.meta = S.hist + (size_t)kSortKeys * max_blk;
     void* a1[] = {(void*)&P, (void*)&B, (void*)&n, (void*)&S, (void*)&flags};
-    cudaError_t e = cudaMemsetAsync(S.meta, 0, kMetaWords * 4, s);  // key totals, claim counter
+    // key totals, claim counter, S5 ticket: zeroed once here, then by the last
+    // CTA of each call's S5 (k_sort_emit)
+    cudaError_t e = fresh ? cudaMemsetAsync(S.meta, 0, kMetaWords * 4, s) : cudaSuccess;
     if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[0], dim3(S.nblk), dim3(kSortBlock), a1, 0, s);
     void* a3[] = {(void*)&n, (void*)&S};
     if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[2], dim3(S.nblk), dim3(kSortBlock), a3, 0, s);
@@ -978,7 +984,8 @@ cudaError_t launch_jit(JitModule* m, const BucketParams& P0, const DevBatch& B, 
     const uint64_t words = (n + 31) / 32;
     const unsigned eb = (unsigned)std::min<uint64_t>((words + 255) / 256, (uint64_t)num_sms * 8);
     const uint8_t* cf = flags;
-    void* a5[] = {(void*)&cf, (void*)&n, (void*)&bits, (void*)&counts};
+    CountSlot* slot = P.count_slot;
+    void* a5[] = {(void*)&cf, (void*)&n, (void*)&bits, (void*)&counts, (void*)&slot, (void*)&S.meta};
     if (e == cudaSuccess) e = cudaLaunchKernel((const void*)m->sk[4], dim3(eb), dim3(256), a5, 0, s);
     return e;
   }

@@ -392,8 +392,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
     __syncthreads();  // s_code and the per-key arrays are reused by the next tile
   }
-  if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid])
-    atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+  flush_counts(s_hist, counts, P.count_slot);
 }
 
 // Pipelined bucketed kernel for at most kPipeKeys grouping keys (the
@@ -658,8 +657,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     }
   }
   __syncthreads();
-  if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid])
-    atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+  flush_counts(s_hist, counts, P.count_slot);
 }
 
 // Small batches (n <= kSmallMax, one CTA): one thread per record straight from

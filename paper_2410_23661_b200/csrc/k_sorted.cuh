@@ -387,7 +387,8 @@ __global__ void __launch_bounds__(kSortThreads, 1)
 
 // S5: one thread per 32 records: the idempotent bit word and the histogram.
 __global__ void __launch_bounds__(256) k_sort_emit(const uint8_t* __restrict__ flags, uint64_t n,
-                                                   uint32_t* __restrict__ bits, unsigned long long* __restrict__ counts) {
+                                                   uint32_t* __restrict__ bits, unsigned long long* __restrict__ counts,
+                                                   CountSlot* slot, uint32_t* meta) {
   __shared__ uint32_t s_hist[PICKER_NUM_COUNTS];
   if (threadIdx.x < PICKER_NUM_COUNTS) s_hist[threadIdx.x] = 0;
   __syncthreads();
@@ -412,8 +413,15 @@ __global__ void __launch_bounds__(256) k_sort_emit(const uint8_t* __restrict__ f
       if (h[x]) atomicAdd(s_hist + x, h[x]);
   }
   __syncthreads();
-  if (counts && threadIdx.x < PICKER_NUM_COUNTS && s_hist[threadIdx.x])
-    atomicAdd(counts + threadIdx.x, (unsigned long long)s_hist[threadIdx.x]);
+  flush_counts(s_hist, counts, slot);
+  // the last CTA clears the key totals and claim counter for the next call
+  // (S1-S4 are done: they precede S5 on the stream)
+  __shared__ uint32_t s_last;
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(meta + kMetaTicket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (s_last)
+    for (uint32_t w = threadIdx.x; w < kMetaWords; w += blockDim.x) meta[w] = 0;
 }
 
 }  // namespace picker

@@ -462,7 +462,7 @@ __global__ void __launch_bounds__(kWideWarps * 32, kWideCtas)
   }
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
-  if (counts && tid < PICKER_NUM_COUNTS && s_hist[tid]) atomicAdd(counts + tid, (unsigned long long)s_hist[tid]);
+  flush_counts(s_hist, counts, P.count_slot);
 }
 
 cudaError_t launch_wide(const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags, uint32_t* bits,

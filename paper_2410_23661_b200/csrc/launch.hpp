@@ -36,6 +36,8 @@ struct Options {
   // summaries whose evaluating kernels are all wide: the K2 persistent kernel
   // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
   int wide_kernel = -1;
+  int loop_min = 6;  // specialised module: loop classes in kernels with >= loop_min streamed descriptors
+                     // (measured: C2-heavy 0.186 -> 0.210 of the HBM peak at 6 instead of 12, C2 unchanged)
   bool wide_only = false;  // set at load: every kernel is a shortcut or PATH_WIDE
 };
 
@@ -54,7 +56,8 @@ struct JitPlan {
   std::vector<uint16_t> key_of;  // [kernels + 1]: grouping key (= shape) of each bin
   int nshapes = 0;
 };
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false);
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false,
+                 int loop_min = 6);
 bool jit_is_stride(const JitModule* m);
 // Kernel launches one picker_validate_batch of n records makes on the module.
 int jit_launch_count(const JitModule* m, uint64_t n);
@@ -62,8 +65,6 @@ int jit_launch_count(const JitModule* m, uint64_t n);
 int jit_warps_per_sm(const JitModule* m);
 // The module has the small-batch kernel and n <= kSmallMax (one CTA, counts written).
 bool jit_small_path(const JitModule* m, uint64_t n);
-// launch_validate will take the small-batch kernel (it writes the counts: no memset).
-bool validate_writes_counts(JitModule* jit, const Options& opt, uint64_t n);
 // Fills in the automatic geometry (tile = 0) from the summaries.
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
 // Stable-sort kernels by generated shape so neighbouring bins share code.

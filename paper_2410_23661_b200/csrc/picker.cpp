@@ -29,6 +29,8 @@ struct picker_ctx {
   void* stage[2] = {nullptr, nullptr};
   size_t stage_bytes[2] = {0, 0};
   unsigned long long* dev_counts = nullptr;
+  CountSlot* count_slots = nullptr;  // kCountSlots histogram slots (flush_counts), zeroed at allocation
+  uint32_t count_seq = 0;            // next slot
   cudaStream_t aux = nullptr;
   void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
   size_t wide_scratch_bytes = 0;
@@ -113,6 +115,7 @@ void picker_destroy(picker_ctx_t* c) {
   {
     DevGuard g(c->device);
     if (c->dev_tables) cudaFree(c->dev_tables);
+    if (c->count_slots) cudaFree(c->count_slots);
     for (int i = 0; i < 2; ++i)
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
@@ -145,6 +148,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sort_slot") c->opt.sort_slot = (int)v;    // tuning: average argument bytes per lane
   else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
   else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
+  else if (k == "loop_min") c->opt.loop_min = (int)v;  // tuning: loop classes of the specialised module
   else if (k == "wide_kernel") c->opt.wide_kernel = v < 0 ? -1 : (int)(v != 0);  // K2 kernel (k_wide.cu)
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
@@ -307,7 +311,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     select_paths(ks, opt);
     order_by_shape(ks);
     Options geo = resolve_geometry(ks, opt);
-    JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0);
+    JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0, geo.loop_min);
     geo.pipe_keys = 3 + plan.nshapes + 1;  // SHAPE_FIRST + shapes + the shortcut key
     std::string cubin, lowered, err;
     if (!jit_compile(plan, geo, cubin, lowered, false, err)) {
@@ -360,12 +364,24 @@ int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, 
   c->last_launches = 0;
   Options o = c->opt;
   if (o.bucket < 0) o.bucket = c->bucket_auto;
-  if (counts && !validate_writes_counts(c->jit, o, n)) {  // the kernels accumulate
+  // counts are written by the launch itself (the last CTA through a histogram
+  // slot, or the small-batch kernel); launch_validate zeroes them first only
+  // on the paths without slots
+  BucketParams P = c->P;
+  if (counts && n) {
+    if (!c->count_slots) {
+      cudaError_t e = cudaMalloc(&c->count_slots, kCountSlots * sizeof(CountSlot));
+      if (e != cudaSuccess) return fail(c, PICKER_ENOMEM, "cudaMalloc(count slots)");
+      e = cudaMemset(c->count_slots, 0, kCountSlots * sizeof(CountSlot));
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset(count slots)");
+    }
+    P.count_slot = c->count_slots + (c->count_seq++ % kCountSlots);
+  } else if (counts) {  // n == 0: nothing launches
     cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
     if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
   }
   DevBatch db{b->rec, b->args, 0, b->args_len};
-  cudaError_t e = launch_validate(c->P, c->jit, o, db, n, flags, bits,
+  cudaError_t e = launch_validate(P, c->jit, o, db, n, flags, bits,
                                   (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
   if (e != cudaSuccess) return cuda_fail(c, e, "validate launch");
   return PICKER_OK;

@@ -177,6 +177,15 @@ struct KbEntry {
 };
 constexpr uint32_t kDirectArity = 0x100u;
 
+// Per-launch histogram accumulator (device_common.cuh flush_counts); the
+// context owns a ring of kCountSlots, zeroed once, each left zeroed by the
+// last CTA of the launch that used it.
+struct CountSlot {
+  unsigned long long acc[PICKER_NUM_COUNTS];
+  unsigned int ticket, pad[3];
+};
+constexpr int kCountSlots = 64;
+
 // Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
 struct BucketParams {
   Tables T;
@@ -189,6 +198,7 @@ struct BucketParams {
   uint32_t wide_key;           // grouping key of the wide (K2) kernels; 0xFFFFFFFF: none
   uint32_t direct_key;         // key whose code is final in the key pass (KbEntry.kn = direct
                                // code, see direct_code); 0xFFFFFFFF: none
+  CountSlot* count_slot;       // this launch's histogram slot (flush_counts); nullptr: accumulate
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads
@@ -267,7 +277,8 @@ struct SortScratch {
   uint32_t nblk;   // blocks of S1 / S3
   uint32_t chunk;  // records per block (a multiple of 32)
 };
-constexpr uint32_t kMetaTot = 0, kMetaClaim = kSortKeys, kMetaWords = kSortKeys + 16;  // key totals, claim counter
+constexpr uint32_t kMetaTot = 0, kMetaClaim = kSortKeys, kMetaTicket = kSortKeys + 1,
+                   kMetaWords = kSortKeys + 16;  // key totals, claim counter, S5's ticket
 
 // Generic-path limits (a kernel beyond them uses the wide path).
 constexpr int kGenMaxDesc = 64;  // per kind
