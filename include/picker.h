@@ -154,7 +154,11 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
  *                            idempotent (code 0 or 1); NULL to skip;
  *   counts_out[16]          per-code histogram (overwritten, not
  *                            accumulated); NULL to skip.
- * Bad records are not call errors: they get codes 0xFE / 0xFF.               */
+ * Bad records are not call errors: they get codes 0xFE / 0xFF.
+ * The launch writes counts_out itself (no memset launch): its CTAs add into
+ * one of the context's 64 histogram slots, the last CTA copies it out and
+ * clears it.  So at most 64 calls of one context may be in flight at once
+ * (on any streams); more need more contexts.                                 */
 int picker_validate_batch(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                           uint8_t* flags_out, uint32_t* idem_bits_out,
                           uint64_t* counts_out, void* stream);
