@@ -806,6 +806,16 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
   return opt;
 }
 
+// After planning: few-argument summaries with more than 64 grouping keys (the
+// 128-key module; C2-heavy: 70) get one CTA of 28 warps per SM on 1792-record
+// tiles: twice the records per key per tile fill the warps' groups, and the
+// tile's barrier tail is spread over twice the work (C2-heavy 0.211 -> 0.273 of
+// the HBM peak; C2 with 34 keys and C3 are faster on 2 x 896: r02_ab_log).
+void geometry_for_keys(Options& opt, bool auto_tile, uint32_t keys) {
+  if (!auto_tile || opt.sorted > 0 || keys <= 64 || opt.tile != 896) return;
+  opt.tile = 1792, opt.threads = 896, opt.ctas = 1, opt.args_per_rec = 6, opt.arg_bufs = 1;
+}
+
 JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std::string& err) {
   Options opt = resolve_geometry(ks, opt_in);
   if (opt.tile < 32 || opt.tile % 32 || opt.tile > 8192 || opt.threads < 32 || opt.threads % 32 ||
@@ -816,6 +826,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   }
   JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
+  geometry_for_keys(opt, opt_in.tile == 0, (uint32_t)opt.pipe_keys);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
     err = "tile must be a multiple of threads";
     return nullptr;

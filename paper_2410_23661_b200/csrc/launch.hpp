@@ -67,6 +67,8 @@ int jit_warps_per_sm(const JitModule* m);
 bool jit_small_path(const JitModule* m, uint64_t n);
 // Fills in the automatic geometry (tile = 0) from the summaries.
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
+// ... and adjusts it once the module's grouping-key count is known.
+void geometry_for_keys(Options& opt, bool auto_tile, uint32_t keys);
 // Stable-sort kernels by generated shape so neighbouring bins share code.
 void order_by_shape(std::vector<IrKernel>& ks);
 bool jit_compile(const JitPlan& plan, const Options& opt, std::string& cubin, std::string& lowered,

@@ -313,6 +313,7 @@ int picker_compile_summaries(const char* text, size_t len, char* msg, size_t msg
     Options geo = resolve_geometry(ks, opt);
     JitPlan plan = jit_plan(ks, false, geo.sorted > 0, geo.sort_ws > 0, geo.loop_min);
     geo.pipe_keys = 3 + plan.nshapes + 1;  // SHAPE_FIRST + shapes + the shortcut key
+    geometry_for_keys(geo, opt.tile == 0, (uint32_t)geo.pipe_keys);
     std::string cubin, lowered, err;
     if (!jit_compile(plan, geo, cubin, lowered, false, err)) {
       put(msg, msg_len, err);

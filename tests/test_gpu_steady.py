@@ -199,10 +199,14 @@ def test_device_replication(pk, c2):
 
 def test_c2heavy_128_keys(pk):
     """C2-heavy has 66 shapes: the pipelined kernel with 128 grouping keys (4
-    per lane in the scan), every record against the oracle, many tiles per CTA."""
+    per lane in the scan), every record against the oracle, many tiles per CTA:
+    the auto geometry for > 64 keys (1792-record tiles, one CTA of 896 threads
+    per SM; x80 = 5.5 tiles per CTA) and the few-key geometry (2 x 448 on 896)."""
     s, rec, args, meta = workloads.make_c2(heavy=True)
     want = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
-    for R, opt in [(1, dict(jit=1)), (40, dict(jit=1)), (4, dict(jit=1, tile=64, threads=32, ctas=1, args_per_rec=8))]:
+    for R, opt in [(1, dict(jit=1)), (80, dict(jit=1)),
+                   (40, dict(jit=1, tile=896, threads=448, ctas=2, args_per_rec=5, arg_bufs=1)),
+                   (4, dict(jit=1, tile=64, threads=32, ctas=1, args_per_rec=8))]:
         rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
         flags, bits, counts = _run(pk, s, rec_t, args_t, **opt)
         _check(flags, bits, counts, np.tile(want, R))
