@@ -147,11 +147,17 @@ __global__ void __launch_bounds__(kModelThreads) k_models(Tables T, DevBatch B, 
 
 cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const uint8_t* codes,
                           const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,
-                          int num_sms, cudaStream_t s) {
-  ModelAcc* acc = nullptr;
-  cudaError_t e = cudaMallocAsync(&acc, sizeof(ModelAcc), s);
-  if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(acc, 0, sizeof(ModelAcc), s);
+                          void** acc_buf, int num_sms, cudaStream_t s) {
+  // the accumulator is owned by the caller's context (allocated once)
+  if (!*acc_buf) {
+    cudaError_t e = cudaMalloc(acc_buf, sizeof(ModelAcc));
+    if (e != cudaSuccess) {
+      *acc_buf = nullptr;
+      return e;
+    }
+  }
+  ModelAcc* acc = (ModelAcc*)*acc_buf;
+  cudaError_t e = cudaMemsetAsync(acc, 0, sizeof(ModelAcc), s);
   if (e == cudaSuccess && n) {
     const uint64_t blocks = std::min<uint64_t>((n + kModelThreads - 1) / kModelThreads, (uint64_t)num_sms * 3);
     k_models<<<(unsigned)blocks, kModelThreads, 0, s>>>(T, b, n, codes, ctx_bytes, kill_ns, save_bpu, acc);
@@ -160,7 +166,6 @@ cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const 
   ModelAcc h;
   if (e == cudaSuccess) e = cudaMemcpyAsync(&h, acc, sizeof(ModelAcc), cudaMemcpyDeviceToHost, s);
   if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  cudaFreeAsync(acc, s);
   if (e != cudaSuccess) return e;
   out->n = n;
   out->n_idem = h.n_idem;

@@ -231,7 +231,8 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch 
 }
 
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
-                            uint32_t max_desc, uint8_t* out, int num_sms, cudaStream_t s, std::string& err) {
+                            uint32_t max_desc, uint8_t* out, void** scratch_buf, size_t* scratch_bytes, int num_sms,
+                            cudaStream_t s, std::string& err) {
   if (n == 0) return cudaSuccess;
   // extents per window <= window x max descriptors per kernel
   const uint32_t cap = std::max<uint32_t>(32, window * std::max<uint32_t>(max_desc, 1));
@@ -242,16 +243,23 @@ cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint
   const uint32_t threads = std::min<uint32_t>(kSeqThreads, (window + 31) / 32 * 32);
   uint64_t grid = std::min<uint64_t>(nwin, (uint64_t)num_sms * (2048 / threads));
   grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (1ULL << 30) / slice));
-  uint8_t* scratch = nullptr;
-  cudaError_t e = cudaMallocAsync(&scratch, grid * slice, s);
-  if (e != cudaSuccess) {
-    err = "scratch allocation";
-    return e;
+  // the slices are owned by the caller's context, grown on demand (a per-call
+  // stream-ordered allocation made the timing depend on the pool's state)
+  if (*scratch_bytes < grid * slice) {
+    cudaError_t e = cudaStreamSynchronize(s);  // a previous call may still use the old buffer
+    if (e == cudaSuccess && *scratch_buf) e = cudaFree(*scratch_buf);
+    *scratch_buf = nullptr;
+    *scratch_bytes = 0;
+    if (e == cudaSuccess) e = cudaMalloc(scratch_buf, grid * slice);
+    if (e != cudaSuccess) {
+      *scratch_buf = nullptr;
+      err = "scratch allocation";
+      return e;
+    }
+    *scratch_bytes = grid * slice;
   }
-  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, scratch, slice, cap, out);
-  e = cudaGetLastError();
-  cudaFreeAsync(scratch, s);
-  return e;
+  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap, out);
+  return cudaGetLastError();
 }
 
 }  // namespace picker

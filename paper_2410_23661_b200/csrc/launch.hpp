@@ -85,12 +85,15 @@ cudaError_t launch_wide(const BucketParams& P, const DevBatch& B, uint64_t n, ui
 int wide_warps_per_sm();
 inline bool use_wide_kernel(const Options& o) { return o.wide_only && o.wide_kernel != 0 && !o.stride; }
 
+// `scratch` / `scratch_bytes` (f1 window slices) and `acc` (f3 accumulator):
+// device buffers owned by the caller's context, grown / allocated here.
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
-                            uint32_t max_desc, uint8_t* out, int num_sms, cudaStream_t s, std::string& err);
+                            uint32_t max_desc, uint8_t* out, void** scratch, size_t* scratch_bytes, int num_sms,
+                            cudaStream_t s, std::string& err);
 
 cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const uint8_t* codes,
                           const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,
-                          int num_sms, cudaStream_t s);
+                          void** acc, int num_sms, cudaStream_t s);
 
 // Exact verifier (k_exact.cu).  `arena` / `arena_bytes`: the byte-set table
 // arena, owned by the caller's context and grown here when max_points needs it.

@@ -31,6 +31,9 @@ struct picker_ctx {
   unsigned long long* dev_counts = nullptr;
   CountSlot* count_slots = nullptr;  // kCountSlots histogram slots (flush_counts), zeroed at allocation
   uint32_t count_seq = 0;            // next slot
+  void* seq_scratch = nullptr;       // row f1 window slices (grown on demand)
+  size_t seq_scratch_bytes = 0;
+  void* model_acc = nullptr;         // row f3 accumulator
   cudaStream_t aux = nullptr;
   void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
   size_t wide_scratch_bytes = 0;
@@ -116,6 +119,8 @@ void picker_destroy(picker_ctx_t* c) {
     DevGuard g(c->device);
     if (c->dev_tables) cudaFree(c->dev_tables);
     if (c->count_slots) cudaFree(c->count_slots);
+    if (c->seq_scratch) cudaFree(c->seq_scratch);
+    if (c->model_acc) cudaFree(c->model_acc);
     for (int i = 0; i < 2; ++i)
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
@@ -511,7 +516,8 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
   DevGuard g(c->device);
   DevBatch db{b->rec, b->args, 0, b->args_len};
   std::string err;
-  cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, max_desc, out, c->num_sms, (cudaStream_t)stream, err);
+  cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, max_desc, out, &c->seq_scratch, &c->seq_scratch_bytes,
+                                  c->num_sms, (cudaStream_t)stream, err);
   if (e != cudaSuccess) return cuda_fail(c, e, ("sequence: " + err).c_str());
   c->last_launches = n ? 1 : 0;
   return PICKER_OK;
@@ -527,7 +533,7 @@ int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
   DevGuard g(c->device);
   DevBatch db{b->rec, b->args, 0, b->args_len};
   cudaError_t e = launch_models(c->P.T, db, n, codes, ctx_bytes, prm->kill_ns, prm->save_bytes_per_us, out,
-                                c->num_sms, (cudaStream_t)stream);
+                                &c->model_acc, c->num_sms, (cudaStream_t)stream);
   if (e != cudaSuccess) return cuda_fail(c, e, "consumer models");
   c->last_launches = n ? 1 : 0;
   return PICKER_OK;
