@@ -256,6 +256,19 @@ int picker_consumer_models(picker_ctx_t* ctx, const picker_batch_t* batch, uint6
                            const uint64_t* ctx_bytes, const picker_model_params_t* params,
                            picker_model_out_t* out, void* stream);
 
+/* Validation and the consumer models in ONE pass over the records: the
+ * outputs of picker_validate_batch (flags_out required, bits / counts
+ * nullable) and of picker_consumer_models on those verdicts, equal to the
+ * two calls made in turn.  Each record's input bytes are computed where its
+ * verdict is (the pipelined kernel of a specialised module built with the
+ * model code on the first call, from the staged arguments); summaries the
+ * fused kernel does not take (table path, sorted schedule, K2 kernel,
+ * n <= 1024) run the two passes.  ctx_bytes: device u64[n] or NULL; out:
+ * HOST struct.  SYNCHRONOUS on `stream`.                                      */
+int picker_validate_models(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n, uint8_t* flags_out,
+                           uint32_t* idem_bits_out, uint64_t* counts_out, const uint64_t* ctx_bytes,
+                           const picker_model_params_t* params, picker_model_out_t* out, void* stream);
+
 /* Number of kernels loaded and the path each kernel was compiled to
  * (per-kernel introspection for tests): path_out[i] for kernel id ids_out[i];
  * path 0 = shortcut, 1 = generic table path, 2 = specialised (JIT) path,

@@ -69,6 +69,9 @@ SIGNATURES = {
     "picker_consumer_models": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P,
                                               ctypes.POINTER(picker_model_params_t),
                                               ctypes.POINTER(picker_model_out_t), P]),
+    "picker_validate_models": (ctypes.c_int, [P, ctypes.POINTER(picker_batch_t), U64, P, P, P, P,
+                                              ctypes.POINTER(picker_model_params_t),
+                                              ctypes.POINTER(picker_model_out_t), P]),
     "picker_kernel_info": (ctypes.c_int, [P, P, P, ctypes.c_uint32]),
     "picker_set_option": (ctypes.c_int, [P, ctypes.c_char_p, ctypes.c_int64]),
     "picker_last_launch_count": (ctypes.c_int, [P]),

@@ -48,6 +48,8 @@ struct JitModule {
   cudaLibrary_t lib = nullptr;
   cudaKernel_t kernel = nullptr;
   cudaKernel_t small_kernel = nullptr;  // k_validate_small: n <= kSmallMax
+  bool pipe = false;                    // main kernel is k_validate_pipe (<= kPipeKeysMax keys)
+  bool models = false;                  // built with PICKER_MODELS (row f3 fused)
   size_t smem = 0;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
@@ -728,6 +730,7 @@ std::vector<std::string> geometry_defines(const Options& opt) {
           "-DPICKER_CTAS=" + std::to_string(opt.ctas),
           "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
           "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
+          opt.models ? "-DPICKER_MODELS=1" : "-DPICKER_NO_MODELS=1",
           "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
           "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot)),
           "-DPICKER_SORT_STAGES=" + std::to_string(std::max(2, opt.sort_warps)),
@@ -839,6 +842,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->tile = opt.tile;
   m->threads = opt.threads;
   m->ctas = opt.ctas;
+  m->pipe = plan.src.find("k_validate_pipe<JitDispatch>") != std::string::npos;
+  m->models = opt.models;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   std::vector<std::string> names;  // main, small, [the sorted schedule's kernels]
   for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
@@ -928,6 +933,9 @@ bool jit_is_stride(const JitModule* m) { return m && m->stride; }
 int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 : 0; }
 
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
+bool jit_fused_models(const JitModule* m, uint64_t n) {
+  return m && m->models && m->pipe && !m->sk[3] && !jit_small_path(m, n);
+}
 
 int jit_launch_count(const JitModule* m, uint64_t n) {
   return m && m->sk[3] && n > kSmallMax && n < (1ULL << 32) ? 4 : 1;

@@ -31,8 +31,18 @@
 #include "device_common.cuh"
 #include "desc_eval.cuh"
 #include "eval_generic.cuh"
+#include "models.cuh"
 
 namespace picker {
+
+// Row f3 fused into the pipelined kernel (picker_validate_models): every
+// record's AR input bytes and Chimera latencies are accumulated where its
+// verdict is decided -- the staged arguments are read once for both.
+#ifdef PICKER_MODELS
+constexpr bool kModels = true;
+#else
+constexpr bool kModels = false;
+#endif
 
 // A specialised module without wide (K2) kernels is compiled with
 // PICKER_NO_WIDE: the warp-cooperative path is then dead code that would sit
@@ -434,9 +444,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   __shared__ __align__(8) uint64_t s_abar;  // kArgBufs == 1: the argument buffer
   __shared__ StageInfo s_info[2];
   __shared__ __align__(16) uint64_t s_bnd[3];  // thread 0: bounds of the next tile to stage
+  __shared__ uint32_t s_mh[kModels ? 2 * PICKER_MODEL_HIST : 1];  // model histograms (without, with)
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t lt_mask = (1u << lane) - 1u;
+  ModelSums ms{};
+  if (kModels)
+    for (int b = tid; b < 2 * PICKER_MODEL_HIST; b += kThreads) s_mh[b] = 0;
+  // one record's models: input bytes from its verdict, context-save latency
+  auto model = [&](uint64_t gi, uint32_t code, const picker_rec_t& r, const int64_t* a) {
+    uint64_t b = 0;
+    const bool known = model_input_bytes_coded(P.T, r, a, code, b);
+    model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, code, known, b, P.ctx_bytes ? P.ctx_bytes[gi] : 0, P.kill_ns,
+              P.save_bpu);
+  };
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t G = gridDim.x;
   if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
@@ -505,8 +526,13 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int i = q * kThreads + warp * 32 + lane;
       if (key[q] == P.direct_key) {  // shortcut / unknown: final here, not sorted
         const uint2 h = *reinterpret_cast<const uint2*>(hdr + 32 * i + 24);
-        s_code[buf * kTile + i] = (uint8_t)direct_code(e[q], *reinterpret_cast<const uint32_t*>(hdr + 32 * i + 4),
-                                                       (uint64_t)h.y << 32 | h.x, B.args_lo, B.args_hi);
+        const uint32_t dc = direct_code(e[q], *reinterpret_cast<const uint32_t*>(hdr + 32 * i + 4),
+                                        (uint64_t)h.y << 32 | h.x, B.args_lo, B.args_hi);
+        s_code[buf * kTile + i] = (uint8_t)dc;
+        if constexpr (kModels) {  // (the arguments of tile + 1 are not staged yet: global)
+          const picker_rec_t r = rec_from_smem(hdr + 32 * i);
+          model(tile * kTile + i, dc, r, B.args + r.arg_off);
+        }
         key[q] = 0xFFu;
       }
     }
@@ -629,6 +655,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                                    : B.args + r.arg_off;
           const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane, wide_scratch(P, warp));
           if (lane == 0) s_code[buf * kTile + wi] = cw;
+          if constexpr (kModels)
+            if (lane == 0) model(base + wi, cw, r, a);
         }
         continue;
       }
@@ -648,6 +676,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
                                  : B.args + r.arg_off;
         const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
         s_code[buf * kTile + li] = code;
+        if constexpr (kModels) model(base + li, code, r, a);
       }
     }
     if (tile + G < ntiles) keys(tile + G, it + 1);
@@ -658,6 +687,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   }
   __syncthreads();
   flush_counts(s_hist, counts, P.count_slot);
+  if constexpr (kModels) model_flush(ms, s_mh, s_mh + PICKER_MODEL_HIST, P.model_acc);
 }
 
 // Small batches (n <= kSmallMax, one CTA): one thread per record straight from

@@ -33,6 +33,7 @@ struct Options {
   int sorted = -1, sort_warps = 0, sort_slot = 0;
   int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
   int sort_ws = -1;   // sorted schedule: warp-specialised S4 (1), one warp per group (0), -1 auto
+  bool models = false;  // module variant with row f3 fused into the pipelined kernel (PICKER_MODELS)
   // summaries whose evaluating kernels are all wide: the K2 persistent kernel
   // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
   int wide_kernel = -1;
@@ -65,6 +66,15 @@ int jit_launch_count(const JitModule* m, uint64_t n);
 int jit_warps_per_sm(const JitModule* m);
 // The module has the small-batch kernel and n <= kSmallMax (one CTA, counts written).
 bool jit_small_path(const JitModule* m, uint64_t n);
+// A models module (Options.models) whose launch for n records is the fused
+// pipelined kernel (not the small-batch kernel, the bucket kernel or the
+// sorted schedule, which carry no model code).
+bool jit_fused_models(const JitModule* m, uint64_t n);
+cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags,
+                       uint32_t* bits, unsigned long long* counts, int num_sms, cudaStream_t s);
+// Row f3 accumulator of a context: zero it on `s` / copy it to `out` and sync.
+cudaError_t model_acc_begin(void** acc, cudaStream_t s);
+cudaError_t model_acc_end(void* acc, uint64_t n, picker_model_out_t* out, cudaStream_t s);
 // Fills in the automatic geometry (tile = 0) from the summaries.
 Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt);
 // ... and adjusts it once the module's grouping-key count is known.

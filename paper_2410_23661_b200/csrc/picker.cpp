@@ -34,6 +34,7 @@ struct picker_ctx {
   void* seq_scratch = nullptr;       // row f1 window slices (grown on demand)
   size_t seq_scratch_bytes = 0;
   void* model_acc = nullptr;         // row f3 accumulator
+  JitModule* jit_models = nullptr;   // the specialised module with row f3 fused (built on first use)
   cudaStream_t aux = nullptr;
   void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
   size_t wide_scratch_bytes = 0;
@@ -90,6 +91,25 @@ int check_batch(picker_ctx* c, const picker_batch_t* b, uint64_t n, const void* 
   return PICKER_OK;
 }
 
+// Counts are written by the launch itself (the last CTA through a histogram
+// slot, or the small-batch kernel): P.count_slot gets this call's slot;
+// launch_validate zeroes counts first only on the paths without slots.
+int count_slot(picker_ctx* c, uint64_t* counts, uint64_t n, cudaStream_t s, BucketParams& P) {
+  if (counts && n) {
+    if (!c->count_slots) {
+      cudaError_t e = cudaMalloc(&c->count_slots, kCountSlots * sizeof(CountSlot));
+      if (e != cudaSuccess) return fail(c, PICKER_ENOMEM, "cudaMalloc(count slots)");
+      e = cudaMemset(c->count_slots, 0, kCountSlots * sizeof(CountSlot));
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset(count slots)");
+    }
+    P.count_slot = c->count_slots + (c->count_seq++ % kCountSlots);
+  } else if (counts) {  // n == 0: nothing launches
+    cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
+  }
+  return PICKER_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -121,6 +141,7 @@ void picker_destroy(picker_ctx_t* c) {
     if (c->count_slots) cudaFree(c->count_slots);
     if (c->seq_scratch) cudaFree(c->seq_scratch);
     if (c->model_acc) cudaFree(c->model_acc);
+    jit_destroy(c->jit_models);
     for (int i = 0; i < 2; ++i)
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
@@ -229,6 +250,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->P.wide_scratch = scratch_bytes ? c->wide_scratch : nullptr;
   if (c->dev_tables) cudaFree(c->dev_tables);
   jit_destroy(c->jit);
+  jit_destroy(c->jit_models);
+  c->jit_models = nullptr;
   c->jit = jm;
   c->dev_tables = dev;
   c->dev_tables_bytes = blob.size();
@@ -370,22 +393,9 @@ int picker_validate_batch(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, 
   c->last_launches = 0;
   Options o = c->opt;
   if (o.bucket < 0) o.bucket = c->bucket_auto;
-  // counts are written by the launch itself (the last CTA through a histogram
-  // slot, or the small-batch kernel); launch_validate zeroes them first only
-  // on the paths without slots
   BucketParams P = c->P;
-  if (counts && n) {
-    if (!c->count_slots) {
-      cudaError_t e = cudaMalloc(&c->count_slots, kCountSlots * sizeof(CountSlot));
-      if (e != cudaSuccess) return fail(c, PICKER_ENOMEM, "cudaMalloc(count slots)");
-      e = cudaMemset(c->count_slots, 0, kCountSlots * sizeof(CountSlot));
-      if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemset(count slots)");
-    }
-    P.count_slot = c->count_slots + (c->count_seq++ % kCountSlots);
-  } else if (counts) {  // n == 0: nothing launches
-    cudaError_t e = cudaMemsetAsync(counts, 0, PICKER_NUM_COUNTS * sizeof(uint64_t), s);
-    if (e != cudaSuccess) return cuda_fail(c, e, "cudaMemsetAsync(counts)");
-  }
+  st = count_slot(c, counts, n, s, P);
+  if (st) return st;
   DevBatch db{b->rec, b->args, 0, b->args_len};
   cudaError_t e = launch_validate(P, c->jit, o, db, n, flags, bits,
                                   (unsigned long long*)counts, c->num_sms, s, &c->last_launches);
@@ -537,6 +547,53 @@ int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
   if (e != cudaSuccess) return cuda_fail(c, e, "consumer models");
   c->last_launches = n ? 1 : 0;
   return PICKER_OK;
+}
+
+int picker_validate_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, uint8_t* flags, uint32_t* bits,
+                           uint64_t* counts, const uint64_t* ctx_bytes, const picker_model_params_t* prm,
+                           picker_model_out_t* out, void* stream) {
+  int st = check_batch(c, b, n, flags);
+  if (st) return st;
+  if (!prm || !out || prm->save_bytes_per_us == 0)
+    return fail(c, PICKER_EINVAL, "params/out must be non-null and save_bytes_per_us > 0");
+  DevGuard g(c->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  // the fused pass: specialised kernels only (no wide kernel: its warp
+  // scratch is sized for the main module's geometry), no stride mode
+  bool fused = c->jit && !c->opt.stride && n > kSmallMax;
+  for (auto& k : c->ir) fused &= k.path != PATH_WIDE && k.path != PATH_GENERIC;
+  if (fused && !c->jit_models) {
+    Options mo = c->opt;
+    mo.models = true;
+    mo.sorted = 0;  // the model code is in the pipelined kernel
+    std::string err;
+    c->jit_models = jit_build(c->ir, mo, err);
+    if (!c->jit_models) return fail(c, PICKER_ECUDA, "JIT (models): " + err);
+  }
+  if (fused && jit_fused_models(c->jit_models, n)) {
+    BucketParams P = c->P;
+    st = count_slot(c, counts, n, s, P);
+    if (st) return st;
+    P.ctx_bytes = ctx_bytes;
+    P.kill_ns = prm->kill_ns;
+    P.save_bpu = prm->save_bytes_per_us;
+    cudaError_t e = model_acc_begin(&c->model_acc, s);
+    P.model_acc = (ModelAcc*)c->model_acc;
+    DevBatch db{b->rec, b->args, 0, b->args_len};
+    if (e == cudaSuccess)
+      e = launch_jit(c->jit_models, P, db, n, flags, bits, (unsigned long long*)counts, c->num_sms, s);
+    if (e == cudaSuccess) e = model_acc_end(c->model_acc, n, out, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "validate + models");
+    c->last_launches = 1;
+    return PICKER_OK;
+  }
+  // two passes: the verdicts, then the models on them
+  st = picker_validate_batch(c, b, n, flags, bits, counts, stream);
+  if (st) return st;
+  const int launches = c->last_launches;
+  st = picker_consumer_models(c, b, n, flags, ctx_bytes, prm, out, stream);
+  c->last_launches += launches;
+  return st;
 }
 
 int picker_replicate(picker_ctx_t* c, const picker_batch_t* b, uint64_t n, const uint8_t* ptr_mask,

@@ -186,6 +186,12 @@ struct CountSlot {
 };
 constexpr int kCountSlots = 64;
 
+// Row f3 accumulator (models.cuh): sums and 1-us histograms of one call.
+struct ModelAcc {
+  unsigned long long n_idem, ckpt_all, ckpt_ni, unknown, pre_without, pre_with;
+  unsigned long long hist_without[PICKER_MODEL_HIST], hist_with[PICKER_MODEL_HIST];
+};
+
 // Kernel-id -> bucket map for the bucketed kernels (k_bucket.cuh).
 struct BucketParams {
   Tables T;
@@ -199,6 +205,10 @@ struct BucketParams {
   uint32_t direct_key;         // key whose code is final in the key pass (KbEntry.kn = direct
                                // code, see direct_code); 0xFFFFFFFF: none
   CountSlot* count_slot;       // this launch's histogram slot (flush_counts); nullptr: accumulate
+  // row f3 fused into the pipelined kernel (module built with PICKER_MODELS)
+  const uint64_t* ctx_bytes;   // per record, or nullptr (0)
+  unsigned long long kill_ns, save_bpu;
+  ModelAcc* model_acc;
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads

@@ -63,6 +63,13 @@ def _stream_handle(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
+def _models_dict(out):
+    return {"n": out.n, "n_idem": out.n_idem, "ckpt_bytes_all": out.ckpt_bytes_all,
+            "ckpt_bytes_ni": out.ckpt_bytes_ni, "unknown_input": out.unknown_input,
+            "preempt_ns_without": out.preempt_ns_without, "preempt_ns_with": out.preempt_ns_with,
+            "hist_without": list(out.hist_without), "hist_with": list(out.hist_with)}
+
+
 class Picker:
     """A validator context on one device (picker_create / picker_destroy)."""
 
@@ -236,7 +243,33 @@ class Picker:
         self._check(lib.picker_consumer_models(
             self._h, ctypes.byref(b), n, codes.data_ptr(), cb.data_ptr() if cb is not None else None,
             ctypes.byref(prm), ctypes.byref(out), _stream_handle(stream)))
-        return {"n": out.n, "n_idem": out.n_idem, "ckpt_bytes_all": out.ckpt_bytes_all,
-                "ckpt_bytes_ni": out.ckpt_bytes_ni, "unknown_input": out.unknown_input,
-                "preempt_ns_without": out.preempt_ns_without, "preempt_ns_with": out.preempt_ns_with,
-                "hist_without": list(out.hist_without), "hist_with": list(out.hist_with)}
+        return _models_dict(out)
+
+    def validate_models(self, rec, args, ctx_bytes=None, *, kill_ns=1000, save_bytes_per_us=1000, out=None,
+                        stream=None):
+        """Verdicts and row f3 in one pass (picker_validate_models).  Synchronous;
+        returns (flags, bits, counts) as ``validate`` plus the models dict of
+        ``consumer_models``."""
+        rec = records_tensor(rec, self.device)
+        if not torch.is_tensor(args):
+            args = torch.from_numpy(np.asarray(args, dtype=np.int64))
+        args = args.to(self.device)
+        n = rec.shape[0]
+        if out is None:
+            flags = torch.empty(n, dtype=torch.uint8, device=self.device)
+            bw = torch.empty((n + 31) // 32, dtype=torch.int32, device=self.device)
+            cnt = torch.empty(NUM_COUNTS, dtype=torch.int64, device=self.device)
+        else:
+            flags, bw, cnt = out
+        cb = None
+        if ctx_bytes is not None:
+            cb = torch.from_numpy(np.asarray(ctx_bytes, np.uint64).view(np.int64)).to(self.device) \
+                if not torch.is_tensor(ctx_bytes) else ctx_bytes.to(self.device)
+        prm = picker_model_params_t(int(kill_ns), int(save_bytes_per_us))
+        mo = picker_model_out_t()
+        b = self._batch(rec, args, True)
+        self._check(lib.picker_validate_models(
+            self._h, ctypes.byref(b), n, flags.data_ptr(), bw.data_ptr() if bw is not None else None,
+            cnt.data_ptr() if cnt is not None else None, cb.data_ptr() if cb is not None else None,
+            ctypes.byref(prm), ctypes.byref(mo), _stream_handle(stream)))
+        return (flags, bw, cnt), _models_dict(mo)

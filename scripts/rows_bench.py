@@ -5,7 +5,8 @@ fraction with the same algorithmic bytes as K1 (32-byte header +
 
   f1 picker_validate_sequence  C2 x686 (12.5 M records), windows of 32,
                                sequential and concurrent
-  f3 picker_consumer_models    C2 x686 with its codes and context sizes
+  f3 picker_consumer_models    C2 x686 with its codes and context sizes (and
+     picker_validate_models: verdicts + models in one pass)
   f4 stride-aware K1           C2 x686, module generated stride-aware
   K3 picker_exact_check        C3 small-grid subset x64 (262,144 records)
 
@@ -80,6 +81,15 @@ def main():
     ctx = torch.from_numpy((np.arange(n, dtype=np.int64) % 97 + 1) * 4096).to(dev)
     ms = timed(lambda: p.consumer_models(rd, ad, flags, ctx), a.steps)
     row("f3_consumer_models", n, base + n + 8 * n, ms)
+    two = p.consumer_models(rd, ad, flags, ctx)
+    # f3 fused: verdicts and models in one pass (the K1 bytes + 8 bytes of
+    # context size per record); equal to the two passes above
+    outs = (torch.empty(n, dtype=torch.uint8, device=dev), torch.empty((n + 31) // 32, dtype=torch.int32, device=dev),
+            torch.empty(16, dtype=torch.int64, device=dev))
+    ms = timed(lambda: p.validate_models(rd, ad, ctx, out=outs), a.steps)
+    (ff, _, _), fused = p.validate_models(rd, ad, ctx, out=outs)
+    row("f3_fused_validate_models", n, base + n + n / 8 + 8 * n, ms, launches=p.last_launch_count(),
+        equal_to_two_passes=bool(fused == two and torch.equal(ff, flags)))
     p.close()
     # f4: the stride-aware specialised module
     ps = pk.Picker(0, stride=1)

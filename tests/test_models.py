@@ -144,6 +144,53 @@ def test_gpu_models_c2():
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("seed", [81, 82])
+def test_gpu_validate_models_random(seed):
+    """Verdicts and models in one pass (picker_validate_models): the fused
+    pipelined kernel for n > 1024, the two passes for a small batch; both equal
+    to the oracle's verdicts and the oracle's models on them."""
+    import paper_2410_23661_b200 as pk
+    s = random_summary(seed, n_kernels=30)
+    rec, args = random_records(seed + 1000, s, 3000, max_threads=256, max_grid=64)
+    codes = np.array(O.oracle_batch(s, rec, args), np.uint8)
+    ctx = np.random.default_rng(seed).integers(0, 200_000, len(rec)).astype(np.uint64)
+    p = pk.Picker(0)
+    p.load(s)
+    for m in (len(rec), 700):
+        (flags, bits, counts), got = p.validate_models(rec[:m], args, ctx[:m], kill_ns=1000, save_bytes_per_us=1500)
+        assert np.array_equal(flags.cpu().numpy(), codes[:m])
+        assert np.array_equal(counts.cpu().numpy(), np.bincount(np.where(codes[:m] <= 11, codes[:m], 15),
+                                                                minlength=16))
+        want = O.oracle_models(s, rec[:m], args, codes[:m], ctx[:m], kill_ns=1000, save_bytes_per_us=1500)
+        assert got == want
+
+
+@pytest.mark.gpu
+def test_gpu_validate_models_c2_fused():
+    """C2 and C2 x 8 (the fused kernel's steady state, >= 3 tiles per CTA): one
+    launch; verdicts = the oracle's (tiled), models = the oracle's on the base
+    trace times 8 (copies are the same instances relocated)."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, meta = workloads.make_c2()
+    codes = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
+    ctx = np.random.default_rng(5).integers(4_000, 98_001, len(rec)).astype(np.uint64)
+    want = O.oracle_models(s, rec, args, codes, ctx)
+    p = pk.Picker(0)
+    p.load(s)
+    (flags, _, _), got = p.validate_models(rec, args, ctx)
+    assert p.last_launch_count() == 1
+    assert np.array_equal(flags.cpu().numpy(), codes)
+    assert got == want
+    R = 8
+    rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
+    (flags, _, _), got = p.validate_models(rec_t, args_t, np.tile(ctx, R))
+    assert np.array_equal(flags.cpu().numpy(), np.tile(codes, R))
+    want_t = {k: (v * R if isinstance(v, int) else [x * R for x in v]) for k, v in want.items()}
+    assert got == want_t
+
+
+@pytest.mark.gpu
 def test_gpu_models_errors():
     """Call errors are statuses, not crashes: save bandwidth 0 -> EINVAL."""
     import paper_2410_23661_b200 as pk
