@@ -134,11 +134,16 @@ constexpr size_t kLoopMin = 3;  // class size
 size_t g_loop_kernel_min = 6;  // streamed descriptors of the kernel (Options.loop_min, set by jit_plan)
 uint64_t fnv1a(const std::string& s);
 
-std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs) {
+// models: the module of picker_validate_models -- the reads are the kept side
+// and, before the verdict, the length of the union of the active non-opaque
+// read extents goes to *inb (row f3, reading Q25; models.cuh).
+std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs,
+                     bool models = false) {
   Gen g(K);
   std::ostringstream& s = g.s;
   const int np = (int)k.param_names.size();
-  s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K) {\n";
+  s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K"
+    << (models ? ", uint64_t* inb" : "") << ") {\n";
   s << "  const int64_t d0 = r.grid_x, d1 = r.grid_y, d2 = r.grid_z, d3 = r.block_x, d4 = r.block_y,"
        " d5 = r.block_z;\n";
   // (the CUDA launch limits are checked once in the dispatch, before the switch)
@@ -238,7 +243,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
   size_t nr = 0, nw = 0;
   for (auto& d : k.desc)
     if (!d.opaque) (d.kind == KIND_R ? nr : nw)++;
-  const uint8_t kept_kind = nw <= nr ? KIND_W : KIND_R;
+  const uint8_t kept_kind = models ? KIND_R : nw <= nr ? KIND_W : KIND_R;
   auto on_expr = [&](size_t di) {
     const IrDesc& d = k.desc[di];
     std::string on = "true";
@@ -435,6 +440,28 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
     for (int i : a) e += " || on" + std::to_string(i);
     return e;
   };
+  if (models) {
+    // union length without sorting: read i contributes its bytes above the
+    // highest ub of the reads before it in (lb, index) order (the sweep line)
+    if (kept.size() <= 12) {
+      s << "  if (inb) {\n    uint64_t un = 0;\n";
+      for (int i : kept) {
+        const std::string I = std::to_string(i);
+        s << "    {\n      int64_t mx = (-9223372036854775807LL - 1);\n";
+        for (int j : kept) {
+          if (j == i) continue;
+          const std::string J = std::to_string(j);
+          s << "      if (on" << J << " & (lb" << J << (j < i ? " <= " : " < ") << "lb" << I << ")) mx = max64(mx, ub" << J
+            << ");\n";
+        }
+        s << "      const int64_t st = max64(lb" << I << " - 1, mx);\n";
+        s << "      if (on" << I << " & (ub" << I << " > st)) un += (uint64_t)(ub" << I << " - st);\n    }\n";
+      }
+      s << "    *inb = (" << any(opq_r) << ") ? kInbUnknown : un;\n  }\n";
+    } else {
+      s << "  if (inb) *inb = kInbTable;\n";
+    }
+  }
   if (!opq_r.empty() || !opq_w.empty())  // opaque rule before overlap (precedence 9 < 10)
     s << "  if (((" << any(opq_r) << ") && act_w) || ((" << any(opq_w) << ") && act_r)) return V_NI_OPAQUE;\n";
   s << "  return ov ? V_NI_OVERLAP : V_IDEM_CHECKED;\n}\n";
@@ -556,7 +583,8 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 
 }  // namespace
 
-JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws, int loop_min) {
+JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws, int loop_min,
+                 bool models) {
   g_loop_kernel_min = (size_t)std::max(1, loop_min);
   JitPlan P;
   std::ostringstream src;
@@ -582,7 +610,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
   std::map<std::string, std::string> idx_defs;  // argument-index tables of the loop classes
   for (size_t i = 0; i < ks.size(); ++i) {
     if (ks[i].path != PATH_JIT) continue;
-    std::string body = gen_body(ks[i], kconst[i], stride, &idx_defs);
+    std::string body = gen_body(ks[i], kconst[i], stride, &idx_defs, models);
     auto it = shape_id.find(body);
     if (it == shape_id.end()) {
       it = shape_id.emplace(body, (uint32_t)shapes.size()).first;
@@ -672,7 +700,8 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
   // only the arity needs a test
   src << "struct JitDispatch {\n"
          "  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local, "
-         "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B) {\n"
+         "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B"
+      << (models ? ", uint64_t* inb = nullptr" : "") << ") {\n"
          "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
       << (!table_path ? ""
@@ -691,7 +720,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n";
   for (size_t s = 0; s < shapes.size(); ++s)
-    src << "      case " << SHAPE_FIRST + s << ": return ks" << s << "(r, a, K);\n";
+    src << "      case " << SHAPE_FIRST + s << ": return ks" << s << (models ? "(r, a, K, inb);\n" : "(r, a, K);\n");
   src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
          "template __global__ void " << (shape_shortcut + 1 <= kPipeKeysMax ? "k_validate_pipe" : "k_validate_bucket")
       << "<JitDispatch>(const __grid_constant__ BucketParams, "
@@ -802,6 +831,9 @@ Options resolve_geometry(const std::vector<IrKernel>& ks, Options opt) {
     // tiles (fuller groups: C2 49.9-50.4 G inst/s) rather than 4 x 224 on 448
     // (C2 47.9-48.1, C3 +1.7 %); profiles/r01_sweep_geometry.txt
     opt.tile = 896, opt.threads = 448, opt.ctas = 2, opt.args_per_rec = 5, opt.arg_bufs = 1;
+    // the models module keeps model sums live across the tile loop: 102
+    // registers per thread (C2 fused f3 0.953 -> 0.831 ms; r02_ab_log)
+    if (opt.models) opt.tile = 640, opt.threads = 320, opt.args_per_rec = 6;
   } else {
     // one argument buffer: its 16 KB go to 2560-record tiles (C4 1.96 -> 2.01 G inst/s)
     opt.tile = 2560, opt.threads = 512, opt.ctas = 1, opt.args_per_rec = 1, opt.arg_bufs = 1;
@@ -827,7 +859,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min, opt.models);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
   geometry_for_keys(opt, opt_in.tile == 0, (uint32_t)opt.pipe_keys);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {

@@ -674,9 +674,20 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         // cache on large summaries (C4: 1.04 -> 0.32 G inst/s)
         const int64_t* a = local ? reinterpret_cast<const int64_t*>(sarg + si.shift + 8 * (r.arg_off - si.lo))
                                  : B.args + r.arg_off;
-        const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
-        s_code[buf * kTile + li] = code;
-        if constexpr (kModels) model(base + li, code, r, a);
+        if constexpr (kModels) {  // the shape also returns the input bytes (specialised code)
+          uint64_t inb = kInbUnknown;
+          const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B, &inb);
+          s_code[buf * kTile + li] = code;
+          if (inb == kInbTable) {
+            model(base + li, code, r, a);
+          } else {
+            model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, code, inb != kInbUnknown, inb,
+                      P.ctx_bytes ? P.ctx_bytes[base + li] : 0, P.kill_ns, P.save_bpu);
+          }
+        } else {
+          const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
+          s_code[buf * kTile + li] = code;
+        }
       }
     }
     if (tile + G < ntiles) keys(tile + G, it + 1);

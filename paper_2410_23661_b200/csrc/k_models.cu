@@ -35,7 +35,7 @@ static __device__ bool input_bytes(const Tables& T, const picker_rec_t& r, const
 __global__ void __launch_bounds__(kModelThreads) k_models(Tables T, DevBatch B, uint64_t n,
                                                           const uint8_t* __restrict__ codes,
                                                           const uint64_t* __restrict__ ctx_bytes, uint64_t kill_ns,
-                                                          uint64_t save_bpu, ModelAcc* __restrict__ acc) {
+                                                          ModelDiv save_bpu, ModelAcc* __restrict__ acc) {
   __shared__ int64_t s_elo[kModelFast * kModelThreads], s_ehi[kModelFast * kModelThreads];
   __shared__ uint32_t s_hw[PICKER_MODEL_HIST], s_hi[PICKER_MODEL_HIST];
   for (int i = threadIdx.x; i < PICKER_MODEL_HIST; i += blockDim.x) s_hw[i] = s_hi[i] = 0;
@@ -84,8 +84,8 @@ cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const 
   cudaError_t e = model_acc_begin(acc_buf, s);
   if (e == cudaSuccess && n) {
     const uint64_t blocks = std::min<uint64_t>((n + kModelThreads - 1) / kModelThreads, (uint64_t)num_sms * 3);
-    k_models<<<(unsigned)blocks, kModelThreads, 0, s>>>(T, b, n, codes, ctx_bytes, kill_ns, save_bpu,
-                                                        (ModelAcc*)*acc_buf);
+    k_models<<<(unsigned)blocks, kModelThreads, 0, s>>>(T, b, n, codes, ctx_bytes, kill_ns,
+                                                        ModelDiv::of(save_bpu), (ModelAcc*)*acc_buf);
     e = cudaGetLastError();
   }
   return e == cudaSuccess ? model_acc_end(*acc_buf, n, out, s) : e;

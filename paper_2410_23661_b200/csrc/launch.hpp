@@ -58,7 +58,7 @@ struct JitPlan {
   int nshapes = 0;
 };
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false,
-                 int loop_min = 6);
+                 int loop_min = 6, bool models = false);
 bool jit_is_stride(const JitModule* m);
 // Kernel launches one picker_validate_batch of n records makes on the module.
 int jit_launch_count(const JitModule* m, uint64_t n);

@@ -17,6 +17,9 @@
 namespace picker {
 
 constexpr int kModelMaxReads = 128;  // reading Q25 (oracle MODEL_MAX_READS)
+// input bytes from a specialised shape (models module): unknown / not computed
+// there (more than 12 reads: the table path below)
+constexpr uint64_t kInbUnknown = ~0ull, kInbTable = ~0ull - 1;
 
 // The read extents of one record in lb order (insertion into lo / hi, `stride`
 // apart, at most `cap`), then the length of their union.  false: unknown (an
@@ -101,20 +104,30 @@ static __device__ __noinline__ bool model_input_bytes_coded(const Tables& T, con
 struct ModelSums {
   unsigned long long n_idem, all, ni, unk, pw, pi;
 };
+// x / d with the invariant divisor's multiplier (ModelDiv, tables.hpp)
+__device__ __forceinline__ uint64_t model_div(uint64_t x, const ModelDiv& d) {
+  const uint64_t t = __umul64hi(d.m, x);
+  return (t + ((x - t) >> d.sh1)) >> d.sh2;
+}
+// one histogram bin += 1 per lane, aggregated over the active lanes with the same bin
+__device__ __forceinline__ void hist_inc(uint32_t* hist, uint32_t bin) {
+  const unsigned peers = __match_any_sync(__activemask(), bin);
+  if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&hist[bin], (uint32_t)__popc(peers));
+}
 __device__ __forceinline__ void model_add(ModelSums& s, uint32_t* hist_without, uint32_t* hist_with, uint32_t code,
                                           bool known, uint64_t bytes, uint64_t ctx_bytes, uint64_t kill_ns,
-                                          uint64_t save_bpu) {
+                                          const ModelDiv& save_bpu) {
   const bool idem = code <= V_IDEM_KERNEL;
   if (!known) ++s.unk, bytes = 0;
   s.all += bytes;
   if (!idem) s.ni += bytes;
   s.n_idem += idem;
-  const uint64_t save = ctx_bytes * 1000ull / save_bpu;
+  const uint64_t save = model_div(ctx_bytes * 1000ull, save_bpu);
   const uint64_t lat = idem ? kill_ns : save;
   s.pw += save;
   s.pi += lat;
-  atomicAdd(&hist_without[min(save / 1000, (uint64_t)PICKER_MODEL_HIST - 1)], 1u);
-  atomicAdd(&hist_with[min(lat / 1000, (uint64_t)PICKER_MODEL_HIST - 1)], 1u);
+  hist_inc(hist_without, (uint32_t)min(save / 1000, (uint64_t)PICKER_MODEL_HIST - 1));
+  hist_inc(hist_with, (uint32_t)min(lat / 1000, (uint64_t)PICKER_MODEL_HIST - 1));
 }
 // Every thread of the CTA: the CTA's sums (warp reductions + shared atomics)
 // and histograms into acc.

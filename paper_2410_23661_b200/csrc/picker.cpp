@@ -576,7 +576,7 @@ int picker_validate_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
     if (st) return st;
     P.ctx_bytes = ctx_bytes;
     P.kill_ns = prm->kill_ns;
-    P.save_bpu = prm->save_bytes_per_us;
+    P.save_bpu = ModelDiv::of(prm->save_bytes_per_us);
     cudaError_t e = model_acc_begin(&c->model_acc, s);
     P.model_acc = (ModelAcc*)c->model_acc;
     DevBatch db{b->rec, b->args, 0, b->args_len};

@@ -186,6 +186,28 @@ struct CountSlot {
 };
 constexpr int kCountSlots = 64;
 
+// x / d for a call's invariant divisor d (save_bytes_per_us), exact for every
+// u64 x (models.cuh model_div): Granlund-Montgomery with l = ceil(log2 d),
+// m = floor(2^64 (2^l - d) / d) + 1, t = mulhi(m, x),
+// q = (t + ((x - t) >> min(l, 1))) >> max(l - 1, 0).
+struct ModelDiv {
+  unsigned long long m;
+  unsigned int sh1, sh2;
+#ifndef __CUDACC_RTC__
+  static ModelDiv of(unsigned long long d) {
+    unsigned int l = 0;
+    while (l < 64 && (1ull << l) < d) ++l;  // ceil(log2 d)
+    const unsigned __int128 two64 = (unsigned __int128)1 << 64;
+    const unsigned __int128 pl = (unsigned __int128)1 << l;
+    ModelDiv v;
+    v.m = (unsigned long long)((two64 * (pl - d)) / d + 1);
+    v.sh1 = l < 1 ? l : 1;
+    v.sh2 = l > 1 ? l - 1 : 0;
+    return v;
+  }
+#endif
+};
+
 // Row f3 accumulator (models.cuh): sums and 1-us histograms of one call.
 struct ModelAcc {
   unsigned long long n_idem, ckpt_all, ckpt_ni, unknown, pre_without, pre_with;
@@ -207,7 +229,8 @@ struct BucketParams {
   CountSlot* count_slot;       // this launch's histogram slot (flush_counts); nullptr: accumulate
   // row f3 fused into the pipelined kernel (module built with PICKER_MODELS)
   const uint64_t* ctx_bytes;   // per record, or nullptr (0)
-  unsigned long long kill_ns, save_bpu;
+  unsigned long long kill_ns;
+  ModelDiv save_bpu;           // divisor of the context-save latency (save_bytes_per_us)
   ModelAcc* model_acc;
 };
 

@@ -51,6 +51,8 @@ def main():
     ap.add_argument("--replicas", type=int, default=686)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--opt", action="append", default=[], help="library option key=value for the C2 rows (tuning)")
+    ap.add_argument("--only", default=None, help="f3: only the f3 rows")
     a = ap.parse_args()
     peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6554.6))
     dev = torch.device("cuda", 0)
@@ -63,13 +65,13 @@ def main():
         print(name, json.dumps(out["rows"][name]), flush=True)
 
     s, rec, args, meta = workloads.make_c2()
-    p = pk.Picker(0)
+    p = pk.Picker(0, **{k: int(v) for k, v in (o.split("=") for o in a.opt)})
     p.load(s)
     rd, ad = p.replicate(rec, args, meta["ptr_mask"], a.replicas)
     n = rd.shape[0]
     base = 32 * n + 8 * int(ad.numel())
     # f1
-    for conc in (False, True):
+    for conc in ((False, True) if a.only is None else ()):
         W = 32
         ms = timed(lambda: p.validate_sequence(rd, ad, W, concurrent=conc), a.steps)
         got = p.validate_sequence(rd[:len(rec)], ad, W, concurrent=conc).cpu().numpy()
@@ -91,6 +93,10 @@ def main():
     row("f3_fused_validate_models", n, base + n + n / 8 + 8 * n, ms, launches=p.last_launch_count(),
         equal_to_two_passes=bool(fused == two and torch.equal(ff, flags)))
     p.close()
+    if a.only == "f3":
+        if a.out:
+            json.dump(out, open(a.out, "w"), indent=1)
+        return
     # f4: the stride-aware specialised module
     ps = pk.Picker(0, stride=1)
     ps.load(s)
