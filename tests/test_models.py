@@ -191,6 +191,25 @@ def test_gpu_validate_models_c2_fused():
 
 
 @pytest.mark.gpu
+def test_gpu_validate_models_c2heavy():
+    """C2-heavy: fused kernels with up to 29 reads (more than the 12 a
+    specialised shape sums itself: those records take the table path inside
+    the fused kernel) and the 128-key module."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, meta = workloads.make_c2(heavy=True)
+    codes = np.array(O.oracle_batch_mp(s, rec, args), np.uint8)
+    ctx = np.random.default_rng(9).integers(0, 300_000, len(rec)).astype(np.uint64)
+    want = O.oracle_models(s, rec, args, codes, ctx, kill_ns=700, save_bytes_per_us=3000)
+    p = pk.Picker(0)
+    p.load(s)
+    (flags, _, _), got = p.validate_models(rec, args, ctx, kill_ns=700, save_bytes_per_us=3000)
+    assert p.last_launch_count() == 1
+    assert np.array_equal(flags.cpu().numpy(), codes)
+    assert got == want
+
+
+@pytest.mark.gpu
 def test_gpu_models_errors():
     """Call errors are statuses, not crashes: save bandwidth 0 -> EINVAL."""
     import paper_2410_23661_b200 as pk
