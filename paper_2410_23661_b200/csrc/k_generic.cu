@@ -62,12 +62,14 @@ cudaError_t launch_bucket_generic(const BucketParams& P0, const DevBatch& B, uin
   const bool pipe = P.nkeys <= kPipeKeys;
   const size_t smem = pipe ? pipe_smem_bytes_for(kTile, PICKER_ARGS_PER_REC) : bucket_smem_bytes(P.nkeys);
   if (smem > kMaxSmem) return cudaErrorInvalidValue;
-  static size_t configured[2] = {0, 0};
-  if (smem > configured[pipe]) {
+  static size_t configured[64][2] = {};  // per device
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev >= 64) dev = -1;
+  if (dev < 0 || smem > configured[dev][pipe]) {
     cudaError_t e = cudaFuncSetAttribute(pipe ? k_validate_pipe<GenericDispatch> : k_validate_bucket<GenericDispatch>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
-    configured[pipe] = smem;
+    if (dev >= 0) configured[dev][pipe] = smem;
   }
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t cap = (uint64_t)num_sms * kCtasPerSm;

@@ -468,12 +468,14 @@ __global__ void __launch_bounds__(kWideWarps * 32, kWideCtas)
 cudaError_t launch_wide(const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags, uint32_t* bits,
                         unsigned long long* counts, int num_sms, cudaStream_t s) {
   if (n == 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(k_validate_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem);
+  static bool configured[64] = {};  // the attribute is per device
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev >= 64 || !configured[dev]) {
+    e = cudaFuncSetAttribute(k_validate_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem);
     if (e != cudaSuccess) return e;
-    configured = true;
+    if (dev < 64) configured[dev] = true;
   }
   const uint64_t nch = (n + 31) / 32;
   const uint64_t ctas_needed = (nch + kWideWarps - 1) / kWideWarps;
