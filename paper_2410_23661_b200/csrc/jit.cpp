@@ -50,6 +50,7 @@ struct JitModule {
   cudaKernel_t small_kernel = nullptr;  // k_validate_small: n <= kSmallMax
   bool pipe = false;                    // main kernel is k_validate_pipe (<= kPipeKeysMax keys)
   bool models = false;                  // built with PICKER_MODELS (row f3 fused)
+  bool extents = false;                 // built with PICKER_EXTENTS (row f1 on K1's extents)
   size_t smem = 0;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
@@ -137,13 +138,16 @@ uint64_t fnv1a(const std::string& s);
 // models: the module of picker_validate_models -- the reads are the kept side
 // and, before the verdict, the length of the union of the active non-opaque
 // read extents goes to *inb (row f3, reading Q25; models.cuh).
+// extents: the module of picker_validate_sequence on K1's extents (row f1) --
+// every active non-opaque extent goes to the record's arena slots and the
+// activity / opaque flags to xo.fl (XOut, models.cuh).
 std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, std::map<std::string, std::string>* defs,
-                     bool models = false) {
+                     bool models = false, bool extents = false) {
   Gen g(K);
   std::ostringstream& s = g.s;
   const int np = (int)k.param_names.size();
   s << "(const picker_rec_t& r, const int64_t* a, const int64_t* __restrict__ K"
-    << (models ? ", uint64_t* inb" : "") << ") {\n";
+    << (models ? ", uint64_t* inb" : "") << (extents ? ", XOut& xo" : "") << ") {\n";
   s << "  const int64_t d0 = r.grid_x, d1 = r.grid_y, d2 = r.grid_z, d3 = r.block_x, d4 = r.block_y,"
        " d5 = r.block_z;\n";
   // (the CUDA launch limits are checked once in the dispatch, before the switch)
@@ -325,9 +329,12 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
     s << "  act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
     if (d.opaque) {
       (d.kind == KIND_R ? opq_r : opq_w).push_back((int)di);
+      if (extents) s << "  if (on" << di << ") xo.fl |= " << (d.kind == KIND_R ? 4 : 8) << "u;\n";
       continue;
     }
     extent(di, "  ");
+    if (extents)
+      s << "  if (on" << di << ") xo_put(xo, " << (d.kind == KIND_W) << ", lb" << di << ", ub" << di << ");\n";
     kept.push_back((int)di);
   }
   // term sums of a descriptor without its base, constants as literals (the
@@ -396,6 +403,8 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
     s << "  {\n    const bool on" << di << " = " << on_expr(di) << ";\n";
     s << "    act_" << (d.kind == KIND_R ? "r" : "w") << " |= on" << di << ";\n";
     extent(di, "    ");
+    if (extents)
+      s << "    if (on" << di << ") xo_put(xo, " << (d.kind == KIND_W) << ", lb" << di << ", ub" << di << ");\n";
     std::string hit = "false";
     for (int j : kept) {
       const std::string I = std::to_string(di), J = std::to_string(j);
@@ -428,6 +437,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
     s << "        const uint32_t ej = " << name << "[j];\n";
     s << "        const int64_t bj = a[ej & 0xFFu];\n";
     s << "        const int64_t lbj = add64(bj, LOC), ubj = add64(add64(bj, HIC), (int64_t)(ej >> 8));\n";
+    if (extents) s << "        xo_put(xo, " << (k.desc[d0].kind == KIND_W) << ", lbj, ubj);\n";
     std::string hit = "false";
     for (int j : kept) {
       const std::string J = std::to_string(j);
@@ -440,6 +450,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
     for (int i : a) e += " || on" + std::to_string(i);
     return e;
   };
+  if (extents) s << "  xo.fl |= (act_r ? 1u : 0u) | (act_w ? 2u : 0u);\n";
   if (models) {
     // union length without sorting: read i contributes its bytes above the
     // highest ub of the reads before it in (lb, index) order (the sweep line)
@@ -584,7 +595,7 @@ bool nvrtc_compile(const std::string& src, const std::vector<std::string>& defin
 }  // namespace
 
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool sort_ws, int loop_min,
-                 bool models) {
+                 bool models, bool extents) {
   g_loop_kernel_min = (size_t)std::max(1, loop_min);
   JitPlan P;
   std::ostringstream src;
@@ -610,7 +621,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
   std::map<std::string, std::string> idx_defs;  // argument-index tables of the loop classes
   for (size_t i = 0; i < ks.size(); ++i) {
     if (ks[i].path != PATH_JIT) continue;
-    std::string body = gen_body(ks[i], kconst[i], stride, &idx_defs, models);
+    std::string body = gen_body(ks[i], kconst[i], stride, &idx_defs, models, extents);
     auto it = shape_id.find(body);
     if (it == shape_id.end()) {
       it = shape_id.emplace(body, (uint32_t)shapes.size()).first;
@@ -701,7 +712,7 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
   src << "struct JitDispatch {\n"
          "  static __device__ __forceinline__ uint8_t eval(uint32_t key, uint32_t bin, uint32_t kn, bool local, "
          "const BucketParams& P, const picker_rec_t& r, const int64_t* a, const DevBatch& B"
-      << (models ? ", uint64_t* inb = nullptr" : "") << ") {\n"
+      << (models ? ", uint64_t* inb = nullptr" : "") << (extents ? ", XOut* xo = nullptr" : "") << ") {\n"
          "    (void)bin;\n"
          "    if (key == 0) return V_ERR_KERNEL;\n"
       << (!table_path ? ""
@@ -720,7 +731,8 @@ JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted, bool
          "    const int64_t* __restrict__ K = P.jit_consts + (kn & 0xFFFFFFu);\n"
          "    switch (key) {\n";
   for (size_t s = 0; s < shapes.size(); ++s)
-    src << "      case " << SHAPE_FIRST + s << ": return ks" << s << (models ? "(r, a, K, inb);\n" : "(r, a, K);\n");
+    src << "      case " << SHAPE_FIRST + s << ": return ks" << s
+        << (models ? "(r, a, K, inb);\n" : extents ? "(r, a, K, *xo);\n" : "(r, a, K);\n");
   src << "    }\n    return V_ERR_KERNEL;\n  }\n};\n"
          "template __global__ void " << (shape_shortcut + 1 <= kPipeKeysMax ? "k_validate_pipe" : "k_validate_bucket")
       << "<JitDispatch>(const __grid_constant__ BucketParams, "
@@ -760,6 +772,7 @@ std::vector<std::string> geometry_defines(const Options& opt) {
           "-DPICKER_ARGS_PER_REC=" + std::to_string(opt.args_per_rec),
           "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
           opt.models ? "-DPICKER_MODELS=1" : "-DPICKER_NO_MODELS=1",
+          opt.extents ? "-DPICKER_EXTENTS=1" : "-DPICKER_NO_EXTENTS=1",
           "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
           "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot)),
           "-DPICKER_SORT_STAGES=" + std::to_string(std::max(2, opt.sort_warps)),
@@ -859,7 +872,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
     err = "invalid tile / threads / ctas / args_per_rec options";
     return nullptr;
   }
-  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min, opt.models);
+  JitPlan plan = jit_plan(ks, opt.stride, opt.sorted > 0, opt.sort_ws > 0, opt.loop_min, opt.models, opt.extents);
   opt.pipe_keys = (int)(SHAPE_FIRST + (uint32_t)plan.nshapes + 1);
   geometry_for_keys(opt, opt_in.tile == 0, (uint32_t)opt.pipe_keys);
   if (SHAPE_FIRST + (uint32_t)plan.nshapes + 1 <= kPipeKeysMax && opt.tile % opt.threads) {
@@ -876,6 +889,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->ctas = opt.ctas;
   m->pipe = plan.src.find("k_validate_pipe<JitDispatch>") != std::string::npos;
   m->models = opt.models;
+  m->extents = opt.extents;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   std::vector<std::string> names;  // main, small, [the sorted schedule's kernels]
   for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
@@ -967,6 +981,9 @@ int jit_warps_per_sm(const JitModule* m) { return m ? m->ctas * m->threads / 32 
 bool jit_small_path(const JitModule* m, uint64_t n) { return m && m->small_kernel && n <= kSmallMax; }
 bool jit_fused_models(const JitModule* m, uint64_t n) {
   return m && m->models && m->pipe && !m->sk[3] && !jit_small_path(m, n);
+}
+bool jit_extents_ok(const JitModule* m, uint64_t n) {
+  return m && m->extents && m->pipe && !m->sk[3] && !jit_small_path(m, n);
 }
 
 int jit_launch_count(const JitModule* m, uint64_t n) {

@@ -43,6 +43,13 @@ constexpr bool kModels = true;
 #else
 constexpr bool kModels = false;
 #endif
+// Row f1 on K1's extents (picker_validate_sequence): the shapes also write each
+// record's extents to the arena.
+#ifdef PICKER_EXTENTS
+constexpr bool kExtents = true;
+#else
+constexpr bool kExtents = false;
+#endif
 
 // A specialised module without wide (K2) kernels is compiled with
 // PICKER_NO_WIDE: the warp-cooperative path is then dead code that would sit
@@ -684,6 +691,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
             model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, code, inb != kInbUnknown, inb,
                       P.ctx_bytes ? P.ctx_bytes[base + li] : 0, P.kill_ns, P.save_bpu);
           }
+        } else if constexpr (kExtents) {
+          XOut xo{P.xarena + (base + li) * 2 * P.xcap, P.xcap, 0, 0, 0};
+          const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B, &xo);
+          s_code[buf * kTile + li] = code;
+          P.xinfo[base + li] = xo_info(xo);
         } else {
           const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
           s_code[buf * kTile + li] = code;

@@ -48,9 +48,18 @@ __device__ __forceinline__ bool seq_less(const SeqIv& a, const SeqIv& b) {
   return a.node < b.node || (a.node == b.node && a.lb < b.lb);
 }
 
+// K1's verdicts and extents of the batch (row f1 reusing K1),
+// or all null: the window kernel evaluates the records from the tables.
+struct SeqK1 {
+  const uint8_t* codes;   // K1 verdict per record
+  const uint32_t* xinfo;  // nr | nw << 11 | flags << 22 (models.cuh XOut)
+  const int64_t* xarena;  // xcap (lb, ub) slots per record: reads first, writes from the back
+  uint32_t xcap;
+};
+
 // One window: returns its code (CTA-uniform).
 __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, uint32_t m, uint32_t mode, SeqIv* Rl,
-                              SeqIv* Wl, SeqIv* S, int64_t* PM, uint32_t cap) {
+                              SeqIv* Wl, SeqIv* S, int64_t* PM, uint32_t cap, const SeqK1& K1) {
   __shared__ uint32_t s_first, s_nr, s_nw, s_ns, s_hit;
   __shared__ uint8_t s_flags[1024];  // per instance: 1 act_r, 2 act_w, 4 opq_r, 8 opq_w
   __shared__ uint8_t s_code;
@@ -59,10 +68,34 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
   __syncthreads();
   // 1. records of the window
   for (uint32_t i = tid; i < m; i += blockDim.x) {
-    const picker_rec_t r = load_rec(B.rec + w0 + i);
     uint8_t status = kEvaluable, fl = 0;
+    if (K1.codes) {
+      // K1 decided the record: a code before any address decides (0xFF, 0xFE,
+      // 2-8); 0 / 9 / 10: its extents and flags are in the arena; 1 (a
+      // kernel-level idempotent kernel, whose checks K1 does not evaluate):
+      // the tables below
+      const uint32_t c = K1.codes[w0 + i];
+      if (c >= V_NI_SO && c != V_NI_OPAQUE && c != V_NI_OVERLAP) {
+        status = (uint8_t)c;
+      } else if (c != V_IDEM_KERNEL) {
+        const uint32_t info = K1.xinfo[w0 + i];
+        const uint32_t nr = info & 0x7FFu, nw = (info >> 11) & 0x7FFu;
+        fl = (uint8_t)(info >> 22);
+        const int64_t* x = K1.xarena + (w0 + i) * 2 * K1.xcap;
+        const uint32_t pr = nr ? atomicAdd(&s_nr, nr) : 0u, pw = nw ? atomicAdd(&s_nw, nw) : 0u;
+        for (uint32_t q = 0; q < nr; ++q)
+          if (pr + q < cap) Rl[pr + q] = SeqIv{x[2 * q], x[2 * q + 1], i, 0};
+        for (uint32_t q = 0; q < nw; ++q) {
+          const uint32_t k = K1.xcap - 1 - q;
+          if (pw + q < cap) Wl[pw + q] = SeqIv{x[2 * k], x[2 * k + 1], i, 0};
+        }
+        s_flags[i] = fl;
+        continue;
+      }
+    }
+    const picker_rec_t r = load_rec(B.rec + w0 + i);
     const uint32_t kid = r.kernel_id;
-    do {
+    if (status == kEvaluable) do {
       if (kid >= T.nkernel_slots || T.kernels[kid].shortcut == V_ERR_KERNEL) {
         status = V_ERR_KERNEL;
         break;
@@ -214,7 +247,8 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
 
 __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch B, uint64_t n, uint32_t window,
                                                               uint32_t mode, uint8_t* __restrict__ scratch,
-                                                              uint64_t slice, uint32_t cap, uint8_t* __restrict__ out) {
+                                                              uint64_t slice, uint32_t cap, uint8_t* __restrict__ out,
+                                                              const SeqK1 K1) {
   // per-CTA slice: reads [cap], writes [cap], sort buffer [2 cap], prefix maxima [2 cap]
   SeqIv* Rl = reinterpret_cast<SeqIv*>(scratch + blockIdx.x * slice);
   SeqIv* Wl = Rl + cap;
@@ -224,7 +258,7 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch 
   for (uint64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
     const uint64_t w0 = w * window;
     const uint32_t m = (uint32_t)min((uint64_t)window, n - w0);
-    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap);
+    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap, K1);
     if (threadIdx.x == 0) out[w] = code;
     __syncthreads();  // the slice and the shared state are reused by the next window
   }
@@ -232,7 +266,8 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch 
 
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
                             uint32_t max_desc, uint8_t* out, void** scratch_buf, size_t* scratch_bytes, int num_sms,
-                            cudaStream_t s, std::string& err) {
+                            cudaStream_t s, std::string& err, const uint8_t* k1_codes, const uint32_t* k1_xinfo,
+                            const int64_t* k1_xarena, uint32_t k1_xcap) {
   if (n == 0) return cudaSuccess;
   // extents per window <= window x max descriptors per kernel
   const uint32_t cap = std::max<uint32_t>(32, window * std::max<uint32_t>(max_desc, 1));
@@ -258,7 +293,9 @@ cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint
     }
     *scratch_bytes = grid * slice;
   }
-  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap, out);
+  const SeqK1 K1{k1_codes, k1_xinfo, k1_xarena, k1_xcap};
+  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap, out,
+                                                   K1);
   return cudaGetLastError();
 }
 

@@ -34,6 +34,8 @@ struct Options {
   int pipe_keys = 0;  // grouping keys of the specialised module (set by jit_build)
   int sort_ws = -1;   // sorted schedule: warp-specialised S4 (1), one warp per group (0), -1 auto
   bool models = false;  // module variant with row f3 fused into the pipelined kernel (PICKER_MODELS)
+  bool extents = false;  // module variant writing K1's extents for row f1 (PICKER_EXTENTS)
+  bool seq_k1 = true;    // picker_validate_sequence on K1's extents when the summary allows it
   // summaries whose evaluating kernels are all wide: the K2 persistent kernel
   // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
   int wide_kernel = -1;
@@ -58,7 +60,7 @@ struct JitPlan {
   int nshapes = 0;
 };
 JitPlan jit_plan(const std::vector<IrKernel>& ks, bool stride, bool sorted = false, bool sort_ws = false,
-                 int loop_min = 6, bool models = false);
+                 int loop_min = 6, bool models = false, bool extents = false);
 bool jit_is_stride(const JitModule* m);
 // Kernel launches one picker_validate_batch of n records makes on the module.
 int jit_launch_count(const JitModule* m, uint64_t n);
@@ -70,6 +72,8 @@ bool jit_small_path(const JitModule* m, uint64_t n);
 // pipelined kernel (not the small-batch kernel, the bucket kernel or the
 // sorted schedule, which carry no model code).
 bool jit_fused_models(const JitModule* m, uint64_t n);
+// An extents module (Options.extents) whose launch for n records is its pipelined kernel.
+bool jit_extents_ok(const JitModule* m, uint64_t n);
 cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags,
                        uint32_t* bits, unsigned long long* counts, int num_sms, cudaStream_t s);
 // Row f3 accumulator of a context: zero it on `s` / copy it to `out` and sync.
@@ -99,7 +103,9 @@ inline bool use_wide_kernel(const Options& o) { return o.wide_only && o.wide_ker
 // device buffers owned by the caller's context, grown / allocated here.
 cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint32_t window, uint32_t mode,
                             uint32_t max_desc, uint8_t* out, void** scratch, size_t* scratch_bytes, int num_sms,
-                            cudaStream_t s, std::string& err);
+                            cudaStream_t s, std::string& err, const uint8_t* k1_codes = nullptr,
+                            const uint32_t* k1_xinfo = nullptr, const int64_t* k1_xarena = nullptr,
+                            uint32_t k1_xcap = 0);
 
 cudaError_t launch_models(const Tables& T, const DevBatch& b, uint64_t n, const uint8_t* codes,
                           const uint64_t* ctx_bytes, uint64_t kill_ns, uint64_t save_bpu, picker_model_out_t* out,

@@ -100,6 +100,21 @@ static __device__ __noinline__ bool model_input_bytes_coded(const Tables& T, con
   return of ? model_read_union_big(T, K, X, bytes) : false;
 }
 
+// Row f1 on K1's extents (picker_validate_sequence with an extents module):
+// the specialised shapes put every active non-opaque extent of a record into
+// its `cap` arena slots (reads from the front, writes from the back) and the
+// activity / opaque flags into fl (1 act_r, 2 act_w, 4 opq_r, 8 opq_w).
+struct XOut {
+  int64_t* ext;  // 2 x cap int64 (lb, ub) per record
+  uint32_t cap, nr, nw, fl;
+};
+__device__ __forceinline__ void xo_put(XOut& x, bool write, int64_t lb, int64_t ub) {
+  const uint32_t k = write ? x.cap - 1 - x.nw++ : x.nr++;
+  x.ext[2 * k] = lb, x.ext[2 * k + 1] = ub;
+}
+// xinfo word of a record: nr | nw << 11 | fl << 22 (cap <= 2047)
+__device__ __forceinline__ uint32_t xo_info(const XOut& x) { return x.nr | x.nw << 11 | x.fl << 22; }
+
 // Per-thread sums of the models and their addition to the global accumulator.
 struct ModelSums {
   unsigned long long n_idem, all, ni, unk, pw, pi;

@@ -35,6 +35,9 @@ struct picker_ctx {
   size_t seq_scratch_bytes = 0;
   void* model_acc = nullptr;         // row f3 accumulator
   JitModule* jit_models = nullptr;   // the specialised module with row f3 fused (built on first use)
+  JitModule* jit_extents = nullptr;  // ... writing K1's extents for row f1 (built on first use)
+  void* seq_arena = nullptr;         // row f1: K1's verdicts, extent slots and info words
+  size_t seq_arena_bytes = 0;
   cudaStream_t aux = nullptr;
   void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
   size_t wide_scratch_bytes = 0;
@@ -142,6 +145,8 @@ void picker_destroy(picker_ctx_t* c) {
     if (c->seq_scratch) cudaFree(c->seq_scratch);
     if (c->model_acc) cudaFree(c->model_acc);
     jit_destroy(c->jit_models);
+    jit_destroy(c->jit_extents);
+    if (c->seq_arena) cudaFree(c->seq_arena);
     for (int i = 0; i < 2; ++i)
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
@@ -175,6 +180,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sort_warps") c->opt.sort_warps = (int)v;  // tuning: warps per CTA of the sorted schedule
   else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
   else if (k == "loop_min") c->opt.loop_min = (int)v;  // tuning: loop classes of the specialised module
+  else if (k == "seq_k1") c->opt.seq_k1 = v != 0;  // row f1 on K1's extents (1, default) or the tables (0)
   else if (k == "wide_kernel") c->opt.wide_kernel = v < 0 ? -1 : (int)(v != 0);  // K2 kernel (k_wide.cu)
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
@@ -252,6 +258,8 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   jit_destroy(c->jit);
   jit_destroy(c->jit_models);
   c->jit_models = nullptr;
+  jit_destroy(c->jit_extents);
+  c->jit_extents = nullptr;
   c->jit = jm;
   c->dev_tables = dev;
   c->dev_tables_bytes = blob.size();
@@ -526,8 +534,50 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
   DevGuard g(c->device);
   DevBatch db{b->rec, b->args, 0, b->args_len};
   std::string err;
+  cudaStream_t s = (cudaStream_t)stream;
+  // Reuse K1's extents: a specialised module built with
+  // PICKER_EXTENTS writes each record's verdict and active extents, the window
+  // kernel reads them instead of evaluating the tables per record.  Specialised
+  // kernels only (no table-path or wide kernel), n > 1024, arena <= 8 GB.
+  bool k1 = c->jit && c->opt.seq_k1 && !c->opt.stride && n > kSmallMax && max_desc <= 2047;
+  for (auto& k : c->ir) k1 &= k.path != PATH_WIDE && k.path != PATH_GENERIC;
+  const size_t slot_b = (size_t)max_desc * 16, need = (size_t)n * (slot_b + 5) + 512;
+  k1 &= need <= (8ull << 30);
+  if (k1 && !c->jit_extents) {
+    Options mo = c->opt;
+    mo.extents = true;
+    mo.sorted = 0;  // the extents are written by the pipelined kernel
+    c->jit_extents = jit_build(c->ir, mo, err);
+    if (!c->jit_extents) return fail(c, PICKER_ECUDA, "JIT (extents): " + err);
+  }
+  if (k1 && jit_extents_ok(c->jit_extents, n)) {
+    if (c->seq_arena_bytes < need) {
+      cudaError_t e = cudaStreamSynchronize(s);  // a previous call may still use the old arena
+      if (c->seq_arena) cudaFree(c->seq_arena);
+      c->seq_arena = nullptr;
+      c->seq_arena_bytes = 0;
+      if (e != cudaSuccess || cudaMalloc(&c->seq_arena, need) != cudaSuccess) {
+        c->seq_arena = nullptr;
+        return fail(c, PICKER_ENOMEM, "cudaMalloc(extent arena) failed");
+      }
+      c->seq_arena_bytes = need;
+    }
+    uint8_t* base = (uint8_t*)c->seq_arena;
+    int64_t* xarena = (int64_t*)base;
+    uint32_t* xinfo = (uint32_t*)(base + (size_t)n * slot_b);
+    uint8_t* codes = (uint8_t*)(xinfo + n);
+    BucketParams P = c->P;
+    P.xarena = xarena, P.xinfo = xinfo, P.xcap = max_desc;
+    cudaError_t e = launch_jit(c->jit_extents, P, db, n, codes, nullptr, nullptr, c->num_sms, s);
+    if (e == cudaSuccess)
+      e = launch_sequence(c->P.T, db, n, window, mode, max_desc, out, &c->seq_scratch, &c->seq_scratch_bytes,
+                          c->num_sms, s, err, codes, xinfo, xarena, max_desc);
+    if (e != cudaSuccess) return cuda_fail(c, e, ("sequence (K1 extents): " + err).c_str());
+    c->last_launches = 2;
+    return PICKER_OK;
+  }
   cudaError_t e = launch_sequence(c->P.T, db, n, window, mode, max_desc, out, &c->seq_scratch, &c->seq_scratch_bytes,
-                                  c->num_sms, (cudaStream_t)stream, err);
+                                  c->num_sms, s, err);
   if (e != cudaSuccess) return cuda_fail(c, e, ("sequence: " + err).c_str());
   c->last_launches = n ? 1 : 0;
   return PICKER_OK;

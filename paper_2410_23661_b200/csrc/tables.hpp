@@ -232,6 +232,11 @@ struct BucketParams {
   unsigned long long kill_ns;
   ModelDiv save_bpu;           // divisor of the context-save latency (save_bytes_per_us)
   ModelAcc* model_acc;
+  // row f1 on K1's extents (module built with PICKER_EXTENTS): per record
+  // xcap extent slots (2 int64 each) and one info word (models.cuh XOut)
+  int64_t* xarena;
+  uint32_t* xinfo;
+  uint32_t xcap;
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads

@@ -164,18 +164,22 @@ def test_gpu_sequence_golden_opaque(concurrent):
 @pytest.mark.gpu
 @pytest.mark.parametrize("window", [32, 1024])
 @pytest.mark.parametrize("concurrent", [False, True])
-def test_gpu_sequence_c2(window, concurrent):
+@pytest.mark.parametrize("k1", [True, False], ids=["k1_extents", "tables"])
+def test_gpu_sequence_c2(window, concurrent, k1):
     """The C2 trace (547 kernels) cut into windows of 32 / 1024 launches: every
     window's code against oracle_windows (sort + sweep passes vs the plain
-    pairwise definition)."""
+    pairwise definition) -- on K1's verdicts and extents (the specialised
+    kernels write them, the window kernel reads them: 2 launches) and on the
+    tables (1 launch)."""
     import paper_2410_23661_b200 as pk
     from tracegen import workloads
     s, rec, args, _ = workloads.make_c2()
     mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
     want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
-    p = pk.Picker(0)
+    p = pk.Picker(0, seq_k1=int(k1))
     p.load(s)
     got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
+    assert p.last_launch_count() == (2 if k1 else 1)
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
     assert len(set(want.tolist())) > 2
