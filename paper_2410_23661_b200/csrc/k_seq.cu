@@ -158,6 +158,26 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
   // 3. overlap passes
   const uint32_t nr = s_nr, nw = s_nw;
   if (nr == 0 || nw == 0) return V_IDEM_CHECKED;
+  if ((uint64_t)nr * nw <= 256ull * blockDim.x) {
+    // few extents (C2 windows of 32: ~70 x 40): every (read, write) pair, the
+    // predicate the passes below decide -- a read of i and a write of j share a
+    // byte, sequential i <= j, concurrent any i, j -- without their sorts and
+    // barriers
+    bool hit = false;
+    for (uint32_t x = tid; x < nr && !hit; x += blockDim.x) {
+      const SeqIv r = Rl[x];
+      for (uint32_t y = 0; y < nw; ++y) {
+        const SeqIv w = Wl[y];  // the same element for every thread: one broadcast
+        if ((mode == 1 || r.inst <= w.inst) && r.lb <= w.ub && w.lb <= r.ub) {
+          hit = true;
+          break;
+        }
+      }
+    }
+    if (hit) s_hit = 1;
+    __syncthreads();
+    return s_hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
+  }
   uint32_t levels = 0;
   while ((1u << levels) < m) ++levels;
   // pass p: mode 1 -> one pass (node 0); mode 0 -> p = levels .. 0: p == levels is
