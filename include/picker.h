@@ -283,7 +283,16 @@ int picker_kernel_info(picker_ctx_t* ctx, uint32_t* ids_out, uint8_t* path_out, 
  *                  COND kernels average more than 8 descriptors)
  *   "wide_pairs"   R*W pair count above which a kernel uses the wide path
  *   "force_path"   0 = automatic, 1 = generic, 2 = jit, 3 = wide
- *   "tile", "threads", "ctas", "args_per_rec"   specialised kernel geometry
+ *   "tile", "threads", "ctas", "args_per_rec", "arg_bufs"   specialised kernel
+ *                  geometry (0 tile = chosen from the summaries)
+ *   "sorted", "sort_warps", "sort_slot", "sort_ws"   shape-sorted schedule of
+ *                  many-argument summaries (-1 / 0 = automatic)
+ *   "loop_min"     streamed descriptors from which a specialised shape loops
+ *                  over classes of descriptors (default 6)
+ *   "wide_kernel"  summaries whose evaluating kernels are all wide: the K2
+ *                  persistent kernel (-1 default / 1) or the module's schedules (0)
+ *   "seq_k1"       picker_validate_sequence on K1's verdicts and extents (1,
+ *                  default, where the summary allows it) or on the tables (0)
  * Semantic key (takes effect at the next picker_validate_batch[_host]):
  *   "stride"       1 = stride-aware ranges (reading Q24 of
  *                  DESIGN.md): a read/write pair whose byte intervals intersect
