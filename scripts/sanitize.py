@@ -49,3 +49,28 @@ q = p.validate_sequence(rec[:500], args, 8).cpu().numpy()
 assert (q == np.array(O.oracle_windows(s, rec[:500], args, 8), np.uint8)).all()
 print("exact + sequence ok", flush=True)
 torch.cuda.synchronize()
+# round 2, session 3: the K2 kernel (wide-only summary), the fused models and
+# K1's extents for the windows (64-record tiles: many tiles per CTA)
+sw, rw, aw, _ = workloads.make_wide(n=150)
+ww = np.array(O.oracle_batch(sw, rw, aw), np.uint8)
+p = pk.Picker(0)
+p.load(sw)
+f, _, _ = p.validate(rw, aw)
+assert p.last_launch_count() == 1 and (f.cpu().numpy() == ww).all()
+p.close()
+print("K2 kernel ok", flush=True)
+s2, r2, a2, _ = workloads.make_c2()
+w2 = np.array(O.oracle_batch_mp(s2, r2, a2), np.uint8)
+ctx = (np.arange(len(r2), dtype=np.uint64) % 97 + 1) * 4096
+p = pk.Picker(0, tile=64, threads=64, ctas=1, args_per_rec=4, arg_bufs=1)
+p.load(s2)
+(f, _, _), m = p.validate_models(r2, a2, ctx)
+assert p.last_launch_count() == 1 and (f.cpu().numpy() == w2).all()
+assert m == O.oracle_models(s2, r2, a2, w2, ctx)
+print("fused models ok", flush=True)
+q = p.validate_sequence(r2, a2, 32).cpu().numpy()
+assert p.last_launch_count() == 2
+assert (q == np.array(O.oracle_windows(s2, r2, a2, 32), np.uint8)).all()
+print("windows on K1 extents ok", flush=True)
+p.close()
+torch.cuda.synchronize()

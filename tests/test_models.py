@@ -167,9 +167,10 @@ def test_gpu_validate_models_random(seed):
 
 @pytest.mark.gpu
 def test_gpu_validate_models_c2_fused():
-    """C2 and C2 x 8 (the fused kernel's steady state, >= 3 tiles per CTA): one
-    launch; verdicts = the oracle's (tiled), models = the oracle's on the base
-    trace times 8 (copies are the same instances relocated)."""
+    """C2 and C2 x 24 (the fused kernel's steady state, >= 2 tiles per CTA):
+    one launch; verdicts = the oracle's (tiled), models = the oracle's on the
+    base trace times 24 (copies are the same instances relocated, SURVEY §8E G9);
+    and the base trace on 64-record tiles (~2 tiles per CTA of 148)."""
     import paper_2410_23661_b200 as pk
     from tracegen import workloads
     s, rec, args, meta = workloads.make_c2()
@@ -182,12 +183,19 @@ def test_gpu_validate_models_c2_fused():
     assert p.last_launch_count() == 1
     assert np.array_equal(flags.cpu().numpy(), codes)
     assert got == want
-    R = 8
+    R = 24  # 437 K records: >= 2 tiles of 640 per CTA of the models module
     rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
     (flags, _, _), got = p.validate_models(rec_t, args_t, np.tile(ctx, R))
     assert np.array_equal(flags.cpu().numpy(), np.tile(codes, R))
     want_t = {k: (v * R if isinstance(v, int) else [x * R for x in v]) for k, v in want.items()}
     assert got == want_t
+    p.close()
+    p = pk.Picker(0, tile=64, threads=64, ctas=1, args_per_rec=4, arg_bufs=1)
+    p.load(s)
+    (flags, _, _), got = p.validate_models(rec, args, ctx)
+    assert p.last_launch_count() == 1
+    assert np.array_equal(flags.cpu().numpy(), codes)
+    assert got == want
 
 
 @pytest.mark.gpu
