@@ -948,7 +948,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes + 1;
   m->smem = m->nkeys <= kPipeKeysMax ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
-                                                        (uint32_t)opt.arg_bufs)
+                                                        (uint32_t)opt.arg_bufs, opt.models)
                                   : bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {
     err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";

@@ -458,12 +458,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   ModelSums ms{};
   if (kModels)
     for (int b = tid; b < 2 * PICKER_MODEL_HIST; b += kThreads) s_mh[b] = 0;
-  // one record's models: input bytes from its verdict, context-save latency
-  auto model = [&](uint64_t gi, uint32_t code, const picker_rec_t& r, const int64_t* a) {
+  // models: each record's input bytes (kInbUnknown: unknown) go to s_inb where
+  // its verdict is decided; the emit adds the models of 32 records in order
+  // (full warps, coalesced context sizes)
+  uint64_t* s_inb = reinterpret_cast<uint64_t*>(
+      ((uintptr_t)(reinterpret_cast<uint8_t*>(s_perm + kTile) + 2 * kTile) + 7) & ~(uintptr_t)7);  // [2][kTile]
+  auto inb_table = [&](uint32_t code, const picker_rec_t& r, const int64_t* a) -> uint64_t {
     uint64_t b = 0;
-    const bool known = model_input_bytes_coded(P.T, r, a, code, b);
-    model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, code, known, b, P.ctx_bytes ? P.ctx_bytes[gi] : 0, P.kill_ns,
-              P.save_bpu);
+    return model_input_bytes_coded(P.T, r, a, code, b) ? b : kInbUnknown;
   };
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t G = gridDim.x;
@@ -538,7 +540,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
         s_code[buf * kTile + i] = (uint8_t)dc;
         if constexpr (kModels) {  // (the arguments of tile + 1 are not staged yet: global)
           const picker_rec_t r = rec_from_smem(hdr + 32 * i);
-          model(tile * kTile + i, dc, r, B.args + r.arg_off);
+          s_inb[buf * kTile + i] = dc == V_IDEM_KERNEL ? inb_table(dc, r, B.args + r.arg_off) : kInbUnknown;
         }
         key[q] = 0xFFu;
       }
@@ -568,6 +570,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const int hb = valid ? count_bin((uint8_t)c) : 16;
       const unsigned same = __match_any_sync(0xffffffffu, hb);
       if (valid && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
+      if constexpr (kModels)
+        if (valid) {
+          const uint64_t inb = s_inb[buf * kTile + i];
+          model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, c, inb != kInbUnknown, inb,
+                    P.ctx_bytes ? P.ctx_bytes[base + i] : 0, P.kill_ns, P.save_bpu);
+        }
     }
   };
 
@@ -663,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           const uint8_t cw = eval_wide_warp(P.T, r, a, B.args_lo, B.args_hi, lane, wide_scratch(P, warp));
           if (lane == 0) s_code[buf * kTile + wi] = cw;
           if constexpr (kModels)
-            if (lane == 0) model(base + wi, cw, r, a);
+            if (lane == 0) s_inb[buf * kTile + wi] = inb_table(cw, r, a);
         }
         continue;
       }
@@ -685,12 +693,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           uint64_t inb = kInbUnknown;
           const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B, &inb);
           s_code[buf * kTile + li] = code;
-          if (inb == kInbTable) {
-            model(base + li, code, r, a);
-          } else {
-            model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, code, inb != kInbUnknown, inb,
-                      P.ctx_bytes ? P.ctx_bytes[base + li] : 0, P.kill_ns, P.save_bpu);
-          }
+          s_inb[buf * kTile + li] = inb == kInbTable ? inb_table(code, r, a) : inb;
         } else if constexpr (kExtents) {
           XOut xo{P.xarena + (base + li) * 2 * P.xcap, P.xcap, 0, 0, 0};
           const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B, &xo);

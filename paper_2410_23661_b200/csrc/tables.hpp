@@ -288,9 +288,11 @@ constexpr uint32_t kSmallMax = 1024, kSmallThreads = 256;
 #define PICKER_ARG_BUFS 2
 #endif
 constexpr int kArgBufs = PICKER_ARG_BUFS;  // 1 or 2 argument staging buffers (pipelined kernel)
-constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint32_t arg_bufs = 2) {
+// (models: + the input bytes of two tiles, u64 per record, for the emit)
+constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint32_t arg_bufs = 2,
+                                     bool models = false) {
   return (size_t)2 * tile * 32 + (size_t)arg_bufs * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 +
-         128;
+         128 + (models ? (size_t)2 * tile * 8 + 8 : 0);
 }
 
 // K2 scratch (desc_eval.cuh): descriptors per kernel sorted in the warp's
