@@ -57,17 +57,35 @@ struct SeqK1 {
   uint32_t xcap;
 };
 
-// One window: returns its code (CTA-uniform).
+// The threads deciding one window: a CTA (any window size) or one warp (windows
+// of <= 32 launches, several windows per CTA), with their shared state.
+template <int F>
+struct SeqShared {
+  uint32_t first, nr, nw, ns, hit;
+  uint8_t code;
+  uint8_t flags[F];  // per instance: 1 act_r, 2 act_w, 4 opq_r, 8 opq_w
+};
+struct SeqCta {
+  SeqShared<1024>* sh;
+  int tid, size;
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct SeqWarp {
+  SeqShared<32>* sh;
+  int tid, size;
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
+
+// One window: returns its code (uniform over the group g).
+template <class Grp>
 __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, uint32_t m, uint32_t mode, SeqIv* Rl,
-                              SeqIv* Wl, SeqIv* S, int64_t* PM, uint32_t cap, const SeqK1& K1) {
-  __shared__ uint32_t s_first, s_nr, s_nw, s_ns, s_hit;
-  __shared__ uint8_t s_flags[1024];  // per instance: 1 act_r, 2 act_w, 4 opq_r, 8 opq_w
-  __shared__ uint8_t s_code;
-  const int tid = threadIdx.x;
-  if (tid == 0) s_first = 0xFFFFFFFFu, s_nr = 0, s_nw = 0, s_hit = 0;
-  __syncthreads();
+                              SeqIv* Wl, SeqIv* S, int64_t* PM, uint32_t cap, const SeqK1& K1, const Grp& g) {
+  auto& sh = *g.sh;
+  const int tid = g.tid;
+  if (tid == 0) sh.first = 0xFFFFFFFFu, sh.nr = 0, sh.nw = 0, sh.hit = 0;
+  g.sync();
   // 1. records of the window
-  for (uint32_t i = tid; i < m; i += blockDim.x) {
+  for (uint32_t i = tid; i < m; i += (uint32_t)g.size) {
     uint8_t status = kEvaluable, fl = 0;
     if (K1.codes) {
       // K1 decided the record: a code before any address decides (0xFF, 0xFE,
@@ -82,14 +100,14 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
         const uint32_t nr = info & 0x7FFu, nw = (info >> 11) & 0x7FFu;
         fl = (uint8_t)(info >> 22);
         const int64_t* x = K1.xarena + (w0 + i) * 2 * K1.xcap;
-        const uint32_t pr = nr ? atomicAdd(&s_nr, nr) : 0u, pw = nw ? atomicAdd(&s_nw, nw) : 0u;
+        const uint32_t pr = nr ? atomicAdd(&sh.nr, nr) : 0u, pw = nw ? atomicAdd(&sh.nw, nw) : 0u;
         for (uint32_t q = 0; q < nr; ++q)
           if (pr + q < cap) Rl[pr + q] = SeqIv{x[2 * q], x[2 * q + 1], i, 0};
         for (uint32_t q = 0; q < nw; ++q) {
           const uint32_t k = K1.xcap - 1 - q;
           if (pw + q < cap) Wl[pw + q] = SeqIv{x[2 * k], x[2 * k + 1], i, 0};
         }
-        s_flags[i] = fl;
+        sh.flags[i] = fl;
         continue;
       }
     }
@@ -130,41 +148,41 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
           fl |= D.kind == KIND_R ? 4 : 8;
           continue;
         }
-        const uint32_t pos = atomicAdd(D.kind == KIND_R ? &s_nr : &s_nw, 1u);
+        const uint32_t pos = atomicAdd(D.kind == KIND_R ? &sh.nr : &sh.nw, 1u);
         if (pos < cap) (D.kind == KIND_R ? Rl : Wl)[pos] = SeqIv{lb, ub, i, 0};
       }
     } while (false);
-    s_flags[i] = fl;
-    if (status != kEvaluable) atomicMin(&s_first, (i << 8) | status);
+    sh.flags[i] = fl;
+    if (status != kEvaluable) atomicMin(&sh.first, (i << 8) | status);
   }
-  __syncthreads();
+  g.sync();
   // the first decisive record (launch order) decides the window
-  if (s_first != 0xFFFFFFFFu) return (uint8_t)(s_first & 0xFF);
+  if (sh.first != 0xFFFFFFFFu) return (uint8_t)(sh.first & 0xFF);
   // 2. opaque rule
   if (tid == 0) {
     uint8_t code = kEvaluable;
     bool pre_opq_r = false, pre_act_r = false, opq_r = false, act_r = false, opq_w = false, act_w = false;
     for (uint32_t j = 0; j < m; ++j) {
-      const uint8_t f = s_flags[j];
+      const uint8_t f = sh.flags[j];
       pre_opq_r |= (f & 4) != 0, pre_act_r |= (f & 1) != 0;
       act_r |= (f & 1) != 0, act_w |= (f & 2) != 0, opq_r |= (f & 4) != 0, opq_w |= (f & 8) != 0;
       if (mode == 0 && ((pre_opq_r && (f & 2)) || (pre_act_r && (f & 8)))) code = V_NI_OPAQUE;
     }
     if (mode == 1 && ((opq_r && act_w) || (act_r && opq_w))) code = V_NI_OPAQUE;
-    s_code = code;
+    sh.code = code;
   }
-  __syncthreads();
-  if (s_code != kEvaluable) return s_code;
+  g.sync();
+  if (sh.code != kEvaluable) return sh.code;
   // 3. overlap passes
-  const uint32_t nr = s_nr, nw = s_nw;
+  const uint32_t nr = sh.nr, nw = sh.nw;
   if (nr == 0 || nw == 0) return V_IDEM_CHECKED;
-  if ((uint64_t)nr * nw <= 256ull * blockDim.x) {
+  if ((uint64_t)nr * nw <= 256ull * (uint32_t)g.size) {
     // few extents (C2 windows of 32: ~70 x 40): every (read, write) pair, the
     // predicate the passes below decide -- a read of i and a write of j share a
     // byte, sequential i <= j, concurrent any i, j -- without their sorts and
     // barriers
     bool hit = false;
-    for (uint32_t x = tid; x < nr && !hit; x += blockDim.x) {
+    for (uint32_t x = tid; x < nr && !hit; x += (uint32_t)g.size) {
       const SeqIv r = Rl[x];
       for (uint32_t y = 0; y < nw; ++y) {
         const SeqIv w = Wl[y];  // the same element for every thread: one broadcast
@@ -174,9 +192,9 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
         }
       }
     }
-    if (hit) s_hit = 1;
-    __syncthreads();
-    return s_hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
+    if (hit) sh.hit = 1;
+    g.sync();
+    return sh.hit ? V_NI_OVERLAP : V_IDEM_CHECKED;
   }
   uint32_t levels = 0;
   while ((1u << levels) < m) ++levels;
@@ -196,30 +214,30 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
       in = !((inst >> p) & 1);  // left half
       return inst >> (p + 1);
     };
-    if (tid == 0) s_ns = 0;
-    __syncthreads();
-    for (uint32_t x = tid; x < nw; x += blockDim.x) {
+    if (tid == 0) sh.ns = 0;
+    g.sync();
+    for (uint32_t x = tid; x < nw; x += (uint32_t)g.size) {
       SeqIv w = Wl[x];
       bool in;
       w.node = wnode(w.inst, in);
-      if (in) S[atomicAdd(&s_ns, 1u)] = w;
+      if (in) S[atomicAdd(&sh.ns, 1u)] = w;
     }
-    __syncthreads();
-    const uint32_t ns = s_ns;
+    g.sync();
+    const uint32_t ns = sh.ns;
     if (ns == 0) continue;
     uint32_t n2 = 32;
     while (n2 < ns) n2 <<= 1;
-    for (uint32_t x = ns + tid; x < n2; x += blockDim.x)
+    for (uint32_t x = ns + tid; x < n2; x += (uint32_t)g.size)
       S[x] = SeqIv{9223372036854775807LL, (-9223372036854775807LL - 1), 0, 0xFFFFFFFFu};  // sorts last
-    __syncthreads();
+    g.sync();
     for (uint32_t k = 2; k <= n2; k <<= 1)  // bitonic sort by (node, lb)
       for (uint32_t j = k >> 1; j > 0; j >>= 1) {
-        for (uint32_t q = tid; q < n2 / 2; q += blockDim.x) {
+        for (uint32_t q = tid; q < n2 / 2; q += (uint32_t)g.size) {
           const uint32_t i = ((q & ~(j - 1)) << 1) | (q & (j - 1)), o = i | j;
           const SeqIv a = S[i], b = S[o];
           if (((i & k) == 0) ? seq_less(b, a) : seq_less(a, b)) S[i] = b, S[o] = a;
         }
-        __syncthreads();
+        g.sync();
       }
     if (tid < 32) {  // prefix maxima of ub within each node segment (one warp, carried)
       const int lane = tid;
@@ -241,8 +259,8 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
         carry_node = __shfl_sync(0xffffffffu, e.node, 31);
       }
     }
-    __syncthreads();
-    for (uint32_t x = tid; x < nr && !s_hit; x += blockDim.x) {
+    g.sync();
+    for (uint32_t x = tid; x < nr && !sh.hit; x += (uint32_t)g.size) {
       const SeqIv r = Rl[x];
       bool in;
       const uint32_t node = rnode(r.inst, in);
@@ -257,10 +275,10 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
         const SeqIv& c = S[lo + 1];
         if (c.node < node || (c.node == node && c.lb <= r.ub)) ++lo;
       }
-      if (lo >= 0 && S[lo].node == node && PM[lo] >= r.lb) s_hit = 1;
+      if (lo >= 0 && S[lo].node == node && PM[lo] >= r.lb) sh.hit = 1;
     }
-    __syncthreads();
-    if (s_hit) return V_NI_OVERLAP;
+    g.sync();
+    if (sh.hit) return V_NI_OVERLAP;
   }
   return V_IDEM_CHECKED;
 }
@@ -270,6 +288,8 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch 
                                                               uint64_t slice, uint32_t cap, uint8_t* __restrict__ out,
                                                               const SeqK1 K1) {
   // per-CTA slice: reads [cap], writes [cap], sort buffer [2 cap], prefix maxima [2 cap]
+  __shared__ SeqShared<1024> sh;
+  const SeqCta grp{&sh, (int)threadIdx.x, (int)blockDim.x};
   SeqIv* Rl = reinterpret_cast<SeqIv*>(scratch + blockIdx.x * slice);
   SeqIv* Wl = Rl + cap;
   SeqIv* S = Wl + cap;
@@ -278,9 +298,35 @@ __global__ void __launch_bounds__(kSeqThreads) k_seq_windows(Tables T, DevBatch 
   for (uint64_t w = blockIdx.x; w < nwin; w += gridDim.x) {
     const uint64_t w0 = w * window;
     const uint32_t m = (uint32_t)min((uint64_t)window, n - w0);
-    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap, K1);
+    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap, K1, grp);
     if (threadIdx.x == 0) out[w] = code;
     __syncthreads();  // the slice and the shared state are reused by the next window
+  }
+}
+
+// Windows of <= 32 launches: one warp per window, 8 windows per CTA at a time
+// (a CTA per window of 32 threads was capped at 32 warps per SM by the CTA
+// limit); each warp has its own scratch slice and shared state.
+constexpr int kSeqWarps = 8;
+__global__ void __launch_bounds__(kSeqWarps * 32) k_seq_windows_w(Tables T, DevBatch B, uint64_t n, uint32_t window,
+                                                                 uint32_t mode, uint8_t* __restrict__ scratch,
+                                                                 uint64_t slice, uint32_t cap,
+                                                                 uint8_t* __restrict__ out, const SeqK1 K1) {
+  __shared__ SeqShared<32> sh[kSeqWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint64_t gw = (uint64_t)blockIdx.x * kSeqWarps + warp, nwarps = (uint64_t)gridDim.x * kSeqWarps;
+  const SeqWarp grp{&sh[warp], lane, 32};
+  SeqIv* Rl = reinterpret_cast<SeqIv*>(scratch + gw * slice);
+  SeqIv* Wl = Rl + cap;
+  SeqIv* S = Wl + cap;
+  int64_t* PM = reinterpret_cast<int64_t*>(S + 2 * (uint64_t)cap);
+  const uint64_t nwin = (n + window - 1) / window;
+  for (uint64_t w = gw; w < nwin; w += nwarps) {
+    const uint64_t w0 = w * window;
+    const uint32_t m = (uint32_t)min((uint64_t)window, n - w0);
+    const uint8_t code = seq_window(T, B, w0, m, mode, Rl, Wl, S, PM, cap, K1, grp);
+    if (lane == 0) out[w] = code;
+    __syncwarp();  // the slice and the shared state are reused by the next window
   }
 }
 
@@ -295,27 +341,35 @@ cudaError_t launch_sequence(const Tables& T, const DevBatch& b, uint64_t n, uint
   const uint64_t nwin = (n + window - 1) / window;
   // a thread per record of a window (32..512 threads per CTA), as many CTAs as
   // fill the SMs (2048 threads each), within ~1 GB of scratch
-  const uint32_t threads = std::min<uint32_t>(kSeqThreads, (window + 31) / 32 * 32);
-  uint64_t grid = std::min<uint64_t>(nwin, (uint64_t)num_sms * (2048 / threads));
-  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (1ULL << 30) / slice));
+  // (windows of <= 32 launches: a warp per window, kSeqWarps windows per CTA)
+  const bool per_warp = window <= 32;
+  const uint32_t threads = per_warp ? kSeqWarps * 32 : std::min<uint32_t>(kSeqThreads, (window + 31) / 32 * 32);
+  const uint64_t units_per_cta = per_warp ? kSeqWarps : 1;
+  uint64_t grid = std::min<uint64_t>((nwin + units_per_cta - 1) / units_per_cta, (uint64_t)num_sms * (2048 / threads));
+  grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (1ULL << 30) / (slice * units_per_cta)));
+  const uint64_t slices = grid * units_per_cta;
   // the slices are owned by the caller's context, grown on demand (a per-call
   // stream-ordered allocation made the timing depend on the pool's state)
-  if (*scratch_bytes < grid * slice) {
+  if (*scratch_bytes < slices * slice) {
     cudaError_t e = cudaStreamSynchronize(s);  // a previous call may still use the old buffer
     if (e == cudaSuccess && *scratch_buf) e = cudaFree(*scratch_buf);
     *scratch_buf = nullptr;
     *scratch_bytes = 0;
-    if (e == cudaSuccess) e = cudaMalloc(scratch_buf, grid * slice);
+    if (e == cudaSuccess) e = cudaMalloc(scratch_buf, slices * slice);
     if (e != cudaSuccess) {
       *scratch_buf = nullptr;
       err = "scratch allocation";
       return e;
     }
-    *scratch_bytes = grid * slice;
+    *scratch_bytes = slices * slice;
   }
   const SeqK1 K1{k1_codes, k1_xinfo, k1_xarena, k1_xcap};
-  k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap, out,
-                                                   K1);
+  if (per_warp)
+    k_seq_windows_w<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap,
+                                                       out, K1);
+  else
+    k_seq_windows<<<(unsigned)grid, threads, 0, s>>>(T, b, n, window, mode, (uint8_t*)*scratch_buf, slice, cap, out,
+                                                     K1);
   return cudaGetLastError();
 }
 
