@@ -51,6 +51,7 @@ struct JitModule {
   bool pipe = false;                    // main kernel is k_validate_pipe (<= kPipeKeysMax keys)
   bool models = false;                  // built with PICKER_MODELS (row f3 fused)
   bool extents = false;                 // built with PICKER_EXTENTS (row f1 on K1's extents)
+  uint32_t seq_xcap = 0;                // ... with the tile's extent slots in shared memory
   size_t smem = 0;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
@@ -890,6 +891,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->pipe = plan.src.find("k_validate_pipe<JitDispatch>") != std::string::npos;
   m->models = opt.models;
   m->extents = opt.extents;
+  m->seq_xcap = opt.extents ? (uint32_t)opt.seq_xcap : 0u;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   std::vector<std::string> names;  // main, small, [the sorted schedule's kernels]
   for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
@@ -948,7 +950,8 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   }
   m->nkeys = SHAPE_FIRST + (uint32_t)plan.nshapes + 1;
   m->smem = m->nkeys <= kPipeKeysMax ? pipe_smem_bytes_for((uint32_t)opt.tile, (uint32_t)opt.args_per_rec,
-                                                        (uint32_t)opt.arg_bufs, opt.models)
+                                                        (uint32_t)opt.arg_bufs, opt.models,
+                                                        opt.extents ? (uint32_t)opt.seq_xcap : 0u)
                                   : bucket_smem_bytes_for(m->nkeys, (uint32_t)opt.tile, (uint32_t)opt.args_per_rec);
   if (m->smem > kMaxSmem) {
     err = "shared memory of the specialised kernel exceeds 227 KB (lower tile / args_per_rec)";
@@ -984,6 +987,9 @@ bool jit_fused_models(const JitModule* m, uint64_t n) {
 }
 bool jit_extents_ok(const JitModule* m, uint64_t n) {
   return m && m->extents && m->pipe && !m->sk[3] && !jit_small_path(m, n);
+}
+bool jit_seq_fused(const JitModule* m, uint64_t n, uint32_t window) {
+  return jit_extents_ok(m, n) && m->seq_xcap && m->nkeys <= kPipeKeysMax && window <= 32 && m->tile % window == 0;
 }
 
 int jit_launch_count(const JitModule* m, uint64_t n) {

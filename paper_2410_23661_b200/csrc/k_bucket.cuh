@@ -32,6 +32,7 @@
 #include "desc_eval.cuh"
 #include "eval_generic.cuh"
 #include "models.cuh"
+#include "seq.cuh"
 
 namespace picker {
 
@@ -467,6 +468,27 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     uint64_t b = 0;
     return model_input_bytes_coded(P.T, r, a, code, b) ? b : kInbUnknown;
   };
+  // extents with P.seq_out (row f1 fused): the tile's extent slots and info
+  // words stay in shared memory (same place as s_inb; the two modes are
+  // exclusive), and the windows of tile t are decided in the emit slot of
+  // t + 1, a warp per window (seq.cuh)
+  const bool seq_fused = kExtents && P.seq_out != nullptr;
+  int64_t* s_ext = reinterpret_cast<int64_t*>(
+      ((uintptr_t)(reinterpret_cast<uint8_t*>(s_perm + kTile) + 2 * kTile) + 15) & ~(uintptr_t)15);
+  uint32_t* s_xinfo = reinterpret_cast<uint32_t*>(s_ext + (size_t)kTile * 2 * P.xcap);
+  auto windows = [&](uint64_t tbase, int m, uint32_t cbuf) {
+    if constexpr (kExtents) {
+      if (!seq_fused) return;
+      const uint32_t W = P.seq_window, nwin = ((uint32_t)m + W - 1) / W;
+      for (uint32_t w = warp; w < nwin; w += kWarps) {
+        const uint32_t i0 = w * W;
+        const uint8_t code = seq_window_lanes(P.T, B, tbase + i0, min(W, (uint32_t)m - i0), P.seq_mode,
+                                              s_code + cbuf * kTile + i0, s_xinfo + i0,
+                                              s_ext + (size_t)i0 * 2 * P.xcap, P.xcap, lane);
+        if (lane == 0) P.seq_out[(tbase + i0) / W] = code;
+      }
+    }
+  };
   const uint64_t ntiles = (n + kTile - 1) / kTile;
   const uint64_t G = gridDim.x;
   if (tid < PICKER_NUM_COUNTS) s_hist[tid] = 0;
@@ -565,7 +587,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       const bool valid = i < m;
       const uint32_t c = valid ? s_code[buf * kTile + i] : 0u;
       const unsigned idem = __ballot_sync(0xffffffffu, valid && c <= V_IDEM_KERNEL);
-      if (valid) flags[base + i] = (uint8_t)c;
+      if (valid && flags != nullptr) flags[base + i] = (uint8_t)c;
       if (bits != nullptr && lane == 0) bits[(base + i0) >> 5] = idem;
       const int hb = valid ? count_bin((uint8_t)c) : 16;
       const unsigned same = __match_any_sync(0xffffffffu, hb);
@@ -590,7 +612,10 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     // single argument buffer: free now; fetch this tile's arguments, which
     // the scan / scatter / emit below overlap
     if (kArgBufs == 1 && tid == 0) stage_args(B, m, smem + buf * kHdrBytes, smem + kArgOff, &s_abar, &s_info[buf]);
-    if (it > 0) emit(base - G * kTile, kTile, buf ^ 1);  // tiles before the last are full
+    if (it > 0) {  // tiles before the last are full
+      emit(base - G * kTile, kTile, buf ^ 1);
+      windows(base - G * kTile, kTile, buf ^ 1);
+    }
     // counters and claim index of the other parity: last used before B_b of
     // t-1, next used after B_b of t
     for (int b = tid; b < (int)kPipeKeys; b += kThreads) s_cnt[buf ^ 1][b] = 0;  // CTAs of < 64 threads too
@@ -695,10 +720,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
           s_code[buf * kTile + li] = code;
           s_inb[buf * kTile + li] = inb == kInbTable ? inb_table(code, r, a) : inb;
         } else if constexpr (kExtents) {
-          XOut xo{P.xarena + (base + li) * 2 * P.xcap, P.xcap, 0, 0, 0};
+          XOut xo{seq_fused ? s_ext + (size_t)li * 2 * P.xcap : P.xarena + (base + li) * 2 * P.xcap, P.xcap, 0, 0,
+                  0};
           const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B, &xo);
           s_code[buf * kTile + li] = code;
-          P.xinfo[base + li] = xo_info(xo);
+          (seq_fused ? s_xinfo[li] : P.xinfo[base + li]) = xo_info(xo);
         } else {
           const uint8_t code = Dispatch::eval(key, pe.x >> 16, pe.y, local, P, r, a, B);
           s_code[buf * kTile + li] = code;
@@ -709,6 +735,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
     if (tile + G >= ntiles) {  // last tile of this CTA
       __syncthreads();
       emit(base, m, buf);
+      windows(base, m, buf);
     }
   }
   __syncthreads();

@@ -36,6 +36,9 @@ struct Options {
   bool models = false;  // module variant with row f3 fused into the pipelined kernel (PICKER_MODELS)
   bool extents = false;  // module variant writing K1's extents for row f1 (PICKER_EXTENTS)
   bool seq_k1 = true;    // picker_validate_sequence on K1's extents when the summary allows it
+  // extents module: extent slots per record held in shared memory for the
+  // tile (0: the module writes them to the global arena only)
+  int seq_xcap = 0;
   // summaries whose evaluating kernels are all wide: the K2 persistent kernel
   // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
   int wide_kernel = -1;
@@ -73,6 +76,10 @@ bool jit_small_path(const JitModule* m, uint64_t n);
 // sorted schedule, which carry no model code).
 bool jit_fused_models(const JitModule* m, uint64_t n);
 // An extents module (Options.extents) whose launch for n records is its pipelined kernel.
+// jit_seq_fused: ... that also decides windows of `window` launches itself from
+// the tile's extents in shared memory (Options.seq_xcap; window <= 32 dividing
+// the tile).
+bool jit_seq_fused(const JitModule* m, uint64_t n, uint32_t window);
 bool jit_extents_ok(const JitModule* m, uint64_t n);
 cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags,
                        uint32_t* bits, unsigned long long* counts, int num_sms, cudaStream_t s);

@@ -547,8 +547,33 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
     Options mo = c->opt;
     mo.extents = true;
     mo.sorted = 0;  // the extents are written by the pipelined kernel
+    // windows decided inside the kernel from the tile's extents in shared
+    // memory: the first geometry whose shared memory (with 4 KB of static
+    // state) fits its CTAs per SM; none: extents through the global arena
+    static const int geo[][4] = {{448, 448, 2, 2}, {448, 448, 2, 1}, {896, 896, 1, 1}, {224, 224, 4, 1},
+                                 {128, 128, 4, 1}};
+    if (mo.tile == 0)
+      for (auto& g : geo) {
+        const size_t sm = pipe_smem_bytes_for((uint32_t)g[0], 5, (uint32_t)g[3], false, max_desc) + 4096;
+        if ((sm + 1024) * g[2] <= 228 * 1024) {
+          mo.tile = g[0], mo.threads = g[1], mo.ctas = g[2], mo.args_per_rec = 5, mo.arg_bufs = g[3];
+          mo.seq_xcap = (int)max_desc;
+          break;
+        }
+      }
     c->jit_extents = jit_build(c->ir, mo, err);
     if (!c->jit_extents) return fail(c, PICKER_ECUDA, "JIT (extents): " + err);
+  }
+  if (k1 && jit_seq_fused(c->jit_extents, n, window)) {
+    // one launch: verdicts, extents and windows, nothing but the window codes
+    // written to global memory
+    BucketParams P = c->P;
+    P.xarena = nullptr, P.xinfo = nullptr, P.xcap = max_desc;
+    P.seq_out = out, P.seq_window = window, P.seq_mode = mode;
+    cudaError_t e = launch_jit(c->jit_extents, P, db, n, nullptr, nullptr, nullptr, c->num_sms, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "sequence (K1 fused)");
+    c->last_launches = 1;
+    return PICKER_OK;
   }
   if (k1 && jit_extents_ok(c->jit_extents, n)) {
     if (c->seq_arena_bytes < need) {

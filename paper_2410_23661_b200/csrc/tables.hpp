@@ -237,6 +237,11 @@ struct BucketParams {
   int64_t* xarena;
   uint32_t* xinfo;
   uint32_t xcap;
+  // ... and, with seq_out set, the windows decided inside the pipelined kernel
+  // from the tile's extents in shared memory (windows of seq_window <= 32
+  // launches, mode 0 sequential / 1 concurrent; tiles are a multiple of it)
+  uint8_t* seq_out;
+  uint32_t seq_window, seq_mode;
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads
@@ -288,11 +293,12 @@ constexpr uint32_t kSmallMax = 1024, kSmallThreads = 256;
 #define PICKER_ARG_BUFS 2
 #endif
 constexpr int kArgBufs = PICKER_ARG_BUFS;  // 1 or 2 argument staging buffers (pipelined kernel)
-// (models: + the input bytes of two tiles, u64 per record, for the emit)
+// (models: + the input bytes of two tiles, u64 per record, for the emit;
+// xcap > 0: + the tile's extent slots and info words of the extents module)
 constexpr size_t pipe_smem_bytes_for(uint32_t tile, uint32_t args_per_rec, uint32_t arg_bufs = 2,
-                                     bool models = false) {
+                                     bool models = false, uint32_t xcap = 0) {
   return (size_t)2 * tile * 32 + (size_t)arg_bufs * ((size_t)tile * args_per_rec * 8 + 16) + (size_t)tile * 10 +
-         128 + (models ? (size_t)2 * tile * 8 + 8 : 0);
+         128 + (models ? (size_t)2 * tile * 8 + 8 : 0) + (xcap ? (size_t)tile * (16 * xcap + 4) + 16 : 0);
 }
 
 // K2 scratch (desc_eval.cuh): descriptors per kernel sorted in the warp's

@@ -52,7 +52,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value for the C2 rows (tuning)")
-    ap.add_argument("--only", default=None, help="f3: only the f3 rows")
+    ap.add_argument("--only", default=None, help="f1 / f3: only those rows")
     a = ap.parse_args()
     peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6554.6))
     dev = torch.device("cuda", 0)
@@ -71,13 +71,17 @@ def main():
     n = rd.shape[0]
     base = 32 * n + 8 * int(ad.numel())
     # f1
-    for conc in ((False, True) if a.only is None else ()):
+    for conc in ((False, True) if a.only in (None, "f1") else ()):
         W = 32
         ms = timed(lambda: p.validate_sequence(rd, ad, W, concurrent=conc), a.steps)
         got = p.validate_sequence(rd[:len(rec)], ad, W, concurrent=conc).cpu().numpy()
         want = np.array(O.oracle_windows(s, rec, args, W, O.SEQ_CONCURRENT if conc else O.SEQ_SEQUENTIAL), np.uint8)
         row(f"f1_windows32_{'concurrent' if conc else 'sequential'}", n, base + (n + W - 1) // W, ms,
             parity_mismatches=int((got != want).sum()), windows_checked=len(want))
+    if a.only == "f1":
+        if a.out:
+            json.dump(out, open(a.out, "w"), indent=1)
+        return
     # f3
     flags, _, _ = p.validate(rd, ad)
     ctx = torch.from_numpy((np.arange(n, dtype=np.int64) % 97 + 1) * 4096).to(dev)

@@ -179,7 +179,9 @@ def test_gpu_sequence_c2(window, concurrent, k1):
     p = pk.Picker(0, seq_k1=int(k1))
     p.load(s)
     got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
-    assert p.last_launch_count() == (2 if k1 else 1)
+    # windows of 32: decided inside the extents module's kernel (1 launch);
+    # of 1024: its extents arena, then the window kernel (2)
+    assert p.last_launch_count() == (2 if k1 and window > 32 else 1)
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
     assert len(set(want.tolist())) > 2
@@ -248,3 +250,33 @@ def test_gpu_sequence_k1_tiles(concurrent):
     assert p.last_launch_count() == 2
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("concurrent", [False, True])
+def test_gpu_sequence_fused_steady(concurrent):
+    """Windows decided inside the extents module's pipelined kernel, at its
+    steady state (C2 cut to a multiple of 32 records, x 24: ~3 tiles per CTA, so
+    windows of tile t run while tile t + 1 is staged and sorted): one launch,
+    every window equal to the oracle's windows of the base trace, tiled (the
+    copies are the base instances relocated); then windows of 8
+    and 16, and a ragged last window."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, meta = workloads.make_c2()
+    mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
+    rec = rec[: len(rec) // 32 * 32]
+    R = 24
+    rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
+    p = pk.Picker(0)
+    p.load(s)
+    for window in (32, 16, 8):
+        want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
+        got = p.validate_sequence(rec_t, args_t, window, concurrent=concurrent).cpu().numpy()
+        assert p.last_launch_count() == 1
+        bad = np.nonzero(got != np.tile(want, R))[0]
+        assert bad.size == 0, (window, bad[:8], got[bad[:8]])
+    m = len(rec) - 13  # ragged: the last window has 19 launches
+    want = np.array(O.oracle_windows(s, rec[:m], args, 32, mode), np.uint8)
+    got = p.validate_sequence(rec[:m], args, 32, concurrent=concurrent).cpu().numpy()
+    assert np.array_equal(got, want)
