@@ -550,17 +550,22 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
     // windows decided inside the kernel from the tile's extents in shared
     // memory: the first geometry whose shared memory (with 4 KB of static
     // state) fits its CTAs per SM; none: extents through the global arena
-    static const int geo[][4] = {{448, 448, 2, 2}, {448, 448, 2, 1}, {896, 896, 1, 1}, {224, 224, 4, 1},
+    static const int geo[][4] = {{448, 448, 2, 1}, {896, 896, 1, 1}, {224, 224, 4, 1},
                                  {128, 128, 4, 1}};
-    if (mo.tile == 0)
-      for (auto& g : geo) {
-        const size_t sm = pipe_smem_bytes_for((uint32_t)g[0], 5, (uint32_t)g[3], false, max_desc) + 4096;
-        if ((sm + 1024) * g[2] <= 228 * 1024) {
+    auto fits = [&](int tile, int apr, int bufs, int ctas) {
+      const size_t sm = pipe_smem_bytes_for((uint32_t)tile, (uint32_t)apr, (uint32_t)bufs, false, max_desc) + 4096;
+      return (sm + 1024) * ctas <= 228 * 1024;
+    };
+    if (mo.tile == 0) {
+      for (auto& g : geo)
+        if (fits(g[0], 5, g[3], g[2])) {
           mo.tile = g[0], mo.threads = g[1], mo.ctas = g[2], mo.args_per_rec = 5, mo.arg_bufs = g[3];
           mo.seq_xcap = (int)max_desc;
           break;
         }
-      }
+    } else if (fits(mo.tile, mo.args_per_rec, mo.arg_bufs, 1)) {  // a given geometry (CTAs per SM: what fits)
+      mo.seq_xcap = (int)max_desc;
+    }
     c->jit_extents = jit_build(c->ir, mo, err);
     if (!c->jit_extents) return fail(c, PICKER_ECUDA, "JIT (extents): " + err);
   }

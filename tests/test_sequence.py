@@ -236,9 +236,10 @@ def test_gpu_sequence_wide(concurrent):
 @pytest.mark.gpu
 @pytest.mark.parametrize("concurrent", [False, True])
 def test_gpu_sequence_k1_tiles(concurrent):
-    """K1's extents written by the extents module on 64-record tiles (285 tiles
-    over 148 CTAs: the restaging / next-tile key pass paths) for the C2 trace,
-    windows of 32 against oracle_windows."""
+    """The extents module on 64-record tiles (285 tiles over 148 CTAs: the
+    restaging / next-tile key pass paths) for the C2 trace: windows of 32
+    decided in its kernel (1 launch), and windows of 24 (not dividing the
+    tile: its extents arena, then the window kernel), against oracle_windows."""
     import paper_2410_23661_b200 as pk
     from tracegen import workloads
     s, rec, args, _ = workloads.make_c2()
@@ -247,6 +248,11 @@ def test_gpu_sequence_k1_tiles(concurrent):
     p = pk.Picker(0, tile=64, threads=64, ctas=1, args_per_rec=4, arg_bufs=1)
     p.load(s)
     got = p.validate_sequence(rec, args, 32, concurrent=concurrent).cpu().numpy()
+    assert p.last_launch_count() == 1
+    bad = np.nonzero(got != want)[0]
+    assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
+    want = np.array(O.oracle_windows(s, rec, args, 24, mode), np.uint8)
+    got = p.validate_sequence(rec, args, 24, concurrent=concurrent).cpu().numpy()
     assert p.last_launch_count() == 2
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
