@@ -293,6 +293,11 @@ int picker_kernel_info(picker_ctx_t* ctx, uint32_t* ids_out, uint8_t* path_out, 
  *                  persistent kernel (-1 default / 1) or the module's schedules (0)
  *   "seq_k1"       picker_validate_sequence on K1's verdicts and extents (1,
  *                  default, where the summary allows it) or on the tables (0)
+ *   "seq_lazy"     windows of <= 32 launches decided from K1's codes, extents
+ *                  evaluated only for windows without a decisive record (1),
+ *                  always from K1's extents (0), or -1 (default): chosen by the
+ *                  context's first call (lazy when <= 1/16 of its windows need
+ *                  extents; that call synchronises its stream once)
  * Semantic key (takes effect at the next picker_validate_batch[_host]):
  *   "stride"       1 = stride-aware ranges (reading Q24 of
  *                  DESIGN.md): a read/write pair whose byte intervals intersect

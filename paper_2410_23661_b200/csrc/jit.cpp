@@ -52,6 +52,7 @@ struct JitModule {
   bool models = false;                  // built with PICKER_MODELS (row f3 fused)
   bool extents = false;                 // built with PICKER_EXTENTS (row f1 on K1's extents)
   uint32_t seq_xcap = 0;                // ... with the tile's extent slots in shared memory
+  bool seq_windows = false;             // built with PICKER_SEQ (row f1 from K1's codes)
   size_t smem = 0;
   int64_t* d_consts = nullptr;
   KbEntry* d_kb = nullptr;
@@ -774,6 +775,7 @@ std::vector<std::string> geometry_defines(const Options& opt) {
           "-DPICKER_ARG_BUFS=" + std::to_string(opt.arg_bufs),
           opt.models ? "-DPICKER_MODELS=1" : "-DPICKER_NO_MODELS=1",
           opt.extents ? "-DPICKER_EXTENTS=1" : "-DPICKER_NO_EXTENTS=1",
+          opt.seq_windows ? "-DPICKER_SEQ=1" : "-DPICKER_NO_SEQ=1",
           "-DPICKER_SORT_WARPS=" + std::to_string(std::max(1, opt.sort_warps)),
           "-DPICKER_SORT_SLOT=" + std::to_string(std::max(16, opt.sort_slot)),
           "-DPICKER_SORT_STAGES=" + std::to_string(std::max(2, opt.sort_warps)),
@@ -892,6 +894,7 @@ JitModule* jit_build(const std::vector<IrKernel>& ks, const Options& opt_in, std
   m->models = opt.models;
   m->extents = opt.extents;
   m->seq_xcap = opt.extents ? (uint32_t)opt.seq_xcap : 0u;
+  m->seq_windows = opt.seq_windows;
   cudaError_t e = cudaLibraryLoadData(&m->lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0);
   std::vector<std::string> names;  // main, small, [the sorted schedule's kernels]
   for (size_t a = 0, b; a <= lowered.size(); a = b + 1) {
@@ -990,6 +993,14 @@ bool jit_extents_ok(const JitModule* m, uint64_t n) {
 }
 bool jit_seq_fused(const JitModule* m, uint64_t n, uint32_t window) {
   return jit_extents_ok(m, n) && m->seq_xcap && m->nkeys <= kPipeKeysMax && window <= 32 && m->tile % window == 0;
+}
+bool jit_seq_lazy(const JitModule* m, uint64_t n, uint32_t window) {
+  return m && m->seq_windows && m->pipe && !m->sk[3] && !jit_small_path(m, n) && m->nkeys <= kPipeKeysMax &&
+         window <= 32 && m->tile % window == 0;
+}
+uint64_t jit_pipe_warps(const JitModule* m, uint64_t n, int num_sms) {
+  const uint64_t ntiles = (n + m->tile - 1) / m->tile, cap = (uint64_t)num_sms * m->ctas;
+  return (ntiles < cap ? ntiles : cap) * (uint64_t)(m->threads / 32);
 }
 
 int jit_launch_count(const JitModule* m, uint64_t n) {

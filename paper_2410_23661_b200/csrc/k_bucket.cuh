@@ -51,6 +51,13 @@ constexpr bool kExtents = true;
 #else
 constexpr bool kExtents = false;
 #endif
+// ... or from K1's codes alone: the shapes are K1's, a window's extents are
+// evaluated (from the tables) only when no decisive record decides it.
+#ifdef PICKER_SEQ
+constexpr bool kSeqLazy = true;
+#else
+constexpr bool kSeqLazy = false;
+#endif
 
 // A specialised module without wide (K2) kernels is compiled with
 // PICKER_NO_WIDE: the warp-cooperative path is then dead code that would sit
@@ -472,20 +479,29 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
   // words stay in shared memory (same place as s_inb; the two modes are
   // exclusive), and the windows of tile t are decided in the emit slot of
   // t + 1, a warp per window (seq.cuh)
-  const bool seq_fused = kExtents && P.seq_out != nullptr;
+  const bool seq_fused = (kExtents || kSeqLazy) && P.seq_out != nullptr;
   int64_t* s_ext = reinterpret_cast<int64_t*>(
       ((uintptr_t)(reinterpret_cast<uint8_t*>(s_perm + kTile) + 2 * kTile) + 15) & ~(uintptr_t)15);
   uint32_t* s_xinfo = reinterpret_cast<uint32_t*>(s_ext + (size_t)kTile * 2 * P.xcap);
   auto windows = [&](uint64_t tbase, int m, uint32_t cbuf) {
-    if constexpr (kExtents) {
+    if constexpr (kExtents || kSeqLazy) {
       if (!seq_fused) return;
       const uint32_t W = P.seq_window, nwin = ((uint32_t)m + W - 1) / W;
       for (uint32_t w = warp; w < nwin; w += kWarps) {
         const uint32_t i0 = w * W;
-        const uint8_t code = seq_window_lanes(P.T, B, tbase + i0, min(W, (uint32_t)m - i0), P.seq_mode,
-                                              s_code + cbuf * kTile + i0, s_xinfo + i0,
-                                              s_ext + (size_t)i0 * 2 * P.xcap, P.xcap, lane);
-        if (lane == 0) P.seq_out[(tbase + i0) / W] = code;
+        bool undecided = false;
+        const uint8_t code =
+            kSeqLazy ? seq_window_lanes(P.T, B, tbase + i0, min(W, (uint32_t)m - i0), P.seq_mode,
+                                        s_code + cbuf * kTile + i0, nullptr,
+                                        P.seq_scratch + ((uint64_t)blockIdx.x * kWarps + warp) * 64 * P.xcap, P.xcap,
+                                        lane, &undecided)
+                     : seq_window_lanes(P.T, B, tbase + i0, min(W, (uint32_t)m - i0), P.seq_mode,
+                                        s_code + cbuf * kTile + i0, s_xinfo + i0,
+                                        s_ext + (size_t)i0 * 2 * P.xcap, P.xcap, lane, nullptr);
+        if (lane == 0) {
+          P.seq_out[(tbase + i0) / W] = code;
+          if (undecided && P.seq_undecided) atomicAdd(P.seq_undecided, 1u);
+        }
       }
     }
   };

@@ -39,6 +39,12 @@ struct Options {
   // extents module: extent slots per record held in shared memory for the
   // tile (0: the module writes them to the global arena only)
   int seq_xcap = 0;
+  // module variant deciding windows in its pipelined kernel from K1's codes,
+  // evaluating extents only for windows no decisive record decides (PICKER_SEQ)
+  bool seq_windows = false;
+  // picker_validate_sequence with that variant: 1 always, 0 never (extents
+  // module), -1 by the first call (lazy while <= 1/8 of its windows need extents)
+  int seq_lazy = -1;
   // summaries whose evaluating kernels are all wide: the K2 persistent kernel
   // (k_wide.cu; 1 on, 0 off = the module's schedules, -1 auto = on)
   int wide_kernel = -1;
@@ -80,6 +86,10 @@ bool jit_fused_models(const JitModule* m, uint64_t n);
 // the tile's extents in shared memory (Options.seq_xcap; window <= 32 dividing
 // the tile).
 bool jit_seq_fused(const JitModule* m, uint64_t n, uint32_t window);
+// A PICKER_SEQ module deciding windows of `window` launches for n records in
+// its pipelined kernel; jit_pipe_warps: warps of that kernel's grid.
+bool jit_seq_lazy(const JitModule* m, uint64_t n, uint32_t window);
+uint64_t jit_pipe_warps(const JitModule* m, uint64_t n, int num_sms);
 bool jit_extents_ok(const JitModule* m, uint64_t n);
 cudaError_t launch_jit(JitModule* m, const BucketParams& P, const DevBatch& B, uint64_t n, uint8_t* flags,
                        uint32_t* bits, unsigned long long* counts, int num_sms, cudaStream_t s);

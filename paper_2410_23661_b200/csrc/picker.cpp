@@ -37,6 +37,9 @@ struct picker_ctx {
   JitModule* jit_models = nullptr;   // the specialised module with row f3 fused (built on first use)
   JitModule* jit_extents = nullptr;  // ... writing K1's extents for row f1 (built on first use)
   void* seq_arena = nullptr;         // row f1: K1's verdicts, extent slots and info words
+  JitModule* jit_seq = nullptr;      // ... deciding windows from K1's codes (PICKER_SEQ, first use)
+  uint32_t* seq_undecided = nullptr;  // its count of windows that needed extents (first call)
+  int seq_lazy_state = -1;           // -1: not calibrated; 0: extents module; 1: PICKER_SEQ module
   size_t seq_arena_bytes = 0;
   cudaStream_t aux = nullptr;
   void* wide_scratch = nullptr;  // K2 sort scratch, kWideMax elements per warp of a grid
@@ -146,7 +149,9 @@ void picker_destroy(picker_ctx_t* c) {
     if (c->model_acc) cudaFree(c->model_acc);
     jit_destroy(c->jit_models);
     jit_destroy(c->jit_extents);
+    jit_destroy(c->jit_seq);
     if (c->seq_arena) cudaFree(c->seq_arena);
+    if (c->seq_undecided) cudaFree(c->seq_undecided);
     for (int i = 0; i < 2; ++i)
       if (c->stage[i]) cudaFree(c->stage[i]);
     if (c->dev_counts) cudaFree(c->dev_counts);
@@ -181,6 +186,7 @@ int picker_set_option(picker_ctx_t* c, const char* key, int64_t v) {
   else if (k == "sort_ws") c->opt.sort_ws = v < 0 ? -1 : (int)(v != 0);  // warp-specialised S4
   else if (k == "loop_min") c->opt.loop_min = (int)v;  // tuning: loop classes of the specialised module
   else if (k == "seq_k1") c->opt.seq_k1 = v != 0;  // row f1 on K1's extents (1, default) or the tables (0)
+  else if (k == "seq_lazy") c->opt.seq_lazy = v < 0 ? -1 : v != 0, c->seq_lazy_state = -1;
   else if (k == "wide_kernel") c->opt.wide_kernel = v < 0 ? -1 : (int)(v != 0);  // K2 kernel (k_wide.cu)
   else return fail(c, PICKER_EINVAL, "unknown option '" + k + "'");
   return PICKER_OK;
@@ -260,6 +266,9 @@ int picker_load_summaries(picker_ctx_t* c, const char* text, size_t len) {
   c->jit_models = nullptr;
   jit_destroy(c->jit_extents);
   c->jit_extents = nullptr;
+  jit_destroy(c->jit_seq);
+  c->jit_seq = nullptr;
+  c->seq_lazy_state = -1;
   c->jit = jm;
   c->dev_tables = dev;
   c->dev_tables_bytes = blob.size();
@@ -543,6 +552,61 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
   for (auto& k : c->ir) k1 &= k.path != PATH_WIDE && k.path != PATH_GENERIC;
   const size_t slot_b = (size_t)max_desc * 16, need = (size_t)n * (slot_b + 5) + 512;
   k1 &= need <= (8ull << 30);
+  // Windows of <= 32 launches from K1's codes (PICKER_SEQ): by Q23 a window
+  // with a decisive record is decided by its first one, whatever the
+  // addresses, so the extents are evaluated (from the tables, in the same
+  // kernel) only for the windows without one.  Calibrated on the first call:
+  // kept when at most 1/16 of its windows needed extents, else the extents
+  // module below (the same codes either way).  Measured on C2 x686, windows
+  // of 32, 20 % of them without a decisive record: lazy 2.25 ms, extents
+  // 1.10 ms (the table evaluation of an undecided window's 32 records sits
+  // between two tile barriers); K1 alone is 0.25 ms.
+  const int lazy = c->opt.seq_lazy >= 0 ? c->opt.seq_lazy : c->seq_lazy_state;
+  if (k1 && lazy != 0 && window <= 32) {
+    if (!c->jit_seq) {
+      Options mo = c->opt;
+      mo.seq_windows = true;
+      mo.sorted = 0;  // windows are decided in the pipelined kernel
+      c->jit_seq = jit_build(c->ir, mo, err);
+      if (!c->jit_seq) return fail(c, PICKER_ECUDA, "JIT (sequence): " + err);
+    }
+    if (jit_seq_lazy(c->jit_seq, n, window)) {
+      const uint64_t slice = 64ull * max_desc, need_s = jit_pipe_warps(c->jit_seq, n, c->num_sms) * slice * 8;
+      if (c->seq_scratch_bytes < need_s) {
+        cudaError_t e = cudaStreamSynchronize(s);  // a previous call may still use the old slices
+        if (c->seq_scratch) cudaFree(c->seq_scratch);
+        c->seq_scratch = nullptr;
+        c->seq_scratch_bytes = 0;
+        if (e != cudaSuccess || cudaMalloc(&c->seq_scratch, need_s) != cudaSuccess) {
+          c->seq_scratch = nullptr;
+          return fail(c, PICKER_ENOMEM, "cudaMalloc(window slots) failed");
+        }
+        c->seq_scratch_bytes = need_s;
+      }
+      const bool calibrate = lazy < 0;
+      if (calibrate && !c->seq_undecided && cudaMalloc(&c->seq_undecided, 4) != cudaSuccess) {
+        c->seq_undecided = nullptr;
+        return fail(c, PICKER_ENOMEM, "cudaMalloc(window count) failed");
+      }
+      BucketParams P = c->P;
+      P.xcap = max_desc;
+      P.seq_out = out, P.seq_window = window, P.seq_mode = mode;
+      P.seq_scratch = (int64_t*)c->seq_scratch;
+      P.seq_undecided = calibrate ? c->seq_undecided : nullptr;
+      cudaError_t e = calibrate ? cudaMemsetAsync(c->seq_undecided, 0, 4, s) : cudaSuccess;
+      if (e == cudaSuccess) e = launch_jit(c->jit_seq, P, db, n, nullptr, nullptr, nullptr, c->num_sms, s);
+      if (e == cudaSuccess && calibrate) {
+        uint32_t und = 0;
+        e = cudaMemcpyAsync(&und, c->seq_undecided, 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        const uint64_t nwin = (n + window - 1) / window;
+        if (e == cudaSuccess) c->seq_lazy_state = (uint64_t)und * 16 <= nwin ? 1 : 0;
+      }
+      if (e != cudaSuccess) return cuda_fail(c, e, "sequence (K1 codes)");
+      c->last_launches = 1;
+      return PICKER_OK;
+    }
+  }
   if (k1 && !c->jit_extents) {
     Options mo = c->opt;
     mo.extents = true;

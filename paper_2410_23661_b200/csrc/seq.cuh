@@ -256,77 +256,88 @@ __device__ uint8_t seq_window(const Tables& T, const DevBatch& B, uint64_t w0, u
   return V_IDEM_CHECKED;
 }
 
-// A window of <= 32 launches decided by one warp from extents already in
-// shared memory (the extents module's tile, k_bucket.cuh): lane i is launch
-// w0 + i, with its slot of xcap (lb, ub) pairs (reads from the front, writes
-// from the back) and info word.  Same decisions as seq_window (Q23): the first
-// decisive code; records K1 did not evaluate (1, kernel-level idempotent) are
-// evaluated from the tables into their own slot (they take part with their
-// writes); the opaque rule on ballots (sequential: an opaque read of i and a
-// write of j >= i is the lowest set bit of one ballot at or below the highest
-// of the other); then every (read of i, write of j) pair, i <= j sequential,
-// any i, j concurrent -- the writes of j broadcast from shared memory, each
-// lane's reads against them.
+// A window of <= 32 launches decided by one warp: lane i is launch w0 + i,
+// with its slot of xcap (lb, ub) pairs (reads from the front, writes from the
+// back) and info word.  Extents module (xinfo set): the slots are the tile's in
+// shared memory, filled by K1's shapes.  Lazy (xinfo null, `undecided` set):
+// the slots are the warp's scratch, filled from the tables only when no
+// decisive record decides the window.  Same decisions as seq_window (Q23): the
+// first decisive code; records K1 did not evaluate (1, kernel-level
+// idempotent) are evaluated from the tables into their own slot (they take
+// part with their writes; their checks may decide); the opaque rule on ballots
+// (sequential: an opaque read of i and a write of j >= i is the lowest set bit
+// of one ballot at or below the highest of the other); then every (read of i,
+// write of j) pair, i <= j sequential, any i, j concurrent -- the writes of j
+// broadcast, each lane's reads against them.
+__device__ __forceinline__ void seq_lane_tables(const Tables& T, const DevBatch& B, uint64_t rec, int64_t* x,
+                                                uint32_t xcap, uint32_t& status, uint32_t& info) {
+  const picker_rec_t r = load_rec(B.rec + rec);
+  const uint32_t kid = r.kernel_id;
+  do {
+    if (kid >= T.nkernel_slots || T.kernels[kid].shortcut == V_ERR_KERNEL) {
+      status = V_ERR_KERNEL;
+      break;
+    }
+    const DKernel K = T.kernels[kid];
+    if (!args_in_range(r, K.nparams, B.args_lo, B.args_hi)) {
+      status = V_ERR_ARITY;
+      break;
+    }
+    if (K.shortcut && K.shortcut != V_IDEM_KERNEL) {
+      status = K.shortcut;
+      break;
+    }
+    const RecVals X(r, B.args + r.arg_off, K.i32mask);
+    if (!launch_limits_ok(X)) {
+      status = V_NI_PRECOND;
+      break;
+    }
+    for (int q = 0; q < K.npre + K.nglob && status == kEvaluable; ++q) {
+      const DCheck ch = T.checks[K.check + q];
+      const int64_t v = X.get(ch.op);
+      if (v < ch.lo || v > ch.hi) status = q < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
+    }
+    if (status != kEvaluable) break;
+    uint32_t nr = 0, nw = 0, fl = 0;
+    for (int d = 0; d < K.ndesc; ++d) {
+      const DDesc D = T.descs[K.desc + d];
+      int64_t lb = 0, ub = 0;
+      if (!desc_active_extent(T, K, D, X, lb, ub)) continue;
+      fl |= D.kind == KIND_R ? 1u : 2u;
+      if (D.opaque) {
+        fl |= D.kind == KIND_R ? 4u : 8u;
+        continue;
+      }
+      const uint32_t k = D.kind == KIND_R ? nr++ : xcap - 1 - nw++;
+      x[2 * k] = lb, x[2 * k + 1] = ub;
+    }
+    info = nr | nw << 11 | fl << 22;
+  } while (false);
+}
+
 __device__ __forceinline__ uint8_t seq_window_lanes(const Tables& T, const DevBatch& B, uint64_t w0, uint32_t m,
-                                                    uint32_t mode, const uint8_t* codes, uint32_t* xinfo,
-                                                    int64_t* xext, uint32_t xcap, int lane) {
+                                                    uint32_t mode, const uint8_t* codes, const uint32_t* xinfo,
+                                                    int64_t* xext, uint32_t xcap, int lane, bool* undecided) {
   constexpr unsigned kAll = 0xffffffffu;
   const bool in = (uint32_t)lane < m;
-  uint32_t status = kEvaluable, info = 0;
+  uint32_t status = kEvaluable, info = 0, c = 0;
   int64_t* x = xext + (size_t)lane * 2 * xcap;
   if (in) {
-    const uint32_t c = codes[lane];
+    c = codes[lane];
     if (c >= V_NI_SO && c != V_NI_OPAQUE && c != V_NI_OVERLAP) {
       status = c;
-    } else if (c != V_IDEM_KERNEL) {
+    } else if (c == V_IDEM_KERNEL) {
+      seq_lane_tables(T, B, w0 + lane, x, xcap, status, info);
+    } else if (xinfo) {
       info = xinfo[lane];
-    } else {
-      const picker_rec_t r = load_rec(B.rec + w0 + lane);
-      const uint32_t kid = r.kernel_id;
-      do {
-        if (kid >= T.nkernel_slots || T.kernels[kid].shortcut == V_ERR_KERNEL) {
-          status = V_ERR_KERNEL;
-          break;
-        }
-        const DKernel K = T.kernels[kid];
-        if (!args_in_range(r, K.nparams, B.args_lo, B.args_hi)) {
-          status = V_ERR_ARITY;
-          break;
-        }
-        if (K.shortcut && K.shortcut != V_IDEM_KERNEL) {
-          status = K.shortcut;
-          break;
-        }
-        const RecVals X(r, B.args + r.arg_off, K.i32mask);
-        if (!launch_limits_ok(X)) {
-          status = V_NI_PRECOND;
-          break;
-        }
-        for (int q = 0; q < K.npre + K.nglob && status == kEvaluable; ++q) {
-          const DCheck ch = T.checks[K.check + q];
-          const int64_t v = X.get(ch.op);
-          if (v < ch.lo || v > ch.hi) status = q < K.npre ? V_NI_PRECOND : V_NI_GLOBAL;
-        }
-        if (status != kEvaluable) break;
-        uint32_t nr = 0, nw = 0, fl = 0;
-        for (int d = 0; d < K.ndesc; ++d) {
-          const DDesc D = T.descs[K.desc + d];
-          int64_t lb = 0, ub = 0;
-          if (!desc_active_extent(T, K, D, X, lb, ub)) continue;
-          fl |= D.kind == KIND_R ? 1u : 2u;
-          if (D.opaque) {
-            fl |= D.kind == KIND_R ? 4u : 8u;
-            continue;
-          }
-          const uint32_t k = D.kind == KIND_R ? nr++ : xcap - 1 - nw++;
-          x[2 * k] = lb, x[2 * k + 1] = ub;
-        }
-        info = nr | nw << 11 | fl << 22;
-      } while (false);
     }
   }
   const uint32_t first = __reduce_min_sync(kAll, (in && status != kEvaluable) ? ((uint32_t)lane << 8 | status) : kAll);
   if (first != kAll) return (uint8_t)(first & 0xFF);
+  if (!xinfo) {  // lazy: the records K1 passed to the address check (0, 9, 10), from the tables
+    *undecided = true;
+    if (in && c != V_IDEM_KERNEL) seq_lane_tables(T, B, w0 + lane, x, xcap, status, info);
+  }
   const uint32_t fl = info >> 22;
   const unsigned br = __ballot_sync(kAll, fl & 1), bw = __ballot_sync(kAll, fl & 2);
   const unsigned bor = __ballot_sync(kAll, fl & 4), bow = __ballot_sync(kAll, fl & 8);

@@ -242,6 +242,10 @@ struct BucketParams {
   // launches, mode 0 sequential / 1 concurrent; tiles are a multiple of it)
   uint8_t* seq_out;
   uint32_t seq_window, seq_mode;
+  // PICKER_SEQ: per-warp slot slices (32 x xcap (lb, ub)) for the windows no
+  // decisive record decides, and a count of those windows (or null)
+  int64_t* seq_scratch;
+  uint32_t* seq_undecided;
 };
 
 // Staged + bucketed kernel geometry (k_bucket.cuh): records per tile, threads

@@ -71,13 +71,19 @@ def main():
     n = rd.shape[0]
     base = 32 * n + 8 * int(ad.numel())
     # f1
-    for conc in ((False, True) if a.only in (None, "f1") else ()):
-        W = 32
-        ms = timed(lambda: p.validate_sequence(rd, ad, W, concurrent=conc), a.steps)
-        got = p.validate_sequence(rd[:len(rec)], ad, W, concurrent=conc).cpu().numpy()
-        want = np.array(O.oracle_windows(s, rec, args, W, O.SEQ_CONCURRENT if conc else O.SEQ_SEQUENTIAL), np.uint8)
-        row(f"f1_windows32_{'concurrent' if conc else 'sequential'}", n, base + (n + W - 1) // W, ms,
-            parity_mismatches=int((got != want).sum()), windows_checked=len(want))
+    # (default: windows from K1's codes, extents only where no decisive record
+    # decides, chosen by the first call; then always from K1's extents)
+    for lazy, tag in (((-1, ""), (1, "_lazy"), (0, "_extents")) if a.only in (None, "f1") else ()):
+        p.set_option("seq_lazy", lazy)
+        for conc in (False, True):
+            W = 32
+            ms = timed(lambda: p.validate_sequence(rd, ad, W, concurrent=conc), a.steps)
+            got = p.validate_sequence(rd[:len(rec)], ad, W, concurrent=conc).cpu().numpy()
+            want = np.array(O.oracle_windows(s, rec, args, W, O.SEQ_CONCURRENT if conc else O.SEQ_SEQUENTIAL),
+                            np.uint8)
+            row(f"f1_windows32_{'concurrent' if conc else 'sequential'}{tag}", n, base + (n + W - 1) // W, ms,
+                parity_mismatches=int((got != want).sum()), windows_checked=len(want))
+    p.set_option("seq_lazy", -1)
     if a.only == "f1":
         if a.out:
             json.dump(out, open(a.out, "w"), indent=1)

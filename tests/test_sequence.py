@@ -164,7 +164,7 @@ def test_gpu_sequence_golden_opaque(concurrent):
 @pytest.mark.gpu
 @pytest.mark.parametrize("window", [32, 1024])
 @pytest.mark.parametrize("concurrent", [False, True])
-@pytest.mark.parametrize("k1", [True, False], ids=["k1_extents", "tables"])
+@pytest.mark.parametrize("k1", ["lazy", "extents", "tables"])
 def test_gpu_sequence_c2(window, concurrent, k1):
     """The C2 trace (547 kernels) cut into windows of 32 / 1024 launches: every
     window's code against oracle_windows (sort + sweep passes vs the plain
@@ -176,12 +176,14 @@ def test_gpu_sequence_c2(window, concurrent, k1):
     s, rec, args, _ = workloads.make_c2()
     mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
     want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
-    p = pk.Picker(0, seq_k1=int(k1))
+    opts = {"lazy": dict(seq_lazy=1), "extents": dict(seq_lazy=0), "tables": dict(seq_k1=0)}[k1]
+    p = pk.Picker(0, **opts)
     p.load(s)
     got = p.validate_sequence(rec, args, window, concurrent=concurrent).cpu().numpy()
-    # windows of 32: decided inside the extents module's kernel (1 launch);
-    # of 1024: its extents arena, then the window kernel (2)
-    assert p.last_launch_count() == (2 if k1 and window > 32 else 1)
+    # windows of 32: decided inside K1's kernel (from its codes, or in the
+    # extents module from its extents: 1 launch); of 1024: the extents arena,
+    # then the window kernel (2)
+    assert p.last_launch_count() == (2 if k1 != "tables" and window > 32 else 1)
     bad = np.nonzero(got != want)[0]
     assert bad.size == 0, (bad[:8], got[bad[:8]], want[bad[:8]])
     assert len(set(want.tolist())) > 2
@@ -260,13 +262,16 @@ def test_gpu_sequence_k1_tiles(concurrent):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("concurrent", [False, True])
-def test_gpu_sequence_fused_steady(concurrent):
+@pytest.mark.parametrize("lazy", [1, 0, -1], ids=["lazy", "extents", "auto"])
+def test_gpu_sequence_fused_steady(concurrent, lazy):
     """Windows decided inside the extents module's pipelined kernel, at its
     steady state (C2 cut to a multiple of 32 records, x 24: ~3 tiles per CTA, so
     windows of tile t run while tile t + 1 is staged and sorted): one launch,
     every window equal to the oracle's windows of the base trace, tiled (the
     copies are the base instances relocated); then windows of 8
-    and 16, and a ragged last window."""
+    and 16, and a ragged last window.  Lazy: from K1's codes, extents only for
+    the windows without a decisive record; extents: K1's extents in shared
+    memory; auto: chosen by the first call."""
     import paper_2410_23661_b200 as pk
     from tracegen import workloads
     s, rec, args, meta = workloads.make_c2()
@@ -274,7 +279,7 @@ def test_gpu_sequence_fused_steady(concurrent):
     rec = rec[: len(rec) // 32 * 32]
     R = 24
     rec_t, args_t = workloads.replicate(rec, args, meta["ptr_mask"], R)
-    p = pk.Picker(0)
+    p = pk.Picker(0, seq_lazy=lazy)
     p.load(s)
     for window in (32, 16, 8):
         want = np.array(O.oracle_windows(s, rec, args, window, mode), np.uint8)
@@ -286,3 +291,30 @@ def test_gpu_sequence_fused_steady(concurrent):
     want = np.array(O.oracle_windows(s, rec[:m], args, 32, mode), np.uint8)
     got = p.validate_sequence(rec[:m], args, 32, concurrent=concurrent).cpu().numpy()
     assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("lazy", [1, -1], ids=["lazy", "auto"])
+def test_gpu_sequence_undecided(lazy):
+    """Windows no decisive record decides (the C2 records K1 passes to the
+    address check, codes 0 / 9 / 10, x 8): every window's extents evaluated --
+    lazily from the tables, or, after the first call finds most windows
+    undecided, by the extents module -- against the oracle, both modes."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, meta = workloads.make_c2()
+    codes = np.array(O.oracle_batch(s, rec, args), np.uint8)
+    sub = rec[np.isin(codes, [0, 9, 10])]
+    sub = sub[: len(sub) // 32 * 32]
+    R = 8
+    rec_t, args_t = workloads.replicate(sub, args, meta["ptr_mask"], R)
+    p = pk.Picker(0, seq_lazy=lazy)
+    p.load(s)
+    for concurrent in (False, True, False):
+        mode = O.SEQ_CONCURRENT if concurrent else O.SEQ_SEQUENTIAL
+        want = np.tile(np.array(O.oracle_windows(s, sub, args, 32, mode), np.uint8), R)
+        got = p.validate_sequence(rec_t, args_t, 32, concurrent=concurrent).cpu().numpy()
+        assert p.last_launch_count() == 1
+        bad = np.nonzero(got != want)[0]
+        assert bad.size == 0, (concurrent, bad[:8], got[bad[:8]])
+        assert (want == 0).sum() > 0 and (want == 10).sum() > 0
