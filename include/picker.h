@@ -29,6 +29,9 @@
  *     summary tables and scratch until picker_destroy.
  *   - Thread safety: one context per host thread.  Loaded tables are immutable
  *     until the next picker_load_summaries on the same context.
+ *   - A context's scratch is shared by its calls and regrown on demand after
+ *     synchronising the CALLING stream only: calls of one context on several
+ *     streams must be ordered by the caller (events), or use one stream.
  */
 #ifndef PICKER_H_
 #define PICKER_H_
@@ -214,11 +217,15 @@ int picker_replicate(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
  * first record whose own check is decided before any address (0xFF, 0xFE, 2-8;
  * kernel-level idempotent instances take part with their writes) decides the
  * window; then the opaque rule (9); then the overlap (10); else 0.
- * Decided by sort + sweep passes over the window's extents (k_seq.cu):
- * concurrent, one pass; sequential, a divide and conquer over launch order.
- * out[ceil(n/window)] is a device pointer.  PICKER_EINVAL when window x (the
- * most descriptors of a loaded kernel) exceeds 2^24.  Asynchronous on
- * `stream`.                                                                    */
+ * Windows of <= 32 launches dividing the specialised kernel's tile (n > 1,024,
+ * specialised kernels only): decided inside K1's pipelined kernel, one warp
+ * per window (seq.cuh; option "seq_lazy").  Otherwise: K1's extents to a
+ * global arena, then sort + sweep passes over each window's extents
+ * (k_seq.cu): concurrent, one pass; sequential, a divide and conquer over
+ * launch order.  out[ceil(n/window)] is a device pointer.  PICKER_EINVAL when
+ * window x (the most descriptors of a loaded kernel) exceeds 2^24.
+ * Asynchronous on `stream` (the context's first call of the in-kernel path
+ * synchronises it once, see "seq_lazy").                                       */
 int picker_validate_sequence(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n,
                              uint32_t window, uint32_t mode, uint8_t* out, void* stream);
 
