@@ -77,6 +77,10 @@ static __device__ __noinline__ bool may_collide(int64_t lb_r, uint64_t g_r, uint
                                                    uint64_t g_w, uint32_t w_w) {
   const uint64_t G = gcd64(g_r, g_w);
   if (G == 0) return true;  // two single addresses: the interval test is exact
+  if ((G & (G - 1)) == 0) {  // power of two (element strides): residues by masks, no 64-bit division
+    const uint64_t M = G - 1, d = ((uint64_t)lb_w - (uint64_t)lb_r) & M;
+    return ((d + (w_w - 1)) & M) <= (uint64_t)w_r + w_w - 2;
+  }
   const uint64_t pr = mod64(lb_r, G), pw = mod64(lb_w, G);
   const uint64_t d = pw >= pr ? pw - pr : pw + (G - pr);  // (lb_w - lb_r) mod G
   const uint64_t t = (d + (w_w - 1)) % G;

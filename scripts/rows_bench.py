@@ -52,7 +52,7 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--opt", action="append", default=[], help="library option key=value for the C2 rows (tuning)")
-    ap.add_argument("--only", default=None, help="f1 / f3: only those rows")
+    ap.add_argument("--only", default=None, help="f1 / f3 / f4: only those rows")
     a = ap.parse_args()
     peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6554.6))
     dev = torch.device("cuda", 0)
@@ -84,7 +84,22 @@ def main():
             row(f"f1_windows32_{'concurrent' if conc else 'sequential'}{tag}", n, base + (n + W - 1) // W, ms,
                 parity_mismatches=int((got != want).sum()), windows_checked=len(want))
     p.set_option("seq_lazy", -1)
-    if a.only == "f1":
+    def run_f4():
+        # f4: the stride-aware specialised module
+        ps = pk.Picker(0, stride=1)
+        ps.load(s)
+        fl = torch.empty(n, dtype=torch.uint8, device=dev)
+        bt = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
+        ct = torch.empty(16, dtype=torch.int64, device=dev)
+        ms = timed(lambda: ps.validate(rd, ad, out=(fl, bt, ct)), a.steps)
+        got = fl[:len(rec)].cpu().numpy()
+        want = np.array(O.oracle_batch_mp(s, rec, args, stride=True), np.uint8)
+        row("f4_stride_aware", n, base + n + n / 8, ms, parity_mismatches=int((got != want).sum()))
+        ps.close()
+
+    if a.only in ("f1", "f4"):
+        if a.only == "f4":
+            run_f4()
         if a.out:
             json.dump(out, open(a.out, "w"), indent=1)
         return
@@ -107,17 +122,7 @@ def main():
         if a.out:
             json.dump(out, open(a.out, "w"), indent=1)
         return
-    # f4: the stride-aware specialised module
-    ps = pk.Picker(0, stride=1)
-    ps.load(s)
-    fl = torch.empty(n, dtype=torch.uint8, device=dev)
-    bt = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
-    ct = torch.empty(16, dtype=torch.int64, device=dev)
-    ms = timed(lambda: ps.validate(rd, ad, out=(fl, bt, ct)), a.steps)
-    got = fl[:len(rec)].cpu().numpy()
-    want = np.array(O.oracle_batch_mp(s, rec, args, stride=True), np.uint8)
-    row("f4_stride_aware", n, base + n + n / 8, ms, parity_mismatches=int((got != want).sum()))
-    ps.close()
+    run_f4()
     # K3 exact verifier
     s3, r3, a3, m3 = workloads.make_c3(seed=23664, n=4096, n_kernels=32, small=True)
     p3 = pk.Picker(0)
