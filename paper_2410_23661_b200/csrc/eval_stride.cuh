@@ -36,6 +36,16 @@ static __device__ __noinline__ uint64_t gcd64(uint64_t a, uint64_t b) {
   return a << sh;
 }
 
+// gcd64 with the common cases inline (a zero, or two powers of two: element
+// strides), so that the shapes make no call -- a call spills the caller's live
+// registers around it
+static __device__ __forceinline__ uint64_t gcd64f(uint64_t a, uint64_t b) {
+  if (a == 0) return b;
+  if (b == 0) return a;
+  if (((a & (a - 1)) | (b & (b - 1))) == 0) return a < b ? a : b;
+  return gcd64(a, b);
+}
+
 static __device__ __forceinline__ uint64_t uabs64(int64_t x) {
   return x < 0 ? (uint64_t)0 - (uint64_t)x : (uint64_t)x;
 }
@@ -67,7 +77,7 @@ static __device__ uint64_t desc_stride(const Tables& T, const DKernel& K, const 
     int64_t lo, hi;
     slot_bounds(T, K, X, tm.var, lo, hi);
     if (floordiv64(lo, tm.div) == floordiv64(hi, tm.div)) continue;  // constant on the box
-    g = gcd64(g, uabs64(c));
+    g = gcd64f(g, uabs64(c));
   }
   return g;
 }
@@ -75,7 +85,7 @@ static __device__ uint64_t desc_stride(const Tables& T, const DKernel& K, const 
 // can the two congruence classes share a byte (intervals already intersect)?
 static __device__ __noinline__ bool may_collide(int64_t lb_r, uint64_t g_r, uint32_t w_r, int64_t lb_w,
                                                    uint64_t g_w, uint32_t w_w) {
-  const uint64_t G = gcd64(g_r, g_w);
+  const uint64_t G = gcd64f(g_r, g_w);
   if (G == 0) return true;  // two single addresses: the interval test is exact
   if ((G & (G - 1)) == 0) {  // power of two (element strides): residues by masks, no 64-bit division
     const uint64_t M = G - 1, d = ((uint64_t)lb_w - (uint64_t)lb_r) & M;

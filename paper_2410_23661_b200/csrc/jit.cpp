@@ -316,7 +316,7 @@ std::string gen_body(const IrKernel& k, std::vector<int64_t>& K, bool stride, st
         const std::string vary = dv == 1 ? L + " != " + H
                                          : "floordiv64(" + L + ", " + std::to_string(dv) + "u) != floordiv64(" + H +
                                                ", " + std::to_string(dv) + "u)";
-        s << ind << "  if (" << vary << ") gg = gcd64(gg, uabs64(" << e.second << "));\n";
+        s << ind << "  if (" << vary << ") gg = gcd64f(gg, uabs64(" << e.second << "));\n";
       }
       s << ind << "  return gg;\n" << ind << "};\n";
       s << ind << "const uint32_t W" << di << " = (uint32_t)" << g.k((int64_t)d.width) << ";\n";
