@@ -567,6 +567,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       }
       key[q] = kb >> 16;
       rb[q] = (uint32_t)i | (kb & 0xFFFFu) << 16;
+      // models: the context sizes the emit of this tile reads (an iteration
+      // from now, right after a barrier) are fetched into L2 here, so that
+      // load does not expose an HBM round trip between two barriers
+      if constexpr (kModels)
+        if (P.ctx_bytes != nullptr && (lane & 15) == 0 && i < m)
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(P.ctx_bytes + base + i));
     }
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
