@@ -616,9 +616,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm)
       if (valid && (__ffs(same) - 1) == lane) atomicAdd(s_hist + hb, (uint32_t)__popc(same));
       if constexpr (kModels)
         if (valid) {
+          // (the input bytes are the record's own, whatever its verdict; the
+          // verdict the models take is the kernel's or the caller's)
           const uint64_t inb = s_inb[buf * kTile + i];
-          model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, c, inb != kInbUnknown, inb,
-                    P.ctx_bytes ? P.ctx_bytes[base + i] : 0, P.kill_ns, P.save_bpu);
+          model_add(ms, s_mh, s_mh + PICKER_MODEL_HIST, P.given_codes ? P.given_codes[base + i] : c,
+                    inb != kInbUnknown, inb, P.ctx_bytes ? P.ctx_bytes[base + i] : 0, P.kill_ns, P.save_bpu);
         }
     }
   };

@@ -686,8 +686,37 @@ int picker_consumer_models(picker_ctx_t* c, const picker_batch_t* b, uint64_t n,
     return fail(c, PICKER_EINVAL, "params/out must be non-null and save_bytes_per_us > 0");
   DevGuard g(c->device);
   DevBatch db{b->rec, b->args, 0, b->args_len};
+  cudaStream_t s = (cudaStream_t)stream;
+  // The models module's pipelined kernel on the caller's verdicts: its shapes
+  // sum each record's read-extent union (the input bytes do not depend on the
+  // verdict), the emit adds the models with codes[i]; its own verdicts are not
+  // written.  Same eligibility as picker_validate_models' fused pass.
+  bool fused = c->jit && !c->opt.stride && n > kSmallMax;
+  for (auto& k : c->ir) fused &= k.path != PATH_WIDE && k.path != PATH_GENERIC;
+  if (fused && !c->jit_models) {
+    Options mo = c->opt;
+    mo.models = true;
+    mo.sorted = 0;
+    std::string err;
+    c->jit_models = jit_build(c->ir, mo, err);
+    if (!c->jit_models) return fail(c, PICKER_ECUDA, "JIT (models): " + err);
+  }
+  if (fused && jit_fused_models(c->jit_models, n)) {
+    BucketParams P = c->P;
+    P.ctx_bytes = ctx_bytes;
+    P.given_codes = codes;
+    P.kill_ns = prm->kill_ns;
+    P.save_bpu = ModelDiv::of(prm->save_bytes_per_us);
+    cudaError_t e = model_acc_begin(&c->model_acc, s);
+    P.model_acc = (ModelAcc*)c->model_acc;
+    if (e == cudaSuccess) e = launch_jit(c->jit_models, P, db, n, nullptr, nullptr, nullptr, c->num_sms, s);
+    if (e == cudaSuccess) e = model_acc_end(c->model_acc, n, out, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "consumer models (fused)");
+    c->last_launches = 1;
+    return PICKER_OK;
+  }
   cudaError_t e = launch_models(c->P.T, db, n, codes, ctx_bytes, prm->kill_ns, prm->save_bytes_per_us, out,
-                                &c->model_acc, c->num_sms, (cudaStream_t)stream);
+                                &c->model_acc, c->num_sms, s);
   if (e != cudaSuccess) return cuda_fail(c, e, "consumer models");
   c->last_launches = n ? 1 : 0;
   return PICKER_OK;

@@ -229,6 +229,7 @@ struct BucketParams {
   CountSlot* count_slot;       // this launch's histogram slot (flush_counts); nullptr: accumulate
   // row f3 fused into the pipelined kernel (module built with PICKER_MODELS)
   const uint64_t* ctx_bytes;   // per record, or nullptr (0)
+  const uint8_t* given_codes;  // models on these verdicts (picker_consumer_models), or nullptr: the kernel's own
   unsigned long long kill_ns;
   ModelDiv save_bpu;           // divisor of the context-save latency (save_bytes_per_us)
   ModelAcc* model_acc;

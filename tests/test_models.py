@@ -199,6 +199,24 @@ def test_gpu_validate_models_c2_fused():
 
 
 @pytest.mark.gpu
+def test_gpu_models_given_codes_c2():
+    """picker_consumer_models through the models module's kernel (1 launch):
+    the models take the CALLER's verdicts, not the kernel's own -- C2 with the
+    oracle's codes rotated by 7 records (every record paired with another
+    record's verdict) against oracle_models on the same rotated codes."""
+    import paper_2410_23661_b200 as pk
+    from tracegen import workloads
+    s, rec, args, _ = workloads.make_c2()
+    codes = np.roll(np.array(O.oracle_batch_mp(s, rec, args), np.uint8), 7)
+    ctx = np.random.default_rng(11).integers(0, 150_000, len(rec)).astype(np.uint64)
+    p = pk.Picker(0)
+    p.load(s)
+    got = p.consumer_models(rec, args, codes, ctx, kill_ns=900, save_bytes_per_us=2500)
+    assert p.last_launch_count() == 1
+    assert got == O.oracle_models(s, rec, args, codes, ctx, kill_ns=900, save_bytes_per_us=2500)
+
+
+@pytest.mark.gpu
 def test_gpu_validate_models_c2heavy():
     """C2-heavy: fused kernels with up to 29 reads (more than the 12 a
     specialised shape sums itself: those records take the table path inside
