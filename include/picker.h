@@ -258,7 +258,10 @@ typedef struct {
  *   Chimera (l.1666-1690): latency = kill_ns if the record's code is 0 or 1,
  *   else ctx_bytes[i] * 1000 / save_bytes_per_us ns (ctx_bytes < 2^54).
  * codes: device u8[n] (e.g. picker_validate_batch's flags); ctx_bytes: device
- * u64[n] or NULL (all 0); out: HOST struct.  SYNCHRONOUS on `stream`.         */
+ * u64[n] or NULL (all 0); out: HOST struct.  SYNCHRONOUS on `stream`.
+ * Summaries of specialised kernels only, n > 1,024: one launch of the models
+ * module's validation kernel (its shapes sum the read-extent unions) with
+ * `codes` in place of its own verdicts; otherwise a table-driven pass.       */
 int picker_consumer_models(picker_ctx_t* ctx, const picker_batch_t* batch, uint64_t n, const uint8_t* codes,
                            const uint64_t* ctx_bytes, const picker_model_params_t* params,
                            picker_model_out_t* out, void* stream);
