@@ -570,8 +570,8 @@ int picker_validate_sequence(picker_ctx_t* c, const picker_batch_t* b, uint64_t 
       c->jit_seq = jit_build(c->ir, mo, err);
       if (!c->jit_seq) return fail(c, PICKER_ECUDA, "JIT (sequence): " + err);
     }
-    if (jit_seq_lazy(c->jit_seq, n, window)) {
-      const uint64_t slice = 64ull * max_desc, need_s = jit_pipe_warps(c->jit_seq, n, c->num_sms) * slice * 8;
+    const uint64_t slice = 64ull * max_desc, need_s = jit_pipe_warps(c->jit_seq, n, c->num_sms) * slice * 8;
+    if (jit_seq_lazy(c->jit_seq, n, window) && need_s <= (1ull << 30)) {  // slot slices <= 1 GB
       if (c->seq_scratch_bytes < need_s) {
         cudaError_t e = cudaStreamSynchronize(s);  // a previous call may still use the old slices
         if (c->seq_scratch) cudaFree(c->seq_scratch);
