@@ -324,14 +324,14 @@ __device__ __forceinline__ uint8_t seq_window_lanes(const Tables& T, const DevBa
   int64_t* x = xext + (size_t)lane * 2 * xcap;
   if (in) {
     c = codes[lane];
-    if (c >= V_NI_SO && c != V_NI_OPAQUE && c != V_NI_OVERLAP) {
-      status = c;
-    } else if (c == V_IDEM_KERNEL) {
-      seq_lane_tables(T, B, w0 + lane, x, xcap, status, info);
-    } else if (xinfo) {
-      info = xinfo[lane];
-    }
+    if (c >= V_NI_SO && c != V_NI_OPAQUE && c != V_NI_OVERLAP) status = c;
+    else if (c != V_IDEM_KERNEL && xinfo) info = xinfo[lane];
   }
+  // records before the first decisive one that K1 did not evaluate (1): their
+  // checks may decide earlier, and they take part with their writes -- only
+  // those are evaluated from the tables (all of them in an undecided window)
+  const uint32_t first0 = __reduce_min_sync(kAll, (in && status != kEvaluable) ? ((uint32_t)lane << 8 | status) : kAll);
+  if (in && c == V_IDEM_KERNEL && (uint32_t)lane < (first0 >> 8)) seq_lane_tables(T, B, w0 + lane, x, xcap, status, info);
   const uint32_t first = __reduce_min_sync(kAll, (in && status != kEvaluable) ? ((uint32_t)lane << 8 | status) : kAll);
   if (first != kAll) return (uint8_t)(first & 0xFF);
   if (!xinfo) {  // lazy: the records K1 passed to the address check (0, 9, 10), from the tables
